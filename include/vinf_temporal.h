@@ -1,0 +1,252 @@
+/* vinf_temporal.h — C ABI of the B200 (sm_100a) clip-parallel dual-scope temporal block.
+ *
+ * Drop-in boundary for the reference's temporal-module API. The reference exposes
+ * this path only as a C++ API in namespace vinf (/root/reference/proj/src/core/
+ * ops.hpp:49-124, clip_parallel.hpp:14-84); its only C ABI (include/vinf.h:27-75) is
+ * run-level. Every entry point below names the reference function it replaces.
+ *
+ * Conventions (mirroring include/vinf.h:1-28 of the reference):
+ *   - every function returns a status code; on failure vinf_last_error() holds a
+ *     thread-local message valid until the next failing call on the same thread;
+ *   - tensors are caller-owned DEVICE buffers in the reference layout [F,H,W,C],
+ *     row-major, channels innermost (tensor.hpp:13-24); conv weights [tap][out][in],
+ *     projections [out][in] (ops.hpp:11-12); fp32 weights are uploaded once into
+ *     parameter handles;
+ *   - work is enqueued on the given CUDA stream (cudaStream_t passed as void*);
+ *     functions never synchronise the stream unless stated;
+ *   - validation happens before any work, as ops.cpp:10-38 does.
+ */
+#ifndef VINF_TEMPORAL_H
+#define VINF_TEMPORAL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: identical values to the reference's vinf.h:18-25. */
+enum {
+    VINF_OK = 0,
+    VINF_ERR = 1,           /* unclassified failure (CUDA errors land here) */
+    VINF_ERR_CONFIG = 2,    /* ConfigError: bad taps/groups/halo/plan */
+    VINF_ERR_TRANSPORT = 3, /* TransportError / ProtocolError: context size mismatch */
+    VINF_ERR_IO = 4,
+    VINF_ERR_INVALID = 5,   /* ShapeError / RangeError: bad argument, shape or range */
+};
+
+/* Activation storage / arithmetic mode.
+ * VINF_F32:  fp32 activations; GEMMs run on tcgen05 as split-bf16 ("bf16x3":
+ *            hi*hi + hi*lo + lo*hi, fp32 accumulate); parity bar 1e-4 normwise.
+ * VINF_BF16: bf16 activations, bf16 tcgen05 GEMMs, fp32 accumulate/statistics;
+ *            parity bar 2e-2 normwise. */
+typedef enum { VINF_F32 = 0, VINF_BF16 = 1 } vinf_dtype;
+
+typedef struct {
+    void* data;          /* device pointer */
+    uint32_t f, h, w, c; /* frames, height, width, channels */
+    vinf_dtype dtype;
+} vinf_tensor;
+
+const char* vinf_version(void);
+const char* vinf_last_error(void);
+/* 1 when a CUDA device of compute capability 10.0 is usable, else 0. */
+int vinf_device_ok(void);
+
+/* ---- token sets and clip plan (integer-exact host functions) ----------------
+ * ops.cpp:177-198, clip_parallel.cpp:54-91, 343-387. `*count` receives the number
+ * of entries; `cap` is the capacity of `out`. */
+int vinf_build_local_window(uint32_t a, uint32_t frames, uint32_t n_local, uint32_t* out,
+                            uint32_t cap, uint32_t* count);
+int vinf_build_global_index_set(uint32_t frames, uint32_t n_global, uint32_t* out, uint32_t cap,
+                                uint32_t* count);
+int vinf_make_plan(uint32_t frames, uint32_t workers, uint32_t* f_clip);
+int vinf_global_members_in_range(uint32_t frames, uint32_t n_global, uint32_t start,
+                                 uint32_t len, uint32_t* out, uint32_t cap, uint32_t* count);
+/* out[3] = {bytes_sent, bytes_contributed, messages} (TrafficPrediction). */
+int vinf_predict_sync_traffic(uint32_t frames, uint32_t workers, uint32_t halo,
+                              uint32_t global_frames, uint32_t worker, uint64_t frame_bytes,
+                              uint64_t* out3);
+int vinf_predict_groupnorm_traffic(uint32_t frames, uint32_t workers, uint32_t groups,
+                                   uint32_t worker, uint64_t* out3);
+
+/* ---- synthetic inputs and random-init weights (bit-exact on device) ----------
+ * tensor_from_seed_at (tensor.cpp:98-106) and draw() (pipeline.cpp:26-31):
+ * dst[i] = unit(seed, first_elem + i) * scale, rounded to dtype. */
+int vinf_fill_seeded(void* dst, vinf_dtype dtype, uint64_t n, uint64_t seed, uint64_t first_elem,
+                     float scale, void* stream);
+uint64_t vinf_mix_seed(uint64_t seed, uint64_t salt); /* rng.hpp:34-37 */
+
+/* ---- parameter handles ------------------------------------------------------- */
+/* ConvKernel (ops.hpp:14-21). weights: taps*C*C fp32, bias: C fp32, both DEVICE. */
+typedef struct vinf_conv_kernel vinf_conv_kernel;
+int vinf_conv_kernel_create(uint32_t taps, uint32_t channels, const float* weights,
+                            const float* bias, vinf_conv_kernel** out);
+void vinf_conv_kernel_destroy(vinf_conv_kernel* k);
+
+/* AttentionParams (ops.hpp:32-36) + a heads extension (heads == 1 is the
+ * reference: head dim == C). wq/wk/wv/wo: C*C fp32 DEVICE. */
+typedef struct vinf_attention_params vinf_attention_params;
+int vinf_attention_params_create(uint32_t dim, uint32_t heads, float scale, const float* wq,
+                                 const float* wk, const float* wv, const float* wo,
+                                 vinf_attention_params** out);
+void vinf_attention_params_destroy(vinf_attention_params* p);
+
+/* GroupNormParams (ops.hpp:23-30); gamma/beta are C fp32 DEVICE pointers. */
+typedef struct {
+    uint32_t groups;
+    const float* gamma;
+    const float* beta;
+    float epsilon;
+} vinf_group_norm_params;
+
+/* DualScopeConfig (ops.hpp:38-43). */
+typedef struct {
+    uint32_t n_local;
+    uint32_t n_global;
+    float bias;
+    double t_star;
+} vinf_dual_scope_config;
+
+/* ---- operators (reference single-process forms) ------------------------------ */
+/* spatial_affine_tanh (ops.cpp:42-55); a, c: C fp32 device. */
+int vinf_spatial_affine_tanh(const vinf_tensor* v, const float* a, const float* c,
+                             vinf_tensor* out, void* stream);
+/* conv_over_extended (ops.cpp:73-104): out frames [out_start, out_start+out_len) of ext;
+ * frames outside [0, ext.f) are zeros. out: [out_len,H,W,C]. */
+int vinf_conv_over_extended(const vinf_tensor* ext, uint32_t out_start, uint32_t out_len,
+                            const vinf_conv_kernel* k, vinf_tensor* out, void* stream);
+/* temporal_conv (ops.cpp:106-108) */
+int vinf_temporal_conv(const vinf_tensor* v, const vinf_conv_kernel* k, vinf_tensor* out,
+                       void* stream);
+/* group_means / group_sqdev (ops.cpp:112-142): f64 DEVICE outputs [groups]. */
+int vinf_group_means(const vinf_tensor* v, uint32_t groups, double* means, void* stream);
+int vinf_group_sqdev(const vinf_tensor* v, uint32_t groups, const double* means, double* vars,
+                     void* stream);
+/* Partial sums for the distributed form: sums[g] = sum x (center == NULL) or
+ * sum (x - center[g])^2 over this clip. f64 DEVICE. */
+int vinf_group_partial_sums(const vinf_tensor* v, uint32_t groups, const double* center,
+                            double* sums, void* stream);
+/* normalize_with_stats (ops.cpp:144-167); means/vars f64 DEVICE. */
+int vinf_normalize_with_stats(const vinf_tensor* v, const vinf_group_norm_params* p,
+                              const double* means, const double* vars, vinf_tensor* out,
+                              void* stream);
+/* group_norm (ops.cpp:169-173) */
+int vinf_group_norm(const vinf_tensor* v, const vinf_group_norm_params* p, vinf_tensor* out,
+                    void* stream);
+/* dual_scope_reference (ops.cpp:291-338); attention_full (ops.cpp:264-289). */
+int vinf_dual_scope_attention(const vinf_tensor* v, double t, const vinf_attention_params* p,
+                              const vinf_dual_scope_config* cfg, vinf_tensor* out, void* stream);
+int vinf_attention_full(const vinf_tensor* v, const vinf_attention_params* p, vinf_tensor* out,
+                        void* stream);
+
+/* ---- distributed operator forms (clip_parallel.cpp:194-341) -------------------
+ * ctx_pre / ctx_post: the neighbours' boundary frames (NULL or f == 0 at the video
+ * edge); ctx_global: the n_global gathered frames in global-index order. Context
+ * sizes are checked exactly as the reference does (ProtocolError ->
+ * VINF_ERR_TRANSPORT). */
+int vinf_conv_parallel(uint32_t frames, uint32_t workers, uint32_t worker, const vinf_tensor* v,
+                       const vinf_tensor* ctx_pre, const vinf_tensor* ctx_post,
+                       const vinf_conv_kernel* k, vinf_tensor* out, void* stream);
+int vinf_attention_parallel(uint32_t frames, uint32_t workers, uint32_t worker,
+                            const vinf_tensor* v, const vinf_tensor* ctx_pre,
+                            const vinf_tensor* ctx_post, const vinf_tensor* ctx_global, double t,
+                            const vinf_attention_params* p, const vinf_dual_scope_config* cfg,
+                            vinf_tensor* out, void* stream);
+
+/* ---- clip engine: the fused, preallocated block stack of one worker -----------
+ * eps_theta_worker (pipeline.cpp:145-172) for `blocks` blocks on one clip, with all
+ * buffers (halo slots, global slots, Q/K/V, statistics) carved from ONE caller-owned
+ * device workspace. Cross-worker context moves (the paper's 3-step sync) are exposed
+ * as exchange lists of (peer, direction, workspace offset, bytes) so the caller's
+ * transport (NCCL via torch.distributed, or in-process copies) executes them between
+ * stages; with one worker every list is empty and vinf_engine_forward runs the whole
+ * stack in one call. */
+typedef struct {
+    uint32_t frames, workers, worker;
+    uint32_t height, width, channels;
+    uint32_t taps, groups, heads;
+    uint32_t n_local, n_global;
+    float bias;
+    double t_star;
+    float epsilon;
+    float scale;        /* 0 -> 1/sqrtf(C/heads) */
+    uint32_t blocks;
+    vinf_dtype dtype;
+} vinf_engine_desc;
+
+typedef struct vinf_layout vinf_layout;
+/* Pure host: buffer layout + exchange plan. No CUDA calls (usable on CPU hosts). */
+int vinf_layout_create(const vinf_engine_desc* d, vinf_layout** out);
+void vinf_layout_destroy(vinf_layout* l);
+int vinf_layout_workspace_bytes(const vinf_layout* l, uint64_t* bytes);
+
+/* Named regions of the workspace (for the caller's views / tests). */
+enum {
+    VINF_BUF_X = 0,      /* block input  [f_clip,H,W,C] dtype */
+    VINF_BUF_Y = 1,      /* block output [f_clip,H,W,C] dtype */
+    VINF_BUF_CONV_IN = 2,/* conv operand, frames [hc | f_clip | hc] (bf16 plane / hi plane) */
+    VINF_BUF_ATTN_IN = 3,/* attention operand, frames [ha | f_clip | ha | remote globals] */
+    VINF_BUF_GN_SUMS = 4 /* f64 [2][groups] */
+};
+int vinf_layout_region(const vinf_layout* l, int which, uint64_t* offset, uint64_t* bytes,
+                       uint64_t* frame_bytes);
+
+/* Exchange stages. */
+enum { VINF_XCHG_CONV = 0, VINF_XCHG_ATTN = 1 };
+typedef struct {
+    uint32_t peer;
+    uint32_t send;      /* 1 = send to peer, 0 = receive from peer */
+    uint32_t tag;       /* matching key: identical on both ends of one message */
+    uint32_t reserved;
+    uint64_t offset;    /* workspace byte offset */
+    uint64_t bytes;
+} vinf_xfer;
+/* Transfers of one exchange stage in a deadlock-free order (every send has exactly one
+ * matching receive with the same tag on the peer). */
+int vinf_layout_exchange(const vinf_layout* l, int stage, vinf_xfer* out, uint32_t cap,
+                         uint32_t* count);
+/* Logical bytes the reference's sync would move for this worker per block
+ * (predict_sync_traffic for conv + attention, predict_groupnorm_traffic). */
+int vinf_layout_reference_traffic(const vinf_layout* l, uint64_t* conv3, uint64_t* gn3,
+                                  uint64_t* attn3);
+
+typedef struct vinf_engine vinf_engine;
+/* workspace: DEVICE buffer of vinf_layout_workspace_bytes bytes (zeroed by create). */
+int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf_engine** out);
+void vinf_engine_destroy(vinf_engine* e);
+/* Block b's weights from fp32 DEVICE buffers in the reference layout. */
+int vinf_engine_set_block(vinf_engine* e, uint32_t block, const float* stub_a,
+                          const float* stub_c, const float* conv_w, const float* conv_b,
+                          const float* gamma, const float* beta, const float* wq,
+                          const float* wk, const float* wv, const float* wo, void* stream);
+/* build_model (pipeline.cpp:35-67) on device for every block. */
+int vinf_engine_init_weights(vinf_engine* e, uint64_t weight_seed, void* stream);
+
+/* Stages of one block (between them the caller runs the exchanges):
+ *   STUB      : x -> u0 (conv operand centre)           then VINF_XCHG_CONV
+ *   CONV      : u1 = u0 + conv(u0); GN partial sums #0  then all-reduce sums #0
+ *   GN_SQDEV  : mean = sums0 / count; partial sqdev #1  then all-reduce sums #1
+ *   GN_APPLY  : var = sums1 / count; u2 = GN(u1)        then VINF_XCHG_ATTN
+ *   ATTENTION : y = u2 + dual_scope(u2, t)  (y becomes the next block's x) */
+enum {
+    VINF_STAGE_STUB = 0,
+    VINF_STAGE_CONV = 1,
+    VINF_STAGE_GN_SQDEV = 2,
+    VINF_STAGE_GN_APPLY = 3,
+    VINF_STAGE_ATTENTION = 4
+};
+int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void* stream);
+/* All blocks, all stages (single worker: no exchanges needed). */
+int vinf_engine_forward(vinf_engine* e, double t, void* stream);
+/* Where the current block input / final output live (device pointers). */
+int vinf_engine_io(const vinf_engine* e, void** x, void** y);
+/* Device-side counters: number of kernel launches enqueued so far. */
+uint64_t vinf_engine_launches(const vinf_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VINF_TEMPORAL_H */

@@ -1,0 +1,177 @@
+// Bandwidth-bound elementwise kernels: seeded synthetic fill (bit-exact SplitMix64,
+// rng.hpp:14-26 / tensor.cpp:98-106), the per-frame spatial stub (ops.cpp:42-55),
+// and the fp32 -> (bf16 hi, bf16 lo) operand split used by the fp32 ("bf16x3") mode.
+// All vectorised 16 B per lane, grid-stride, grid sized to a multiple of the SM count.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace vinf {
+
+namespace {
+
+__device__ __forceinline__ float unit_from_state(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const uint32_t top24 = uint32_t(z >> 40);
+    // exact in binary32: k * 2^-23 - 1 with k < 2^24
+    return __fsub_rn(__fmul_rn(float(top24), 2.0f / 16777216.0f), 1.0f);
+}
+
+template <bool BF16>
+__global__ void fill_seeded_kernel(void* out, uint64_t n, uint64_t seed, uint64_t first,
+                                   float scale, int apply_scale) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        // state after (first + i + 1) draws
+        const uint64_t z = seed + (first + i + 1) * 0x9E3779B97F4A7C15ull;
+        float u = unit_from_state(z);
+        if (apply_scale) u = __fmul_rn(u, scale);
+        if (BF16)
+            static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(u);
+        else
+            static_cast<float*>(out)[i] = u;
+    }
+}
+
+// o = tanh(a[c] * x + c[c]); separate rounding of mul and add (no FMA contraction),
+// as the reference evaluates it in binary32.
+__device__ __forceinline__ float stub_fn(float x, float a, float c) {
+    return tanhf(__fadd_rn(__fmul_rn(a, x), c));
+}
+
+template <bool IN_BF16, bool OUT_BF16, bool SPLIT>
+__global__ void stub_kernel(const void* __restrict__ in, uint64_t n, uint32_t C,
+                            const float* __restrict__ a, const float* __restrict__ c,
+                            void* __restrict__ out, __nv_bfloat16* __restrict__ hi,
+                            __nv_bfloat16* __restrict__ lo) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t nv = n / 4;
+    for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv; v += stride) {
+        const uint64_t i = v * 4;
+        float x[4];
+        if (IN_BF16) {
+            const uint2 w = reinterpret_cast<const uint2*>(in)[v];
+            x[0] = __uint_as_float(w.x << 16);
+            x[1] = __uint_as_float(w.x & 0xFFFF0000u);
+            x[2] = __uint_as_float(w.y << 16);
+            x[3] = __uint_as_float(w.y & 0xFFFF0000u);
+        } else {
+            const float4 w = reinterpret_cast<const float4*>(in)[v];
+            x[0] = w.x; x[1] = w.y; x[2] = w.z; x[3] = w.w;
+        }
+        const uint32_t ch = uint32_t(i % C);
+        float y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) y[k] = stub_fn(x[k], __ldg(a + ch + k), __ldg(c + ch + k));
+        if (OUT_BF16) {
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(y[0], y[1]);
+            __nv_bfloat162 p1 = __floats2bfloat162_rn(y[2], y[3]);
+            reinterpret_cast<uint2*>(out)[v] =
+                make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+        } else {
+            reinterpret_cast<float4*>(out)[v] = make_float4(y[0], y[1], y[2], y[3]);
+        }
+        if (SPLIT) {
+            __nv_bfloat16 h[4], l[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dev::split_bf16(y[k], h[k], l[k]);
+            reinterpret_cast<uint2*>(hi)[v] = *reinterpret_cast<uint2*>(h);
+            reinterpret_cast<uint2*>(lo)[v] = *reinterpret_cast<uint2*>(l);
+        }
+    }
+}
+
+template <bool IN_BF16>
+__global__ void split_kernel(const void* __restrict__ in, uint64_t n,
+                             __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float x = IN_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(in)[i])
+                                : static_cast<const float*>(in)[i];
+        __nv_bfloat16 h, l;
+        dev::split_bf16(x, h, l);
+        hi[i] = h;
+        if (lo) lo[i] = l;
+    }
+}
+
+__global__ void cast_kernel(const void* __restrict__ in, int in_bf16, void* __restrict__ out,
+                            int out_bf16, uint64_t n) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float x = in_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(in)[i])
+                                : static_cast<const float*>(in)[i];
+        if (out_bf16)
+            static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(x);
+        else
+            static_cast<float*>(out)[i] = x;
+    }
+}
+
+}  // namespace
+
+int grid_for(uint64_t work_items, int block) {
+    const uint64_t want = (work_items + block - 1) / block;
+    const uint64_t cap = uint64_t(num_sms()) * 8;
+    return int(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+int launch_fill_seeded(void* out, bool bf16, uint64_t n, uint64_t seed, uint64_t first,
+                       float scale, cudaStream_t s) {
+    if (n == 0) return 0;
+    const int apply = scale != 1.0f;
+    if (bf16)
+        fill_seeded_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(out, n, seed, first, scale, apply);
+    else
+        fill_seeded_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(out, n, seed, first, scale, apply);
+    return int(cudaGetLastError());
+}
+
+int launch_stub(const void* in, bool in_bf16, uint64_t n, uint32_t C, const float* a,
+                const float* c, void* out, bool out_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                cudaStream_t s) {
+    if (n == 0) return 0;
+    if (C % 4 != 0 || n % 4 != 0) return int(cudaErrorInvalidValue);
+    const uint64_t nv = n / 4;
+    const int g = grid_for(nv, 256);
+    const bool split = hi != nullptr;
+#define STUB_CASE(IB, OB, SP)                                                              \
+    if (in_bf16 == IB && out_bf16 == OB && split == SP) {                                  \
+        stub_kernel<IB, OB, SP><<<g, 256, 0, s>>>(in, n, C, a, c, out, hi, lo);            \
+        return int(cudaGetLastError());                                                    \
+    }
+    STUB_CASE(false, false, false)
+    STUB_CASE(false, false, true)
+    STUB_CASE(true, true, false)
+    STUB_CASE(true, true, true)
+    STUB_CASE(false, true, false)
+    STUB_CASE(true, false, false)
+    STUB_CASE(true, false, true)
+    STUB_CASE(false, true, true)
+#undef STUB_CASE
+    return int(cudaErrorInvalidValue);
+}
+
+int launch_split(const void* in, bool in_bf16, uint64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                 cudaStream_t s) {
+    if (n == 0) return 0;
+    if (in_bf16)
+        split_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(in, n, hi, lo);
+    else
+        split_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(in, n, hi, lo);
+    return int(cudaGetLastError());
+}
+
+int launch_cast(const void* in, bool in_bf16, void* out, bool out_bf16, uint64_t n,
+                cudaStream_t s) {
+    if (n == 0) return 0;
+    cast_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, in_bf16, out, out_bf16, n);
+    return int(cudaGetLastError());
+}
+
+}  // namespace vinf

@@ -1,0 +1,366 @@
+// Clip engine: eps_theta_worker (pipeline.cpp:145-172) for one worker's clip, with every
+// activation buffer carved from one preallocated workspace (layout.hpp) and every
+// kernel enqueued on the caller's stream. The 3-step context sync happens between
+// stages through exchange lists (plan.cpp), executed by the caller's transport.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <functional>
+
+#include "host.hpp"
+#include "layout.hpp"
+#include "ops.hpp"
+
+namespace vinf {
+
+enum ParamSlot : uint64_t {  // pipeline.cpp:16-26
+    kStub = 0, kConvW = 1, kConvB = 2, kGamma = 3, kBeta = 4, kWq = 5, kWk = 6, kWv = 7, kWo = 8
+};
+
+uint64_t mix_seed(uint64_t seed, uint64_t salt) {  // rng.hpp:34-37
+    uint64_t z = (seed ^ (salt * 0xD1B54A32D192ED03ull)) + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+}  // namespace vinf
+
+using namespace vinf;
+
+struct EngineBlock {
+    float* f32 = nullptr;  // one allocation: stub_a, stub_c, conv_b, gamma, beta (5*C)
+    float* stub_a() const { return f32; }
+    float* stub_c() const { return f32 + C; }
+    float* conv_b() const { return f32 + 2 * C; }
+    float* gamma() const { return f32 + 3 * C; }
+    float* beta() const { return f32 + 4 * C; }
+    uint32_t C = 0;
+    DevMat conv;  // [taps*C, C]
+    DevMat wqkv;  // [3C, C]
+    DevMat wo;    // [C, C]
+};
+
+struct vinf_engine {
+    explicit vinf_engine(const Layout& l) : L(l) {}
+    Layout L;
+    uint8_t* ws = nullptr;
+    std::vector<EngineBlock> blocks;
+    TokenTable tt[2];
+    uint64_t launches = 0;
+
+    template <class T = uint8_t>
+    T* at(uint64_t off) const { return reinterpret_cast<T*>(ws + off); }
+    bool f32() const { return L.f32; }
+    uint64_t clip_elems() const { return uint64_t(L.f_clip) * L.E; }
+    void* x_of(uint32_t b) const { return at(b % 2 == 0 ? L.off_x : L.off_y); }
+    void* y_of(uint32_t b) const { return at(b % 2 == 0 ? L.off_y : L.off_x); }
+    double gn_count() const {  // elements per group over the whole video
+        return double(uint64_t(L.d.frames) * L.hw * L.d.channels / L.d.groups);
+    }
+
+    void stage_stub(uint32_t b, cudaStream_t s);
+    void stage_conv(uint32_t b, cudaStream_t s);
+    void stage_gn_sqdev(uint32_t b, cudaStream_t s);
+    void stage_gn_apply(uint32_t b, cudaStream_t s);
+    void stage_attention(uint32_t b, double t, cudaStream_t s);
+};
+
+void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
+    const EngineBlock& B = blocks.at(b);
+    const uint64_t n = clip_elems();
+    auto* u0 = at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E;
+    if (f32()) {
+        auto* lo = at<__nv_bfloat16>(L.off_u0lo) + uint64_t(L.hc) * L.E;
+        cuda_check(launch_stub(x_of(b), false, n, L.d.channels, B.stub_a(), B.stub_c(),
+                               at(L.off_u0f), false, u0, lo, s),
+                   "stub");
+    } else {
+        cuda_check(launch_stub(x_of(b), true, n, L.d.channels, B.stub_a(), B.stub_c(), u0, true,
+                               nullptr, nullptr, s),
+                   "stub");
+    }
+    ++launches;
+}
+
+void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
+    const EngineBlock& B = blocks.at(b);
+    const uint32_t C = L.d.channels;
+    Operand A;
+    A.hi = at<__nv_bfloat16>(L.off_u0);
+    A.lo = f32() ? at<__nv_bfloat16>(L.off_u0lo) : nullptr;
+    A.rows = uint64_t(L.cf) * L.hw;
+    A.cols = C;
+    A.ld = C;
+    std::vector<int64_t> ar, br;
+    for (uint32_t j = 0; j < L.d.taps; ++j) {
+        ar.push_back(int64_t(j) * L.hw);  // tap j reads own frame f at buffer frame f + j
+        br.push_back(int64_t(j) * C);
+    }
+    Epilogue ep;
+    ep.bias = B.conv_b();
+    ep.res = f32() ? at(L.off_u0f) : static_cast<void*>(at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E);
+    ep.res_ld = C;
+    ep.res_bf16 = !f32();
+    ep.out = at(L.off_u1);
+    ep.out_ld = C;
+    ep.out_bf16 = !f32();
+    gemm(A, ar, B.conv, br, int64_t(L.f_clip) * L.hw, C, ep, f32(), s);
+    ++launches;
+    double* sums = at<double>(L.off_sums);
+    cuda_check(launch_group_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, C, L.d.groups,
+                                 nullptr, sums, at<double>(L.off_scratch), false, s),
+               "gn sums");
+    launches += 2;
+}
+
+void vinf_engine::stage_gn_sqdev(uint32_t, cudaStream_t s) {
+    double* sums = at<double>(L.off_sums);
+    double* stats = at<double>(L.off_stats);
+    cuda_check(launch_group_finalize(sums, gn_count(), L.d.groups, stats, s), "gn mean");
+    cuda_check(launch_group_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, L.d.channels,
+                                 L.d.groups, stats, sums + L.d.groups, at<double>(L.off_scratch),
+                                 false, s),
+               "gn sqdev");
+    launches += 3;
+}
+
+void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
+    const EngineBlock& B = blocks.at(b);
+    double* sums = at<double>(L.off_sums);
+    double* stats = at<double>(L.off_stats);
+    const uint32_t G = L.d.groups;
+    cuda_check(launch_group_finalize(sums + G, gn_count(), G, stats + G, s), "gn var");
+    auto* u2 = at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E;
+    if (f32()) {
+        auto* lo = at<__nv_bfloat16>(L.off_u2lo) + uint64_t(L.ha) * L.E;
+        cuda_check(launch_group_apply(at(L.off_u1), false, uint64_t(L.f_clip) * L.hw,
+                                      L.d.channels, G, stats, stats + G, B.gamma(), B.beta(),
+                                      L.d.epsilon, at(L.off_u2f), false, u2, lo, s),
+                   "gn apply");
+    } else {
+        cuda_check(launch_group_apply(at(L.off_u1), true, uint64_t(L.f_clip) * L.hw,
+                                      L.d.channels, G, stats, stats + G, B.gamma(), B.beta(),
+                                      L.d.epsilon, u2, true, nullptr, nullptr, s),
+                   "gn apply");
+    }
+    launches += 2;
+}
+
+void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
+    const EngineBlock& B = blocks.at(b);
+    const uint32_t C = L.d.channels;
+    const uint64_t hw = L.hw;
+    Operand A;
+    A.hi = at<__nv_bfloat16>(L.off_u2);
+    A.lo = f32() ? at<__nv_bfloat16>(L.off_u2lo) : nullptr;
+    A.rows = uint64_t(L.af) * hw;
+    A.cols = C;
+    A.ld = C;
+    const size_t qes = f32() ? 4 : 2;
+    uint8_t* qkv = at(L.off_qkv);
+    auto project = [&](uint32_t frame0, uint32_t nframes, bool with_q) {
+        if (!nframes) return;
+        Epilogue ep;
+        ep.out = qkv + (uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C)) * qes;
+        ep.out_ld = 3 * C;
+        ep.out_bf16 = !f32();
+        gemm(A, {int64_t(frame0) * int64_t(hw)}, B.wqkv, {with_q ? 0 : int64_t(C)},
+             int64_t(nframes) * int64_t(hw), with_q ? 3 * C : 2 * C, ep, f32(), s);
+        ++launches;
+    };
+    project(L.ha, L.f_clip, true);                           // own frames: Q, K, V
+    project(L.ha - L.npre_a, L.npre_a, false);               // pre halo: K, V
+    project(L.ha + L.f_clip, L.npost_a, false);              // post halo: K, V
+    project(2 * L.ha + L.f_clip, L.n_remote, false);         // remote global frames: K, V
+    const bool bias_global = t > L.d.t_star;                  // ops.cpp:298
+    auto* ctx = at<__nv_bfloat16>(L.off_ctx);
+    auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
+    cuda_check(launch_attention_core(qkv, !f32(), L.hw, C, L.d.heads, L.f_clip, L.ha,
+                                     tt[bias_global ? 1 : 0], L.scale, L.d.bias, ctx, !f32(),
+                                     f32() ? ctx : nullptr, ctxlo, s),
+               "attention core");
+    ++launches;
+    Operand O;
+    O.hi = ctx;
+    O.lo = ctxlo;
+    O.rows = uint64_t(L.f_clip) * hw;
+    O.cols = C;
+    O.ld = C;
+    Epilogue ep;
+    ep.res = f32() ? at(L.off_u2f) : static_cast<void*>(at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E);
+    ep.res_ld = C;
+    ep.res_bf16 = !f32();
+    ep.out = y_of(b);
+    ep.out_ld = C;
+    ep.out_bf16 = !f32();
+    gemm(O, {0}, B.wo, {0}, int64_t(L.f_clip) * hw, C, ep, f32(), s);
+    ++launches;
+}
+
+// ---- C ABI (engine part) ---------------------------------------------------------
+
+namespace vinf {
+int guarded_call(const std::function<void()>& f);
+}
+
+extern "C" {
+
+int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf_engine** out) {
+    return guarded_call([&] {
+        if (!l || !out) shape_error("null argument");
+        if (!workspace) shape_error("null workspace");
+        auto s = static_cast<cudaStream_t>(stream);
+        auto* e = new vinf_engine(l->L);
+        e->ws = static_cast<uint8_t*>(workspace);
+        const Layout& L = e->L;
+        cuda_check(cudaMemsetAsync(e->ws, 0, L.total, s), "workspace memset");
+        for (int b = 0; b < 2; ++b) {
+            uint8_t* p = e->at(L.off_tok[b]);
+            const size_t nr = L.tok[b].rows.size() * 2, nb = L.tok[b].biased.size();
+            cuda_check(cudaMemcpyAsync(p, L.tok[b].rows.data(), nr, cudaMemcpyHostToDevice, s), "tok");
+            cuda_check(cudaMemcpyAsync(p + nr, L.tok[b].biased.data(), nb, cudaMemcpyHostToDevice, s), "tok");
+            cuda_check(cudaMemcpyAsync(p + nr + nb, L.tok[b].count.data(), L.tok[b].count.size() * 2,
+                                       cudaMemcpyHostToDevice, s), "tok");
+            e->tt[b].rows = reinterpret_cast<const uint16_t*>(p);
+            e->tt[b].biased = p + nr;
+            e->tt[b].count = reinterpret_cast<const uint16_t*>(p + nr + nb);
+        }
+        const uint32_t C = L.d.channels;
+        e->blocks.resize(L.d.blocks);
+        for (auto& B : e->blocks) {
+            B.C = C;
+            cuda_check(cudaMalloc(&B.f32, sizeof(float) * 5 * C), "cudaMalloc(block)");
+            B.conv.alloc(L.d.taps * C, C);
+            B.wqkv.alloc(3 * C, C);
+            B.wo.alloc(C, C);
+        }
+        cuda_check(cudaStreamSynchronize(s), "engine create sync");
+        *out = e;
+    });
+}
+
+void vinf_engine_destroy(vinf_engine* e) {
+    if (!e) return;
+    for (auto& B : e->blocks) {
+        if (B.f32) cudaFree(B.f32);
+        B.conv.release();
+        B.wqkv.release();
+        B.wo.release();
+    }
+    delete e;
+}
+
+int vinf_engine_set_block(vinf_engine* e, uint32_t block, const float* stub_a,
+                          const float* stub_c, const float* conv_w, const float* conv_b,
+                          const float* gamma, const float* beta, const float* wq, const float* wk,
+                          const float* wv, const float* wo, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        if (block >= e->blocks.size()) range_error("block index out of range");
+        auto s = static_cast<cudaStream_t>(stream);
+        EngineBlock& B = e->blocks[block];
+        const uint32_t C = B.C;
+        const size_t vb = sizeof(float) * C;
+        const float* vecs[5] = {stub_a, stub_c, conv_b, gamma, beta};
+        for (int i = 0; i < 5; ++i) {
+            if (!vecs[i]) shape_error("null block parameter");
+            cuda_check(cudaMemcpyAsync(B.f32 + i * C, vecs[i], vb, cudaMemcpyDeviceToDevice, s), "params");
+        }
+        if (!conv_w || !wq || !wk || !wv || !wo) shape_error("null block weight");
+        B.conv.from_f32(conv_w, s);
+        const size_t mat = size_t(C) * C;
+        float* tmp = nullptr;
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&tmp), 3 * mat * 4, s), "tmp");
+        cuda_check(cudaMemcpyAsync(tmp, wq, mat * 4, cudaMemcpyDeviceToDevice, s), "wq");
+        cuda_check(cudaMemcpyAsync(tmp + mat, wk, mat * 4, cudaMemcpyDeviceToDevice, s), "wk");
+        cuda_check(cudaMemcpyAsync(tmp + 2 * mat, wv, mat * 4, cudaMemcpyDeviceToDevice, s), "wv");
+        B.wqkv.from_f32(tmp, s);
+        cuda_check(cudaFreeAsync(tmp, s), "tmp");
+        B.wo.from_f32(wo, s);
+    });
+}
+
+int vinf_engine_init_weights(vinf_engine* e, uint64_t weight_seed, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        auto s = static_cast<cudaStream_t>(stream);
+        const uint32_t C = e->L.d.channels, taps = e->L.d.taps;
+        const float mat = 1.0f / std::sqrt(float(C));  // pipeline.cpp:44
+        const size_t m = size_t(C) * C;
+        float* tmp = nullptr;
+        const size_t n_tmp = size_t(taps) * m + 4 * m + 5 * C;
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n_tmp * 4, s), "tmp");
+        float* cw = tmp;
+        float* wq = cw + size_t(taps) * m;
+        float* wk = wq + m;
+        float* wv = wk + m;
+        float* wo = wv + m;
+        float* vec = wo + m;  // stub_a, stub_c, conv_b, gamma, beta
+        for (uint32_t b = 0; b < e->blocks.size(); ++b) {
+            auto salt = [&](uint64_t slot) { return mix_seed(weight_seed, uint64_t(b) * 16 + slot); };
+            // spatial_stub_coeffs (ops.cpp:57-65): a = draws [0, C), c = draws [C, 2C)
+            cuda_check(launch_fill_seeded(vec, false, C, salt(kStub), 0, 1.0f, s), "fill");
+            cuda_check(launch_fill_seeded(vec + C, false, C, salt(kStub), C, 1.0f, s), "fill");
+            cuda_check(launch_fill_seeded(cw, false, uint64_t(taps) * m, salt(kConvW), 0, mat, s), "fill");
+            cuda_check(launch_fill_seeded(vec + 2 * C, false, C, salt(kConvB), 0, 1.0f, s), "fill");
+            cuda_check(launch_fill_seeded(vec + 3 * C, false, C, salt(kGamma), 0, 1.0f, s), "fill");
+            cuda_check(launch_fill_seeded(vec + 4 * C, false, C, salt(kBeta), 0, 1.0f, s), "fill");
+            cuda_check(launch_fill_seeded(wq, false, m, salt(kWq), 0, mat, s), "fill");
+            cuda_check(launch_fill_seeded(wk, false, m, salt(kWk), 0, mat, s), "fill");
+            cuda_check(launch_fill_seeded(wv, false, m, salt(kWv), 0, mat, s), "fill");
+            cuda_check(launch_fill_seeded(wo, false, m, salt(kWo), 0, mat, s), "fill");
+            const int rc = vinf_engine_set_block(e, b, vec, vec + C, cw, vec + 2 * C, vec + 3 * C,
+                                                 vec + 4 * C, wq, wk, wv, wo, stream);
+            if (rc) throw Error(rc, vinf_last_error());
+        }
+        cuda_check(cudaFreeAsync(tmp, s), "tmp");
+        cuda_check(cudaStreamSynchronize(s), "init weights sync");
+    });
+}
+
+int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        if (block >= e->blocks.size()) range_error("block index out of range");
+        auto s = static_cast<cudaStream_t>(stream);
+        switch (stage) {
+            case VINF_STAGE_STUB: e->stage_stub(block, s); break;
+            case VINF_STAGE_CONV: e->stage_conv(block, s); break;
+            case VINF_STAGE_GN_SQDEV: e->stage_gn_sqdev(block, s); break;
+            case VINF_STAGE_GN_APPLY: e->stage_gn_apply(block, s); break;
+            case VINF_STAGE_ATTENTION: e->stage_attention(block, t, s); break;
+            default: range_error("unknown stage");
+        }
+    });
+}
+
+int vinf_engine_forward(vinf_engine* e, double t, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        if (e->L.d.workers != 1)
+            config_error("vinf_engine_forward runs a single worker; use vinf_engine_stage with a "
+                         "transport for workers > 1");
+        auto s = static_cast<cudaStream_t>(stream);
+        for (uint32_t b = 0; b < e->blocks.size(); ++b) {
+            e->stage_stub(b, s);
+            e->stage_conv(b, s);
+            e->stage_gn_sqdev(b, s);
+            e->stage_gn_apply(b, s);
+            e->stage_attention(b, t, s);
+        }
+    });
+}
+
+int vinf_engine_io(const vinf_engine* e, void** x, void** y) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        if (x) *x = e->at(e->L.off_x);
+        if (y) *y = e->blocks.size() % 2 == 1 ? e->at(e->L.off_y) : e->at(e->L.off_x);
+    });
+}
+
+uint64_t vinf_engine_launches(const vinf_engine* e) { return e ? e->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// Segmented-K tcgen05 GEMM used by every dense contraction of the temporal block:
+//
+//   D[m, n] = sum_s  A_s[m + a_row_s, :] . B_s[n + b_row_s, :]   (+ bias[n]) (+ R[m, n])
+//
+// Each segment s names one A and one B tensor map (bf16, K-major, [rows, K]) and a
+// row offset into each. This single form covers
+//   * the temporal conv as an implicit GEMM: one segment per tap j, A rows shifted
+//     by j*H*W inside the halo-extended clip buffer (ops.cpp:87-102), B = W[j];
+//   * the Q/K/V and O projections (ops.cpp:200-207): one segment;
+//   * the fp32 mode ("bf16x3"): every segment becomes three, hi*hi + hi*lo + lo*hi,
+//     with A = a_hi + a_lo and B = b_hi + b_lo split on the producer side.
+// TMA zero-fills out-of-range rows (negative or past the end), which is exactly the
+// reference's zero padding at the video boundary (ops.cpp:94).
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+namespace vinf {
+
+constexpr int kGemmMaxSeg = 12;
+
+struct GemmSeg {
+    int32_t a_map;  // 0 or 1 (A hi / A lo)
+    int32_t a_row;  // row offset added to the output row
+    int32_t b_map;  // 0 or 1 (B hi / B lo)
+    int32_t b_row;  // row offset added to the output column
+};
+
+struct GemmParams {
+    int32_t M, N, K;
+    int32_t nseg;
+    GemmSeg seg[kGemmMaxSeg];
+    const float* bias;  // [N] fp32 or null
+    const void* res;    // residual [M, ld] or null
+    int64_t res_ld;
+    int32_t res_bf16;
+    void* out;
+    int64_t out_ld;
+    int32_t out_bf16;
+};
+
+struct GemmMaps {
+    CUtensorMap a[2];
+    CUtensorMap b[2];
+};
+
+// Host side: encode a 2D bf16 K-major tensor map over [rows, cols] with row stride
+// ld_elems, box = 64 (K) x box_rows, 128B swizzle.
+int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t ld_elems, uint32_t box_rows);
+
+// Launches the GEMM on `stream`; picks the N tile. Returns 0 or a cudaError_t.
+int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream);
+
+// Largest supported N tile for a given N (used to build B tensor maps).
+int gemm_pick_block_n(int N);
+
+}  // namespace vinf

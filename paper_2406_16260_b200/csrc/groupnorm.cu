@@ -1,0 +1,254 @@
+// GroupNorm over [rows, C] clips with contiguous channel groups (ops.cpp:112-173,
+// clip_parallel.cpp:211-254). HBM-bound: one streaming read per statistics pass and
+// one read + write for the normalise/affine pass, 16 B per lane per access.
+//
+// Thread mapping: a block is CC x R threads (CC = C / VEC column chunks, R rows) and the
+// grid strides over rows by gridDim.x * R, so every thread keeps the SAME VEC channels
+// for the whole pass: per-channel affine constants are loaded once, and statistics are
+// accumulated per channel in registers (fp32 over a few dozen rows), reduced per block
+// into per-group f64 partials, then combined in a fixed order (deterministic, no atomics).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace vinf {
+
+namespace {
+
+constexpr int kMaxBlocksPerSm = 2;
+
+template <int VEC, bool BF16>
+__device__ __forceinline__ void load_vec(const void* base, uint64_t idx, float (&v)[VEC]) {
+    if (VEC == 8) {
+        if (BF16) {
+            const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + idx);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                v[2 * h] = __uint_as_float(ws[h] << 16);
+                v[2 * h + 1] = __uint_as_float(ws[h] & 0xFFFF0000u);
+            }
+        } else {
+            const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + idx);
+            const float4 b = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + idx + 4);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+            v[k] = BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx + k])
+                        : static_cast<const float*>(base)[idx + k];
+    }
+}
+
+template <int VEC, bool BF16>
+__global__ void group_sums_kernel(const void* __restrict__ x, uint64_t rows, uint32_t C,
+                                  uint32_t groups, const double* __restrict__ center,
+                                  double* __restrict__ partial /* [gridDim.x][groups] */) {
+    extern __shared__ double sh[];  // [groups]
+    const uint32_t CC = C / VEC;
+    const uint32_t R = blockDim.x / CC;
+    const uint32_t cc = threadIdx.x % CC;
+    const uint32_t rl = threadIdx.x / CC;
+    const uint32_t gs = C / groups;
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) sh[g] = 0.0;
+    __syncthreads();
+    if (rl < R) {
+        float ctr[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) ctr[k] = center ? float(center[(cc * VEC + k) / gs]) : 0.0f;
+        float acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[k] = 0.0f;
+        const uint64_t rstride = uint64_t(gridDim.x) * R;
+        for (uint64_t r = uint64_t(blockIdx.x) * R + rl; r < rows; r += rstride) {
+            float v[VEC];
+            load_vec<VEC, BF16>(x, r * C + cc * VEC, v);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                if (center) {
+                    const float d = v[k] - ctr[k];
+                    acc[k] = fmaf(d, d, acc[k]);
+                } else {
+                    acc[k] += v[k];
+                }
+            }
+        }
+        // per-channel partials -> per-group f64 in shared memory
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) atomicAdd(&sh[(cc * VEC + k) / gs], double(acc[k]));
+    }
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x)
+        partial[uint64_t(blockIdx.x) * groups + g] = sh[g];
+}
+
+__global__ void group_combine_kernel(const double* __restrict__ partial, uint32_t nblocks,
+                                     uint32_t groups, double* __restrict__ sums, int accumulate) {
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups;
+         g += gridDim.x * blockDim.x) {
+        double s = accumulate ? sums[g] : 0.0;
+        for (uint32_t b = 0; b < nblocks; ++b) s += partial[uint64_t(b) * groups + g];
+        sums[g] = s;
+    }
+}
+
+__global__ void group_finalize_kernel(const double* __restrict__ sums, double count,
+                                      uint32_t groups, double* __restrict__ stats) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < groups) stats[g] = sums[g] / count;
+}
+
+template <int VEC, bool IN_BF16, bool OUT_BF16, bool SPLIT>
+__global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, uint32_t C,
+                                   uint32_t groups, const double* __restrict__ means,
+                                   const double* __restrict__ vars,
+                                   const float* __restrict__ gamma, const float* __restrict__ beta,
+                                   float eps, void* __restrict__ y, __nv_bfloat16* __restrict__ hi,
+                                   __nv_bfloat16* __restrict__ lo) {
+    const uint32_t CC = C / VEC;
+    const uint32_t R = blockDim.x / CC;
+    const uint32_t cc = threadIdx.x % CC;
+    const uint32_t rl = threadIdx.x / CC;
+    if (rl >= R) return;
+    const uint32_t gs = C / groups;
+    float mu[VEC], sc[VEC], bt[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+        const uint32_t ch = cc * VEC + k;
+        const uint32_t g = ch / gs;
+        const double inv = 1.0 / sqrt(vars[g] + double(eps));  // ops.cpp:152
+        mu[k] = float(means[g]);
+        sc[k] = float(double(gamma[ch]) * inv);
+        bt[k] = beta[ch];
+    }
+    const uint64_t rstride = uint64_t(gridDim.x) * R;
+    for (uint64_t r = uint64_t(blockIdx.x) * R + rl; r < rows; r += rstride) {
+        const uint64_t idx = r * C + cc * VEC;
+        float v[VEC];
+        load_vec<VEC, IN_BF16>(x, idx, v);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) v[k] = fmaf(v[k] - mu[k], sc[k], bt[k]);
+        if (OUT_BF16) {
+            if (VEC == 8) {
+                uint32_t w[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+                    w[h] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(y) + idx) =
+                    make_uint4(w[0], w[1], w[2], w[3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < VEC; ++k)
+                    static_cast<__nv_bfloat16*>(y)[idx + k] = __float2bfloat16_rn(v[k]);
+            }
+        } else {
+            if (VEC == 8) {
+                float* yo = static_cast<float*>(y) + idx;
+                *reinterpret_cast<float4*>(yo) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4*>(yo + 4) = make_float4(v[4], v[5], v[6], v[7]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) static_cast<float*>(y)[idx + k] = v[k];
+            }
+        }
+        if (SPLIT) {
+            __nv_bfloat16 h[VEC], l[VEC];
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) dev::split_bf16(v[k], h[k], l[k]);
+            if (VEC == 8) {
+                *reinterpret_cast<uint4*>(hi + idx) = *reinterpret_cast<uint4*>(h);
+                *reinterpret_cast<uint4*>(lo + idx) = *reinterpret_cast<uint4*>(l);
+            } else {
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) { hi[idx + k] = h[k]; lo[idx + k] = l[k]; }
+            }
+        }
+    }
+}
+
+// Block = CC * R threads with R = max(1, 256 / CC); returns 0 if C is too wide.
+inline int block_for(uint32_t C, int vec, int* R) {
+    const uint32_t CC = C / vec;
+    if (CC == 0 || CC > 1024) return 0;
+    *R = CC >= 256 ? 1 : int(256 / CC);
+    return int(CC) * *R;
+}
+
+}  // namespace
+
+uint64_t group_sums_scratch_elems(uint32_t C) {
+    return uint64_t(num_sms()) * kMaxBlocksPerSm * (C ? C : 1);
+}
+
+int launch_group_sums(const void* x, bool bf16, uint64_t rows, uint32_t C, uint32_t groups,
+                      const double* center, double* sums, double* scratch, bool accumulate,
+                      cudaStream_t s) {
+    if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
+    const int vec = (C % 8 == 0) ? 8 : 1;
+    int R = 1;
+    const int block = block_for(C, vec, &R);
+    if (block == 0) return int(cudaErrorInvalidValue);
+    int grid = int((rows + R - 1) / R);
+    const int cap = num_sms() * kMaxBlocksPerSm;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    const size_t shm = sizeof(double) * groups;
+    if (rows > 0) {
+        if (vec == 8) {
+            if (bf16) group_sums_kernel<8, true><<<grid, block, shm, s>>>(x, rows, C, groups, center, scratch);
+            else group_sums_kernel<8, false><<<grid, block, shm, s>>>(x, rows, C, groups, center, scratch);
+        } else {
+            if (bf16) group_sums_kernel<1, true><<<grid, block, shm, s>>>(x, rows, C, groups, center, scratch);
+            else group_sums_kernel<1, false><<<grid, block, shm, s>>>(x, rows, C, groups, center, scratch);
+        }
+    } else {
+        grid = 0;
+    }
+    group_combine_kernel<<<(groups + 127) / 128, 128, 0, s>>>(scratch, uint32_t(grid), groups, sums,
+                                                             accumulate ? 1 : 0);
+    return int(cudaGetLastError());
+}
+
+int launch_group_finalize(const double* sums, double count, uint32_t groups, double* stats,
+                          cudaStream_t s) {
+    group_finalize_kernel<<<(groups + 127) / 128, 128, 0, s>>>(sums, count, groups, stats);
+    return int(cudaGetLastError());
+}
+
+int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
+                       const double* means, const double* vars, const float* gamma,
+                       const float* beta, float eps, void* y, bool out_bf16, __nv_bfloat16* hi,
+                       __nv_bfloat16* lo, cudaStream_t s) {
+    if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
+    if (rows == 0) return 0;
+    const int vec = (C % 8 == 0) ? 8 : 1;
+    int R = 1;
+    const int block = block_for(C, vec, &R);
+    if (block == 0) return int(cudaErrorInvalidValue);
+    int grid = int((rows + R - 1) / R);
+    const int cap = num_sms() * 8;
+    if (grid > cap) grid = cap;
+    const bool split = hi != nullptr;
+#define GA(V, IB, OB, SP)                                                                     \
+    if (vec == V && in_bf16 == IB && out_bf16 == OB && split == SP) {                         \
+        group_apply_kernel<V, IB, OB, SP><<<grid, block, 0, s>>>(x, rows, C, groups, means,   \
+                                                                 vars, gamma, beta, eps, y,   \
+                                                                 hi, lo);                     \
+        return int(cudaGetLastError());                                                       \
+    }
+    GA(8, false, false, false) GA(8, false, false, true) GA(8, true, true, false)
+    GA(8, true, true, true) GA(8, false, true, false) GA(8, true, false, false)
+    GA(1, false, false, false) GA(1, false, false, true) GA(1, true, true, false)
+    GA(1, false, true, false) GA(1, true, false, false)
+#undef GA
+    return int(cudaErrorInvalidValue);
+}
+
+}  // namespace vinf

@@ -1,0 +1,60 @@
+// Launchers for the non-GEMM kernels (elementwise, GroupNorm, dual-scope attention core).
+// Every launcher returns 0 or a cudaError_t value; none allocates device memory.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace vinf {
+
+int num_sms();
+int grid_for(uint64_t work_items, int block);
+
+// ---- elementwise.cu ----
+int launch_fill_seeded(void* out, bool bf16, uint64_t n, uint64_t seed, uint64_t first,
+                       float scale, cudaStream_t s);
+int launch_stub(const void* in, bool in_bf16, uint64_t n, uint32_t C, const float* a,
+                const float* c, void* out, bool out_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                cudaStream_t s);
+int launch_split(const void* in, bool in_bf16, uint64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                 cudaStream_t s);
+int launch_cast(const void* in, bool in_bf16, void* out, bool out_bf16, uint64_t n,
+                cudaStream_t s);
+
+// ---- groupnorm.cu ----
+// Scratch needed by launch_group_sums (doubles).
+uint64_t group_sums_scratch_elems(uint32_t C);
+// sums[g] (+)= sum over the group's elements of x (center == nullptr) or of
+// (x - center[g])^2. `accumulate` adds into sums instead of overwriting.
+int launch_group_sums(const void* x, bool bf16, uint64_t rows, uint32_t C, uint32_t groups,
+                      const double* center, double* sums, double* scratch, bool accumulate,
+                      cudaStream_t s);
+// stats[g] = sums[g] / count  (count = elements per group, across all clips)
+int launch_group_finalize(const double* sums, double count, uint32_t groups, double* stats,
+                          cudaStream_t s);
+// y = gamma * (x - mean_g) / sqrt(var_g + eps) + beta; optional hi/lo split output.
+int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
+                       const double* means, const double* vars, const float* gamma,
+                       const float* beta, float eps, void* y, bool out_bf16, __nv_bfloat16* hi,
+                       __nv_bfloat16* lo, cudaStream_t s);
+
+// ---- attention.cu ----
+constexpr int kMaxTokens = 160;  // n_local + 1 + n_global upper bound
+
+struct TokenTable {
+    const uint16_t* rows;   // [nq][kMaxTokens] key/value frame row (in QKV frame units)
+    const uint8_t* biased;  // [nq][kMaxTokens] 1 if this token's logit gets +bias
+    const uint16_t* count;  // [nq]
+};
+
+// (hi/lo non-null: only the split bf16 planes are written, the fp32-mode GEMM operand)
+// ctx[a, p, :] = softmax-attention of query frame a at position p over its token list.
+// qkv: [(frames) * HW, 3C] with Q in cols [0,C), K in [C,2C), V in [2C,3C);
+// query frame a lives at QKV frame row q_frame0 + a. ctx: [nq * HW, C].
+int launch_attention_core(const void* qkv, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
+                          uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale, float bias,
+                          void* ctx, bool ctx_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                          cudaStream_t s);
+
+}  // namespace vinf

@@ -1,0 +1,247 @@
+// Pure-host, integer-exact parts of the path: token sets (ops.cpp:177-198), the clip
+// plan (clip_parallel.cpp:54-91), traffic closed forms (clip_parallel.cpp:343-387), and
+// the clip engine's workspace layout + exchange plan. No CUDA calls in this file, so
+// layouts and exchange plans can be built and tested on CPU-only hosts.
+#include <algorithm>
+#include <cstring>
+
+#include "host.hpp"
+#include "layout.hpp"
+
+namespace vinf {
+
+std::vector<uint32_t> build_local_window(uint32_t a, uint32_t frames, uint32_t n_local) {
+    if (a >= frames) range_error("query frame outside video");
+    const uint32_t half = n_local / 2;
+    const uint32_t lo = a > half ? a - half : 0;
+    const uint32_t hi = (a + half < frames) ? a + half : frames - 1;
+    std::vector<uint32_t> w;
+    w.reserve(hi - lo + 1);
+    for (uint32_t i = lo; i <= hi; ++i) w.push_back(i);
+    return w;
+}
+
+std::vector<uint32_t> build_global_index_set(uint32_t frames, uint32_t n_global) {
+    if (n_global > frames)
+        config_error("global set size exceeds frame count: " + std::to_string(n_global) + " > " +
+                     std::to_string(frames));
+    std::vector<uint32_t> idx(n_global);
+    for (uint32_t j = 0; j < n_global; ++j) idx[j] = uint32_t((uint64_t(j) * frames) / n_global);
+    return idx;
+}
+
+uint32_t make_plan(uint32_t frames, uint32_t workers) {
+    if (workers == 0) config_error("worker count must be >= 1");
+    if (frames == 0 || frames % workers != 0)
+        config_error("workers must divide frames evenly: frames=" + std::to_string(frames) +
+                     " workers=" + std::to_string(workers));
+    return frames / workers;
+}
+
+std::vector<uint32_t> global_members_in_range(uint32_t frames, uint32_t n_global, uint32_t start,
+                                              uint32_t len) {
+    std::vector<uint32_t> local;
+    for (uint32_t g : build_global_index_set(frames, n_global))
+        if (g >= start && g < start + len) local.push_back(g - start);
+    return local;
+}
+
+void predict_sync_traffic(uint32_t frames, uint32_t workers, uint32_t halo, uint32_t gframes,
+                          uint32_t worker, uint64_t frame_bytes, uint64_t out[3]) {
+    const uint32_t f_clip = make_plan(frames, workers);
+    out[0] = out[1] = out[2] = 0;
+    if (workers == 1) return;
+    if (gframes > 0) {
+        // ring all-gather: worker i forwards every block except the one from i+1
+        uint64_t total = 0, next = 0, mine = 0;
+        for (uint32_t w = 0; w < workers; ++w) {
+            const uint64_t b =
+                global_members_in_range(frames, gframes, w * f_clip, f_clip).size() * frame_bytes;
+            total += b;
+            if (w == (worker + 1) % workers) next = b;
+            if (w == worker) mine = b;
+        }
+        out[0] += total - next;
+        out[1] += mine;
+        out[2] += workers - 1;
+    }
+    if (halo > 0) {
+        const uint64_t hb = uint64_t(halo) * frame_bytes;
+        if (worker + 1 < workers) { out[0] += hb; out[1] += hb; out[2] += 1; }
+        if (worker > 0) { out[0] += hb; out[1] += hb; out[2] += 1; }
+    }
+}
+
+void predict_groupnorm_traffic(uint32_t frames, uint32_t workers, uint32_t groups,
+                               uint64_t out[3]) {
+    make_plan(frames, workers);
+    out[0] = out[1] = out[2] = 0;
+    if (workers == 1) return;
+    const uint64_t block = uint64_t(groups) * sizeof(double);
+    out[0] = 2 * block * (workers - 1);
+    out[1] = 2 * block;
+    out[2] = 2 * uint64_t(workers - 1);
+}
+
+// ---------------------------------------------------------------------------
+// Engine layout
+
+namespace {
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
+    if (d.height == 0 || d.width == 0 || d.channels == 0) shape_error("zero tensor dimension");
+    if (d.taps == 0 || d.taps % 2 == 0) config_error("conv taps must be odd and >= 1");
+    if (d.groups == 0 || d.channels % d.groups != 0)
+        config_error("norm groups must divide channels: groups=" + std::to_string(d.groups) +
+                     " channels=" + std::to_string(d.channels));
+    if (d.heads == 0 || d.channels % d.heads != 0) config_error("heads must divide channels");
+    if (d.blocks == 0) config_error("model needs at least one block");
+    if (!(d.epsilon > 0.0f)) config_error("group norm epsilon must be > 0");
+    if (d.channels % 8 != 0)
+        shape_error("the clip engine needs channels % 8 == 0 (16-byte TMA rows)");
+    f_clip = make_plan(d.frames, d.workers);
+    if (d.worker >= d.workers) range_error("worker index out of range");
+    hw = d.height * d.width;
+    hc = (d.taps - 1) / 2;
+    ha = d.n_local / 2;
+    // pipeline.cpp:131-143
+    if (hc > f_clip)
+        config_error("conv halo exceeds clip: (taps-1)/2 = " + std::to_string(hc) +
+                     " > frames/workers = " + std::to_string(f_clip));
+    if (ha > f_clip)
+        config_error("attention halo exceeds clip: n_local/2 = " + std::to_string(ha) +
+                     " > frames/workers = " + std::to_string(f_clip));
+    if (d.n_local + 1 + d.n_global > uint32_t(kMaxTokens))
+        config_error("n_local + 1 + n_global exceeds " + std::to_string(kMaxTokens));
+    gset = build_global_index_set(d.frames, d.n_global);
+    start = d.worker * f_clip;
+    f32 = d.dtype == VINF_F32;
+    es = f32 ? 4 : 2;
+    E = uint64_t(hw) * d.channels;
+    scale = d.scale > 0.0f ? d.scale : 1.0f / std::sqrt(float(d.channels / d.heads));
+
+    npre_c = d.worker > 0 ? hc : 0;
+    npost_c = d.worker + 1 < d.workers ? hc : 0;
+    npre_a = d.worker > 0 ? ha : 0;
+    npost_a = d.worker + 1 < d.workers ? ha : 0;
+
+    // Global frames: local (inside this worker's synchronized window) or remote.
+    auto ext_lo = [&](uint32_t w) { return w * f_clip - (w > 0 ? ha : 0); };
+    auto ext_hi = [&](uint32_t w) { return (w + 1) * f_clip + (w + 1 < d.workers ? ha : 0); };
+    g_frame.assign(d.n_global, 0);
+    n_remote = 0;
+    for (uint32_t j = 0; j < d.n_global; ++j) {
+        const uint32_t g = gset[j];
+        if (g >= ext_lo(d.worker) && g < ext_hi(d.worker))
+            g_frame[j] = ha + (g - start);  // may sit in a halo slot (g < start)
+        else
+            g_frame[j] = 2 * ha + f_clip + n_remote++;
+    }
+    cf = hc + f_clip + hc;
+    af = 2 * ha + f_clip + n_remote;
+
+    // Token lists (clip_parallel.cpp:285-305): window first, then the global set.
+    for (int b = 0; b < 2; ++b) {
+        tok[b].resize(f_clip);
+        for (uint32_t a = 0; a < f_clip; ++a) {
+            for (uint32_t g : build_local_window(start + a, d.frames, d.n_local))
+                tok[b].push(a, ha + g - start, b == 0);
+            for (uint32_t j = 0; j < d.n_global; ++j) tok[b].push(a, g_frame[j], b == 1);
+        }
+    }
+
+    // Workspace regions.
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t o = off;
+        off = align_up(off + bytes, 1024);
+        return o;
+    };
+    const uint64_t clip = uint64_t(f_clip) * E;
+    off_x = take(clip * es);
+    off_y = take(clip * es);
+    off_u0 = take(uint64_t(cf) * E * 2);  // bf16 plane (bf16 mode) / hi plane (f32 mode)
+    off_u0lo = f32 ? take(uint64_t(cf) * E * 2) : 0;
+    off_u0f = f32 ? take(clip * 4) : 0;
+    off_u1 = take(clip * es);
+    off_u2 = take(uint64_t(af) * E * 2);
+    off_u2lo = f32 ? take(uint64_t(af) * E * 2) : 0;
+    off_u2f = f32 ? take(clip * 4) : 0;
+    off_qkv = take(uint64_t(af) * E * 3 * es);
+    off_ctx = take(clip * 2);
+    off_ctxlo = f32 ? take(clip * 2) : 0;
+    off_sums = take(sizeof(double) * 2 * d.groups);
+    off_stats = take(sizeof(double) * 2 * d.groups);
+    scratch_elems = uint64_t(kScratchBlocks) * d.groups;
+    off_scratch = take(sizeof(double) * scratch_elems);
+    const uint64_t tbytes = uint64_t(f_clip) * kMaxTokens * 3 + uint64_t(f_clip) * 2;
+    off_tok[0] = take(tbytes);
+    off_tok[1] = take(tbytes);
+    total = off;
+
+    build_exchanges();
+}
+
+void Layout::build_exchanges() {
+    const uint32_t i = d.worker, n = d.workers;
+    const uint64_t fb = E * 2;  // one frame of one bf16 plane
+    const int planes = f32 ? 2 : 1;
+    auto plane_off = [&](bool conv, int p) {
+        return conv ? (p == 0 ? off_u0 : off_u0lo) : (p == 0 ? off_u2 : off_u2lo);
+    };
+    auto halos = [&](std::vector<vinf_xfer>& xs, bool conv, uint32_t h, uint32_t stage) {
+        if (h == 0 || n == 1) return;
+        const uint32_t hslot = conv ? hc : ha;  // halo slot width in the buffer
+        for (int p = 0; p < planes; ++p) {
+            const uint64_t base = plane_off(conv, p);
+            // tag: stage * 1000 + direction * 10 + plane (direction 0 = i -> i+1)
+            if (i + 1 < n) {
+                // last h own frames -> next worker's pre slot; next's first h -> our post slot
+                xs.push_back({i + 1, 1, stage * 1000 + 0 * 10 + uint32_t(p), 0,
+                              base + uint64_t(hslot + f_clip - h) * fb, uint64_t(h) * fb});
+                xs.push_back({i + 1, 0, stage * 1000 + 1 * 10 + uint32_t(p), 0,
+                              base + uint64_t(hslot + f_clip) * fb, uint64_t(h) * fb});
+            }
+            if (i > 0) {
+                xs.push_back({i - 1, 0, stage * 1000 + 0 * 10 + uint32_t(p), 0,
+                              base + uint64_t(hslot - h) * fb, uint64_t(h) * fb});
+                xs.push_back({i - 1, 1, stage * 1000 + 1 * 10 + uint32_t(p), 0,
+                              base + uint64_t(hslot) * fb, uint64_t(h) * fb});
+            }
+        }
+    };
+    xconv.clear();
+    xattn.clear();
+    halos(xconv, true, hc, 1);
+    halos(xattn, false, ha, 2);
+    if (n > 1 && d.n_global > 0) {
+        // Remote global frames: the owner sends each of its members to every worker for
+        // which the frame lies outside the synchronized window (T1, clip_parallel.cpp:114-148,
+        // minus frames the receiver already holds).
+        auto lo_of = [&](uint32_t w) { return w * f_clip - (w > 0 ? ha : 0); };
+        auto hi_of = [&](uint32_t w) { return (w + 1) * f_clip + (w + 1 < n ? ha : 0); };
+        std::vector<uint32_t> slot_count(n, 0);
+        for (uint32_t j = 0; j < d.n_global; ++j) {
+            const uint32_t g = gset[j];
+            const uint32_t owner = g / f_clip;
+            for (uint32_t r = 0; r < n; ++r) {
+                if (g >= lo_of(r) && g < hi_of(r)) continue;  // local to r
+                const uint32_t slot = slot_count[r]++;
+                if (r == owner) continue;  // cannot happen (own frames are local)
+                for (int p = 0; p < planes; ++p) {
+                    const uint32_t tag = 3000 + j * 4 + uint32_t(p);
+                    const uint64_t base = plane_off(false, p);
+                    if (owner == i)
+                        xattn.push_back({r, 1, tag, 0, base + uint64_t(ha + g - start) * fb, fb});
+                    if (r == i)
+                        xattn.push_back(
+                            {owner, 0, tag, 0, base + uint64_t(2 * ha + f_clip + slot) * fb, fb});
+                }
+            }
+        }
+    }
+}
+
+}  // namespace vinf

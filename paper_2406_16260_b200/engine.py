@@ -1,0 +1,196 @@
+"""Clip engine: the preallocated, fused temporal block stack of one worker
+(eps_theta_worker, pipeline.cpp:145-172) and the stage loop that interleaves it with the
+paper's 3-step context sync.
+
+    layout = Layout(EngineDesc(...))         # pure host: buffers + exchange plan
+    eng = ClipEngine(layout)                 # one device workspace, weights on device
+    eng.init_weights(weight_seed=1)          # build_model (pipeline.cpp:35-67) on device
+    eng.x.copy_(clip)                        # [f_clip, H, W, C] in the engine dtype
+    forward(t=900.0, engines=[eng])          # single worker: one C call
+    forward(t, [eng], DistGroup(transport))  # clip-parallel over torch.distributed
+
+Exchanges are the workspace byte ranges the C++ layout lists (halo frames into the
+neighbours' halo slots, remote global frames into global slots), so the transport moves
+bf16 planes straight between the producers' and consumers' operand buffers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import EngineDesc
+from .transport import Msg, Transport
+
+_TORCH_DT = {_lib.VINF_F32: torch.float32, _lib.VINF_BF16: torch.bfloat16}
+
+
+def make_desc(frames, workers=1, worker=0, height=32, width=32, channels=320, taps=3, groups=32,
+              heads=1, n_local=16, n_global=16, bias=10.0, t_star=800.0, epsilon=1e-5,
+              scale=0.0, blocks=1, dtype=torch.float32) -> EngineDesc:
+    dt = _lib.VINF_F32 if dtype == torch.float32 else _lib.VINF_BF16
+    return EngineDesc(frames, workers, worker, height, width, channels, taps, groups, heads,
+                      n_local, n_global, bias, t_star, epsilon, scale, blocks, dt)
+
+
+class Layout:
+    """Host-side workspace layout + exchange plan (vinf_layout_*); no CUDA needed."""
+
+    def __init__(self, desc: EngineDesc):
+        self.desc = desc
+        self._lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(self._lib.vinf_layout_create(C.byref(desc), C.byref(h)))
+        self._h = h
+        n = C.c_uint64()
+        _lib.check(self._lib.vinf_layout_workspace_bytes(h, C.byref(n)))
+        self.workspace_bytes = n.value
+        self.f_clip = desc.frames // desc.workers
+        self.dtype = _TORCH_DT[desc.dtype]
+
+    def region(self, which: int):
+        off, n, fb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _lib.check(self._lib.vinf_layout_region(self._h, which, C.byref(off), C.byref(n),
+                                                C.byref(fb)))
+        return off.value, n.value, fb.value
+
+    def exchange(self, stage: int) -> list[_lib.Xfer]:
+        n = C.c_uint32()
+        cap = 4096
+        arr = (_lib.Xfer * cap)()
+        _lib.check(self._lib.vinf_layout_exchange(self._h, stage, arr, cap, C.byref(n)))
+        return [arr[i] for i in range(n.value)]
+
+    def reference_traffic(self):
+        a, b, c = (C.c_uint64 * 3)(), (C.c_uint64 * 3)(), (C.c_uint64 * 3)()
+        _lib.check(self._lib.vinf_layout_reference_traffic(self._h, a, b, c))
+        return list(a), list(b), list(c)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.vinf_layout_destroy(self._h)
+            self._h = None
+
+
+class ClipEngine:
+    def __init__(self, layout: Layout, device=None, workspace: torch.Tensor | None = None):
+        self.layout = layout
+        self.device = torch.device(device or "cuda")
+        self.ws = workspace if workspace is not None else torch.empty(
+            layout.workspace_bytes, dtype=torch.uint8, device=self.device)
+        d = layout.desc
+        self.shape = (layout.f_clip, d.height, d.width, d.channels)
+        h = C.c_void_p()
+        _lib.check(_lib.load().vinf_engine_create(layout._h, C.c_void_p(self.ws.data_ptr()),
+                                                  self._stream(), C.byref(h)))
+        self._h = h
+        xo, xn, _ = layout.region(_lib.VINF_BUF_X)
+        self.x = self.ws[xo:xo + xn].view(layout.dtype).view(self.shape)
+        yp = C.c_void_p()
+        _lib.check(_lib.load().vinf_engine_io(h, None, C.byref(yp)))
+        yo = yp.value - self.ws.data_ptr()
+        self.y = self.ws[yo:yo + xn].view(layout.dtype).view(self.shape)
+        so, sn, _ = layout.region(_lib.VINF_BUF_GN_SUMS)
+        self.gn_sums = self.ws[so:so + sn].view(torch.float64).view(2, d.groups)
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def init_weights(self, weight_seed: int = 1) -> None:
+        _lib.check(_lib.load().vinf_engine_init_weights(self._h, weight_seed, self._stream()))
+
+    def set_block(self, b: int, stub_a, stub_c, conv_w, conv_b, gamma, beta, wq, wk, wv, wo):
+        ts = [t.detach().to(device=self.device, dtype=torch.float32).contiguous()
+              for t in (stub_a, stub_c, conv_w, conv_b, gamma, beta, wq, wk, wv, wo)]
+        _lib.check(_lib.load().vinf_engine_set_block(self._h, b, *[C.c_void_p(t.data_ptr()) for t in ts],
+                                                     self._stream()))
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def stage(self, block: int, stage: int, t: float) -> None:
+        _lib.check(_lib.load().vinf_engine_stage(self._h, block, stage, C.c_double(t), self._stream()))
+
+    def forward_single(self, t: float) -> None:
+        _lib.check(_lib.load().vinf_engine_forward(self._h, C.c_double(t), self._stream()))
+
+    def launches(self) -> int:
+        return int(_lib.load().vinf_engine_launches(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None and _lib._lib is not None:
+            _lib._lib.vinf_engine_destroy(self._h)
+            self._h = None
+
+
+class LocalGroup:
+    """All workers' engines in this process (e.g. N clips on one GPU): exchanges are
+    device-to-device copies between workspaces, all-reduces sum in worker order."""
+
+    def exchange(self, engines: list[ClipEngine], stage: int) -> None:
+        by_worker = {e.layout.desc.worker: e for e in engines}
+        lists = {w: e.layout.exchange(stage) for w, e in by_worker.items()}
+        for w, xs in lists.items():
+            for x in xs:
+                if x.send:
+                    continue
+                src = [s for s in lists[x.peer] if s.send and s.peer == w and s.tag == x.tag]
+                if len(src) != 1 or src[0].bytes != x.bytes:
+                    raise _lib.ProtocolError(f"unmatched transfer into worker {w} tag {x.tag}")
+                s = src[0]
+                dst_ws, src_ws = by_worker[w].ws, by_worker[x.peer].ws
+                dst_ws[x.offset:x.offset + x.bytes].copy_(src_ws[s.offset:s.offset + s.bytes])
+
+    def allreduce_sums(self, engines: list[ClipEngine], k: int) -> None:
+        if len(engines) == 1:
+            return
+        ordered = sorted(engines, key=lambda e: e.layout.desc.worker)
+        total = ordered[0].gn_sums[k].clone()
+        for e in ordered[1:]:
+            total += e.gn_sums[k]
+        for e in ordered:
+            e.gn_sums[k].copy_(total)
+
+
+class DistGroup:
+    """One engine per process; exchanges over a Transport (torch.distributed / NCCL)."""
+
+    def __init__(self, transport: Transport):
+        self.t = transport
+
+    def exchange(self, engines: list[ClipEngine], stage: int) -> None:
+        (e,) = engines
+        msgs = [Msg(x.peer, bool(x.send), e.ws[x.offset:x.offset + x.bytes], x.tag)
+                for x in e.layout.exchange(stage)]
+        self.t.exchange(msgs)
+
+    def allreduce_sums(self, engines: list[ClipEngine], k: int) -> None:
+        (e,) = engines
+        self.t.allreduce_sum_(e.gn_sums[k])
+
+
+def forward(t: float, engines: list[ClipEngine], group=None) -> None:
+    """All blocks of eps_theta_worker for every engine in `engines` (pipeline.cpp:150-170):
+    stub -> [conv halo sync] -> conv + residual + GN partial sums -> [sum all-reduce]
+    -> GN sq-dev partials -> [sum all-reduce] -> GN apply -> [attention halo + global
+    sync] -> dual-scope attention + residual."""
+    blocks = engines[0].layout.desc.blocks
+    if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1:
+        engines[0].forward_single(t)
+        return
+    group = group or LocalGroup()
+    for b in range(blocks):
+        for e in engines:
+            e.stage(b, _lib.VINF_STAGE_STUB, t)
+        group.exchange(engines, _lib.VINF_XCHG_CONV)
+        for e in engines:
+            e.stage(b, _lib.VINF_STAGE_CONV, t)
+        group.allreduce_sums(engines, 0)
+        for e in engines:
+            e.stage(b, _lib.VINF_STAGE_GN_SQDEV, t)
+        group.allreduce_sums(engines, 1)
+        for e in engines:
+            e.stage(b, _lib.VINF_STAGE_GN_APPLY, t)
+        group.exchange(engines, _lib.VINF_XCHG_ATTN)
+        for e in engines:
+            e.stage(b, _lib.VINF_STAGE_ATTENTION, t)

@@ -1,0 +1,185 @@
+"""GPU parity: each operator of the path through the C ABI vs the CPU oracle
+(oracle/vinf_oracle.c, itself pinned bitwise to the reference library).
+
+Tolerances (written here as the north star states them): fp32 mode 1e-4 normwise,
+bf16 mode 2e-2 normwise; integer/RNG work bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import TOL_BF16, TOL_F32, normwise, to_np
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+TOL = {"f32": TOL_F32, "bf16": TOL_BF16}
+
+
+@pytest.fixture(scope="module")
+def ops(lib):
+    from paper_2406_16260_b200 import ops as _ops
+    return _ops
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+
+
+def test_fill_seeded_bitexact(ops, oracle):
+    for seed, first, n in [(0, 0, 1000), (7, 12345, 4097), (2**40 + 3, 99, 333)]:
+        got = ops.tensor_from_seed((1, 1, 1, n), seed, first).cpu().numpy().ravel()
+        want = oracle.fill_seeded(n, seed, first)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # frozen goldens (test_tensor.cpp:57-58)
+    assert ops.tensor_from_seed((1, 1, 1, 1), 0).item() == np.float32(0.7666215896606445)
+    assert ops.tensor_from_seed((1, 1, 1, 1), 1).item() == np.float32(0.13312304019927979)
+    b = ops.tensor_from_seed((2, 3, 4, 8), 5, dtype=torch.bfloat16).float().cpu().numpy().ravel()
+    w = torch.from_numpy(oracle.fill_seeded(192, 5)).bfloat16().float().numpy()
+    assert np.array_equal(b, w)
+
+
+def test_mix_seed(ops, oracle):
+    for s, t in [(1, 0), (1, 17), (12345, 3)]:
+        assert ops.mix_seed(s, t) == oracle.mix_seed(s, t)
+
+
+def test_spatial_stub(ops, oracle):
+    x = oracle.tensor_from_seed((4, 3, 5, 16), 3)
+    bp = oracle.build_block(16)
+    want = oracle.spatial_affine_tanh(x, bp.stub_a, bp.stub_c)
+    got = to_np(ops.spatial_affine_tanh(dev(x), dev(bp.stub_a), dev(bp.stub_c)))
+    assert np.abs(got - want).max() <= 2e-7
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("F,H,W,C,taps", [(8, 4, 4, 64, 3), (6, 4, 8, 320, 3), (9, 2, 4, 96, 5),
+                                          (5, 8, 8, 128, 1)])
+def test_temporal_conv(ops, oracle, mode, F, H, W, C, taps):
+    x = oracle.tensor_from_seed((F, H, W, C), 11)
+    bp = oracle.build_block(C, taps, weight_seed=3)
+    want = oracle.temporal_conv(x, taps, bp.conv_w, bp.conv_b)
+    k = ops.ConvKernel(taps, dev(bp.conv_w), dev(bp.conv_b))
+    got = to_np(ops.temporal_conv(dev(x, DT[mode]), k))
+    assert normwise(got, want) <= TOL[mode], normwise(got, want)
+
+
+def test_conv_over_extended_range(ops, oracle):
+    x = oracle.tensor_from_seed((10, 4, 4, 64), 12)
+    bp = oracle.build_block(64, 3)
+    k = ops.ConvKernel(3, dev(bp.conv_w), dev(bp.conv_b))
+    for start, n in [(0, 10), (1, 8), (3, 4), (9, 1)]:
+        want = oracle.conv_over_extended(x, start, n, 3, bp.conv_w, bp.conv_b)
+        got = to_np(ops.conv_over_extended(dev(x), start, n, k))
+        assert normwise(got, want) <= TOL_F32
+    with pytest.raises(ops.ShapeError):
+        ops.conv_over_extended(dev(x), 8, 3, k)
+
+
+def test_conv_zero_pad_boundary(ops):
+    # test_ops.cpp:179-194: all-ones input, all-ones weights, zero bias -> the video-edge
+    # frames see 2 of 3 taps, i.e. 2/3 of the interior value.
+    C = 16
+    x = torch.ones((5, 2, 2, C), device="cuda")
+    k = ops.ConvKernel(3, torch.ones(3 * C * C, device="cuda"), torch.zeros(C, device="cuda"))
+    y = ops.temporal_conv(x, k).cpu().numpy()
+    assert np.allclose(y[1:-1], 3 * C) and np.allclose(y[0], 2 * C) and np.allclose(y[-1], 2 * C)
+
+
+def test_conv_large_gemm_vs_torch(ops):
+    # taps=1 conv is the plain projection y = x W^T + b: check against torch fp32 at a
+    # size with many M/N tiles (plain PyTorch fp32 reference of the same op).
+    g = torch.Generator(device="cuda").manual_seed(0)
+    F, H, W, C = 16, 16, 32, 640
+    x = torch.rand((F, H, W, C), device="cuda", generator=g) * 2 - 1
+    w = (torch.rand((C, C), device="cuda", generator=g) * 2 - 1) / C ** 0.5
+    b = torch.rand(C, device="cuda", generator=g)
+    k = ops.ConvKernel(1, w, b)
+    want = (x.reshape(-1, C).double() @ w.double().T + b.double()).reshape(F, H, W, C)
+    got = ops.temporal_conv(x, k)
+    assert normwise(to_np(got), want.cpu().numpy()) <= TOL_F32
+    got16 = ops.temporal_conv(x.bfloat16(), k)
+    assert normwise(to_np(got16), want.cpu().numpy()) <= TOL_BF16
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("groups", [1, 2, 32])
+def test_group_norm(ops, oracle, mode, groups):
+    x = oracle.tensor_from_seed((6, 4, 8, 64), 21) * 3.0 + 0.5
+    bp = oracle.build_block(64)
+    want = oracle.group_norm(x, groups, bp.gamma, bp.beta)
+    p = ops.GroupNormParams(groups, dev(bp.gamma), dev(bp.beta))
+    xd = dev(x, DT[mode])
+    got = to_np(ops.group_norm(xd, p))
+    if mode == "f32":
+        assert normwise(got, want) <= 1e-5
+        m, s = oracle.group_stats(x, groups)
+        gm = ops.group_means(xd, groups).cpu().numpy()
+        gs = ops.group_sqdev(xd, groups, ops.group_means(xd, groups)).cpu().numpy()
+        assert np.allclose(gm, m, rtol=1e-6, atol=1e-7) and np.allclose(gs, s, rtol=1e-6)
+    else:
+        want16 = oracle.group_norm(to_np(xd), groups, bp.gamma, bp.beta)
+        assert normwise(got, want16) <= TOL_BF16
+
+
+def test_group_norm_config_error(ops):
+    x = torch.zeros((2, 2, 2, 16), device="cuda")
+    p = ops.GroupNormParams(3, torch.ones(16, device="cuda"), torch.zeros(16, device="cuda"))
+    with pytest.raises(ops.ConfigError):
+        ops.group_norm(x, p)
+
+
+def _attn(ops, bp, C, heads=1):
+    return ops.AttentionParams(C, dev(bp.wq), dev(bp.wk), dev(bp.wv), dev(bp.wo), heads=heads)
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("t", [700.0, 900.0])
+@pytest.mark.parametrize("F,H,W,C,nl,ng", [(24, 2, 4, 64, 16, 16), (24, 2, 2, 32, 6, 5),
+                                           (12, 4, 4, 128, 4, 3)])
+def test_dual_scope(ops, oracle, mode, t, F, H, W, C, nl, ng):
+    x = oracle.tensor_from_seed((F, H, W, C), 60)
+    bp = oracle.build_block(C, weight_seed=61)
+    sc = float(np.float32(1) / np.sqrt(np.float32(C)))
+    want = oracle.dual_scope(x, t, bp.wq, bp.wk, bp.wv, bp.wo, sc, nl, ng, 4.0, 800.0)
+    cfg = ops.DualScopeConfig(nl, ng, 4.0, 800.0)
+    got = to_np(ops.dual_scope_reference(dev(x, DT[mode]), t, _attn(ops, bp, C), cfg))
+    assert normwise(got, want) <= TOL[mode], normwise(got, want)
+
+
+def test_dual_scope_heads_extension(ops, oracle):
+    F, H, W, C = 16, 2, 4, 64
+    x = oracle.tensor_from_seed((F, H, W, C), 62)
+    bp = oracle.build_block(C, weight_seed=63)
+    sc = float(np.float32(1) / np.sqrt(np.float32(C // 8)))
+    want = oracle.dual_scope(x, 900.0, bp.wq, bp.wk, bp.wv, bp.wo, sc, 8, 4, 10.0, 800.0, heads=8)
+    got = to_np(ops.dual_scope_reference(dev(x), 900.0, _attn(ops, bp, C, heads=8),
+                                         ops.DualScopeConfig(8, 4, 10.0, 800.0)))
+    assert normwise(got, want) <= TOL_F32
+
+
+def test_attention_full_and_degenerate(ops, oracle):
+    F, H, W, C = 10, 2, 2, 32
+    x = oracle.tensor_from_seed((F, H, W, C), 90)
+    bp = oracle.build_block(C, weight_seed=91)
+    sc = float(np.float32(1) / np.sqrt(np.float32(C)))
+    want = oracle.attention_full(x, bp.wq, bp.wk, bp.wv, bp.wo, sc)
+    p = _attn(ops, bp, C)
+    full = to_np(ops.attention_full(dev(x), p))
+    assert normwise(full, want) <= TOL_F32
+    # test_ops.cpp:427-440: window spans every frame + identity global set, zero bias
+    cfg = ops.DualScopeConfig(2 * (F - 1), F, 0.0, 800.0)
+    deg = to_np(ops.dual_scope_reference(dev(x), 900.0, p, cfg))
+    assert normwise(deg, want) <= TOL_F32
+
+
+def test_t_star_is_strict(ops, oracle):
+    F, H, W, C = 24, 2, 2, 32
+    x = dev(oracle.tensor_from_seed((F, H, W, C), 60))
+    bp = oracle.build_block(C, weight_seed=61)
+    p = _attn(ops, bp, C)
+    cfg = ops.DualScopeConfig(6, 5, 4.0, 800.0)
+    at = ops.dual_scope_reference(x, 800.0, p, cfg)
+    late = ops.dual_scope_reference(x, 700.0, p, cfg)
+    early = ops.dual_scope_reference(x, 900.0, p, cfg)
+    assert torch.equal(at, late)
+    assert (early - late).abs().max().item() > 1e-3
