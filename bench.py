@@ -1,0 +1,378 @@
+"""Benchmark: temporal-layer latent frames/s of the clip-parallel dual-scope temporal block
+(BASELINE.json metric) on 1..8 B200s, with roofline and CPU-reference context.
+
+    python bench.py [--gpus N --steps K --warmup W --dtype bf16|f32]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+    python bench.py --impl reference ...                      (reference CPU arm)
+
+A step = one pass of the temporal block (stub -> temporal conv + residual -> GroupNorm
+-> dual-scope attention + residual, pipeline.cpp:150-170) over this GPU's clip of
+BASELINE configs[1]/[2]: 24 frames per GPU of a 40x64 latent, C=640, 16 global frames
+(n_local 16, bias 10, groups 32, taps 3, heads 1 = the reference's single-head form).
+Weak scaling: F = 24 * N frames over N GPUs with the 3-step context sync every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "temporal-layer latent frames/s at 1/2/4/8 B200; % of HBM/tensor roofline"
+FRAMES_PER_GPU, H, W, C = 24, 40, 64, 640
+N_LOCAL, N_GLOBAL, GROUPS, TAPS, HEADS, BIAS, T_STAR = 16, 16, 32, 3, 1, 10.0, 800.0
+T_STEP = 900.0  # t > t_star: bias on the global tokens (first denoising steps)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-hw", type=int, default=8, help="spatial crop side for CPU arms")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---- reference CPU arm ------------------------------------------------------------
+
+
+def cpu_reference_sample(frames: int, side: int, workers: int):
+    """The reference's own public run path (execute_run, runner.cpp:213-227) on a
+    bounded spatial crop (side x side of the 40x64 latent); positions are independent in
+    the temporal layers, so frames/s scales by crop/full positions. Returns
+    (frames/s at the full 40x64 size, wall seconds, threads)."""
+    from oracle.oracle import Reference
+    ref = Reference()
+    wall = ref.execute_run(frames, side, side, C, groups=GROUPS, n_local=N_LOCAL, n_global=N_GLOBAL,
+                           blocks=1, steps=1, workers=workers)
+    fps_crop = frames / wall
+    return fps_crop * (side * side) / (H * W), wall
+
+
+def ref_workers(frames: int) -> int:
+    cores = os.cpu_count() or 1
+    best = 0  # 0 = sequential oracle path (1 thread)
+    for n in range(2, min(cores, frames) + 1):
+        if frames % n == 0 and frames // n >= N_LOCAL // 2:
+            best = n
+    return best
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    frames = FRAMES_PER_GPU * args.gpus
+    workers = ref_workers(frames)
+    side = args.cpu_sample_hw
+    for _ in range(args.warmup):
+        cpu_reference_sample(frames, side, workers)
+    vals, walls = [], []
+    for _ in range(args.steps):
+        v, w = cpu_reference_sample(frames, side, workers)
+        vals.append(v)
+        walls.append(w)
+    value = float(sum(vals) / len(vals))
+    threads = max(workers, 1)
+    sample = (f"reference execute_run (1 block, 1 step) on F={frames} frames of a {side}x{side} "
+              f"crop of the 40x64 latent, C={C}, {'in-process clip-parallel x%d' % workers if workers else 'sequential'}; "
+              f"frames/s scaled by {side * side}/{H * W} positions")
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * sum(walls) / len(walls), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": workload_config(args.gpus, "f32"),
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(n: int, dtype: str) -> dict:
+    return {"workload": "BASELINE configs[1] (N=1) / configs[2] (N>1): clip-parallel dual-scope "
+                        "temporal block, 24 frames/GPU, 40x64 latent, C=640, 16 global frames",
+            "frames": FRAMES_PER_GPU * n, "frames_per_gpu": FRAMES_PER_GPU, "height": H,
+            "width": W, "channels": C, "taps": TAPS, "groups": GROUPS, "heads": HEADS,
+            "n_local": N_LOCAL, "n_global": N_GLOBAL, "bias": BIAS, "t": T_STEP, "blocks": 1,
+            "parallelism": f"clip-parallel x{n}",
+            "l2": "per-step working set ~1 GB >> 126 MB L2; the step's input is re-read cold",
+            "dtype": dtype}
+
+
+# ---- clocks ---------------------------------------------------------------------
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML every 20 ms on a thread."""
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ---- our arm --------------------------------------------------------------------
+
+KERNEL_WORK = None  # filled in main: kernel -> (flops or bytes per launch, bound)
+
+
+def kernel_work(f_clip: int, dtype_bytes: int):
+    """Algorithmic work per launch for each kernel group: GEMM flops
+    2*M*N*K; bandwidth kernels their compulsory bytes."""
+    hw = H * W
+    M = f_clip * hw
+    E = hw * C
+    s = dtype_bytes
+    return {
+        "conv_gemm": (2.0 * M * C * TAPS * C, "tensor"),
+        "qkv_gemm": (2.0 * M * 3 * C * C, "tensor"),
+        "o_gemm": (2.0 * M * C * C, "tensor"),
+        "kv_gemm_ctx": (None, "tensor"),
+        "stub": (f_clip * E * (s + s), "hbm"),
+        "gn_stats": (f_clip * E * s, "hbm"),
+        "gn_apply": (f_clip * E * (s + s), "hbm"),
+        "attn_core": (f_clip * E * s * 4, "hbm"),  # Q, K, V once + ctx write
+    }
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_16260_b200 import engine as en
+    from paper_2406_16260_b200.transport import DistTransport
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(world, 1)
+    if args.gpus != n and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = en.DistGroup(DistTransport())
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    F = FRAMES_PER_GPU * n
+    desc = en.make_desc(F, n, rank, H, W, C, TAPS, GROUPS, HEADS, N_LOCAL, N_GLOBAL, BIAS,
+                        T_STAR, 1e-5, 0.0, 1, dtype)
+    eng = en.ClipEngine(en.Layout(desc), device=dev)
+    eng.init_weights(1)
+    # synthetic latent: this rank's frames of tensor_from_seed({F,H,W,C}, 0) (runner.cpp:59-60)
+    from paper_2406_16260_b200 import ops
+    fc = FRAMES_PER_GPU
+    x_dev = ops.tensor_from_seed((fc, H, W, C), 0, first_elem=rank * fc * H * W * C, dtype=dtype,
+                                 device=dev)
+    eng.x.copy_(x_dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        en.forward(T_STEP, [eng], group)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region: K device-resident steps (value) ---------------------------
+    eng.profile(True)
+    l0 = eng.launches()
+    clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    with clocks:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        barrier()
+    launches = (eng.launches() - l0) // args.steps
+    stats = eng.kernel_stats()
+    eng.profile(False)
+    ms = t0.elapsed_time(t1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_per_step = ms_max / args.steps
+    value = n * fc * args.steps / (ms_max / 1000.0)
+
+    # ---- e2e: host buffers in, host buffers out, through the public engine API ----
+    es = 2 if dtype == torch.bfloat16 else 4
+    h_in = torch.empty((fc, H, W, C), dtype=dtype, pin_memory=True)
+    h_in.copy_(x_dev.cpu())
+    h_out = torch.empty_like(h_in, pin_memory=True)
+    e_steps = max(3, min(args.steps, 30))
+    for _ in range(2):
+        eng.x.copy_(h_in, non_blocking=True)
+        step()
+        h_out.copy_(eng.y, non_blocking=True)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e_steps):
+        eng.x.copy_(h_in, non_blocking=True)
+        step()
+        h_out.copy_(eng.y, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+    e2e_value = n * fc * e_steps / (float(ems.item()) / 1000.0)
+    clip_bytes = fc * H * W * C * es
+
+    # ---- roofline of the dominant kernel -------------------------------------------
+    hbm, tf_burst, tf_sus, src = peaks()
+    work = kernel_work(fc, es)
+    per_kernel = {}
+    for k, (tot, cnt) in stats.items():
+        per_kernel[k] = {"ms_per_launch": tot / max(cnt, 1), "launches": cnt,
+                         "share": 0.0}
+    tot_all = sum(v[0] for v in stats.values()) or 1.0
+    for k in per_kernel:
+        per_kernel[k]["share"] = stats[k][0] / tot_all
+    dom = max(stats, key=lambda k: stats[k][0]) if stats else None
+    roof = None
+    if dom:
+        w_, bound = work.get(dom, (None, "tensor"))
+        avg_ms = per_kernel[dom]["ms_per_launch"]
+        if bound == "tensor" and w_:
+            ach = w_ / (avg_ms / 1000.0) / 1e12
+            roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tf_sus,
+                    "unit": "TFLOP/s", "frac": ach / tf_sus, "traffic": None,
+                    "peak_source": f"{src} bf16 sustained (kernel timed inside the step)",
+                    "work_per_launch": w_}
+        elif w_:
+            ach = w_ / (avg_ms / 1000.0) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": None, "peak_source": f"{src} HBM copy",
+                    "work_per_launch": w_}
+    # whole-block roofline: all tensor work of the step at the sustained tensor peak
+    flops_step = sum(work[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm"))
+    block_roof = {"flops_per_step": flops_step,
+                  "achieved_tflops": flops_step / (ms_per_step / 1000.0) / 1e12,
+                  "frac_of_sustained": flops_step / (ms_per_step / 1000.0) / 1e12 / tf_sus}
+    for k, v in per_kernel.items():
+        w_, bound = work.get(k, (None, None))
+        if w_:
+            v["achieved"] = (w_ / (v["ms_per_launch"] / 1000.0) / (1e12 if bound == "tensor" else 1e9))
+            v["unit"] = "TFLOP/s" if bound == "tensor" else "GB/s"
+            v["frac"] = v["achieved"] / (tf_sus if bound == "tensor" else hbm)
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        try:
+            side = args.cpu_sample_hw
+            v, wall = cpu_reference_sample(fc, side, 0)
+            cpu = {"value": v, "unit": "frames/s", "cores": 1, "kind": "reference",
+                   "sample": f"reference execute_run, sequential (1 thread), F={fc}, "
+                             f"{side}x{side} crop of 40x64, C={C}, 1 block 1 step, wall "
+                             f"{wall:.2f}s; frames/s scaled by {side * side}/{H * W} positions"}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.dtype, "data": "synthetic (tensor_from_seed / build_model seeds 0/1)",
+                "config": workload_config(n, args.dtype),
+                "roofline": roof, "block_roofline": block_roof, "kernels": per_kernel,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": clip_bytes,
+                        "d2h_bytes_per_step": clip_bytes, "steps": e_steps},
+                "gpu_launches": int(launches * args.steps), "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -242,8 +242,15 @@ int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void*
 int vinf_engine_forward(vinf_engine* e, double t, void* stream);
 /* Where the current block input / final output live (device pointers). */
 int vinf_engine_io(const vinf_engine* e, void** x, void** y);
-/* Device-side counters: number of kernel launches enqueued so far. */
+/* Number of kernel launches this engine has enqueued so far. */
 uint64_t vinf_engine_launches(const vinf_engine* e);
+/* Per-kernel timing: with profiling on, CUDA events are recorded on the launching
+ * stream around each kernel group; vinf_engine_kernel_stats synchronises on them and
+ * returns, per kernel name (comma-separated in `names`), the summed milliseconds and
+ * the launch count since the last read, then resets. */
+int vinf_engine_profile(vinf_engine* e, int enable);
+int vinf_engine_kernel_stats(vinf_engine* e, char* names, uint32_t name_cap, double* total_ms,
+                             uint64_t* counts, uint32_t cap, uint32_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -124,6 +124,9 @@ _SIGS = {
     "vinf_engine_forward": (C.c_int, [_vp, C.c_double, _vp]),
     "vinf_engine_io": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
     "vinf_engine_launches": (C.c_uint64, [_vp]),
+    "vinf_engine_profile": (C.c_int, [_vp, C.c_int]),
+    "vinf_engine_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.c_uint32, C.POINTER(C.c_double),
+                                           _u64p, C.c_uint32, _u32p]),
 }
 
 _lib = None

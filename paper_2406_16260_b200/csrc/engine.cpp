@@ -50,6 +50,41 @@ struct vinf_engine {
     TokenTable tt[2];
     uint64_t launches = 0;
 
+    // Optional per-kernel timing: CUDA events recorded on the launching stream around
+    // each kernel (group), aggregated by name on request (vinf_engine_kernel_stats).
+    bool profiling = false;
+    struct Rec { const char* name; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+    cudaEvent_t ev() {
+        if (pool_used == pool.size()) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+            pool.push_back(e);
+        }
+        return pool[pool_used++];
+    }
+    struct Span {
+        vinf_engine* e;
+        const char* name;
+        cudaStream_t s;
+        cudaEvent_t a = nullptr;
+        Span(vinf_engine* eng, const char* n, cudaStream_t st) : e(eng), name(n), s(st) {
+            if (e->profiling) {
+                a = e->ev();
+                cudaEventRecord(a, s);
+            }
+        }
+        ~Span() {
+            if (a) {
+                cudaEvent_t b = e->ev();
+                cudaEventRecord(b, s);
+                e->recs.push_back({name, a, b});
+            }
+        }
+    };
+
     template <class T = uint8_t>
     T* at(uint64_t off) const { return reinterpret_cast<T*>(ws + off); }
     bool f32() const { return L.f32; }
@@ -71,6 +106,7 @@ void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
     const EngineBlock& B = blocks.at(b);
     const uint64_t n = clip_elems();
     auto* u0 = at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E;
+    Span span(this, "stub", s);
     if (f32()) {
         auto* lo = at<__nv_bfloat16>(L.off_u0lo) + uint64_t(L.hc) * L.E;
         cuda_check(launch_stub(x_of(b), false, n, L.d.channels, B.stub_a(), B.stub_c(),
@@ -106,9 +142,13 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     ep.out = at(L.off_u1);
     ep.out_ld = C;
     ep.out_bf16 = !f32();
-    gemm(A, ar, B.conv, br, int64_t(L.f_clip) * L.hw, C, ep, f32(), s);
+    {
+        Span span(this, "conv_gemm", s);
+        gemm(A, ar, B.conv, br, int64_t(L.f_clip) * L.hw, C, ep, f32(), s);
+    }
     ++launches;
     double* sums = at<double>(L.off_sums);
+    Span span(this, "gn_stats", s);
     cuda_check(launch_group_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, C, L.d.groups,
                                  nullptr, sums, at<double>(L.off_scratch), false, s),
                "gn sums");
@@ -118,6 +158,7 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
 void vinf_engine::stage_gn_sqdev(uint32_t, cudaStream_t s) {
     double* sums = at<double>(L.off_sums);
     double* stats = at<double>(L.off_stats);
+    Span span(this, "gn_stats", s);
     cuda_check(launch_group_finalize(sums, gn_count(), L.d.groups, stats, s), "gn mean");
     cuda_check(launch_group_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, L.d.channels,
                                  L.d.groups, stats, sums + L.d.groups, at<double>(L.off_scratch),
@@ -131,6 +172,7 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     double* sums = at<double>(L.off_sums);
     double* stats = at<double>(L.off_stats);
     const uint32_t G = L.d.groups;
+    Span span(this, "gn_apply", s);
     cuda_check(launch_group_finalize(sums + G, gn_count(), G, stats + G, s), "gn var");
     auto* u2 = at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E;
     if (f32()) {
@@ -166,6 +208,7 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
         ep.out = qkv + (uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C)) * qes;
         ep.out_ld = 3 * C;
         ep.out_bf16 = !f32();
+        Span span(this, with_q ? "qkv_gemm" : "kv_gemm_ctx", s);
         gemm(A, {int64_t(frame0) * int64_t(hw)}, B.wqkv, {with_q ? 0 : int64_t(C)},
              int64_t(nframes) * int64_t(hw), with_q ? 3 * C : 2 * C, ep, f32(), s);
         ++launches;
@@ -177,10 +220,13 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     const bool bias_global = t > L.d.t_star;                  // ops.cpp:298
     auto* ctx = at<__nv_bfloat16>(L.off_ctx);
     auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
+    {
+    Span span(this, "attn_core", s);
     cuda_check(launch_attention_core(qkv, !f32(), L.hw, C, L.d.heads, L.f_clip, L.ha,
                                      tt[bias_global ? 1 : 0], L.scale, L.d.bias, ctx, !f32(),
                                      f32() ? ctx : nullptr, ctxlo, s),
                "attention core");
+    }
     ++launches;
     Operand O;
     O.hi = ctx;
@@ -195,6 +241,7 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     ep.out = y_of(b);
     ep.out_ld = C;
     ep.out_bf16 = !f32();
+    Span span(this, "o_gemm", s);
     gemm(O, {0}, B.wo, {0}, int64_t(L.f_clip) * hw, C, ep, f32(), s);
     ++launches;
 }
@@ -243,6 +290,7 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
 
 void vinf_engine_destroy(vinf_engine* e) {
     if (!e) return;
+    for (cudaEvent_t ev : e->pool) cudaEventDestroy(ev);
     for (auto& B : e->blocks) {
         if (B.f32) cudaFree(B.f32);
         B.conv.release();
@@ -362,5 +410,51 @@ int vinf_engine_io(const vinf_engine* e, void** x, void** y) {
 }
 
 uint64_t vinf_engine_launches(const vinf_engine* e) { return e ? e->launches : 0; }
+
+int vinf_engine_profile(vinf_engine* e, int enable) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        e->profiling = enable != 0;
+        e->recs.clear();
+        e->pool_used = 0;
+    });
+}
+
+int vinf_engine_kernel_stats(vinf_engine* e, char* names, uint32_t name_cap, double* total_ms,
+                             uint64_t* counts, uint32_t cap, uint32_t* n_out) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        std::vector<std::string> keys;
+        std::vector<double> ms;
+        std::vector<uint64_t> cnt;
+        for (const auto& r : e->recs) {
+            cuda_check(cudaEventSynchronize(r.b), "event sync");
+            float t = 0.f;
+            cuda_check(cudaEventElapsedTime(&t, r.a, r.b), "event elapsed");
+            size_t k = 0;
+            while (k < keys.size() && keys[k] != r.name) ++k;
+            if (k == keys.size()) {
+                keys.push_back(r.name);
+                ms.push_back(0.0);
+                cnt.push_back(0);
+            }
+            ms[k] += t;
+            cnt[k] += 1;
+        }
+        if (n_out) *n_out = uint32_t(keys.size());
+        std::string joined;
+        for (size_t k = 0; k < keys.size(); ++k) joined += (k ? "," : "") + keys[k];
+        if (names && name_cap) {
+            std::strncpy(names, joined.c_str(), name_cap - 1);
+            names[name_cap - 1] = 0;
+        }
+        for (size_t k = 0; k < keys.size() && k < cap; ++k) {
+            if (total_ms) total_ms[k] = ms[k];
+            if (counts) counts[k] = cnt[k];
+        }
+        e->recs.clear();
+        e->pool_used = 0;
+    });
+}
 
 }  // extern "C"

@@ -117,6 +117,20 @@ class ClipEngine:
     def launches(self) -> int:
         return int(_lib.load().vinf_engine_launches(self._h))
 
+    def profile(self, enable: bool = True) -> None:
+        _lib.check(_lib.load().vinf_engine_profile(self._h, int(enable)))
+
+    def kernel_stats(self) -> dict:
+        """{kernel name: (total ms, launches)} since the last read (needs profile())."""
+        names = C.create_string_buffer(1024)
+        ms = (C.c_double * 32)()
+        cnt = (C.c_uint64 * 32)()
+        n = C.c_uint32()
+        _lib.check(_lib.load().vinf_engine_kernel_stats(self._h, names, 1024, ms, cnt, 32,
+                                                        C.byref(n)))
+        keys = names.value.decode().split(",") if n.value else []
+        return {k: (ms[i], int(cnt[i])) for i, k in enumerate(keys)}
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None and _lib._lib is not None:
             _lib._lib.vinf_engine_destroy(self._h)
