@@ -225,17 +225,19 @@ int vinf_engine_set_block(vinf_engine* e, uint32_t block, const float* stub_a,
 int vinf_engine_init_weights(vinf_engine* e, uint64_t weight_seed, void* stream);
 
 /* Stages of one block (between them the caller runs the exchanges):
- *   STUB      : x -> u0 (conv operand centre)           then VINF_XCHG_CONV
- *   CONV      : u1 = u0 + conv(u0); GN partial sums #0  then all-reduce sums #0
- *   GN_SQDEV  : mean = sums0 / count; partial sqdev #1  then all-reduce sums #1
- *   GN_APPLY  : var = sums1 / count; u2 = GN(u1)        then VINF_XCHG_ATTN
- *   ATTENTION : y = u2 + dual_scope(u2, t)  (y becomes the next block's x) */
+ *   STUB      : x -> u0 (conv operand centre)                 then VINF_XCHG_CONV
+ *   CONV      : u1 = u0 + conv(u0), with the clip's GroupNorm (sum, sum of squares)
+ *               per group fused into the GEMM epilogue            then all-reduce GN_SUMS
+ *   GN_APPLY  : mean/var from the all-reduced sums; u2 = GN(u1)  then VINF_XCHG_ATTN
+ *   ATTENTION : y = u2 + dual_scope(u2, t)  (y becomes the next block's x)
+ * (The reference combines GN statistics in two rounds, clip_parallel.cpp:242-253; the
+ * engine needs one all-reduce of 2*groups doubles; op-level vinf_group_norm keeps the
+ * reference's two-pass arithmetic.) */
 enum {
     VINF_STAGE_STUB = 0,
     VINF_STAGE_CONV = 1,
-    VINF_STAGE_GN_SQDEV = 2,
-    VINF_STAGE_GN_APPLY = 3,
-    VINF_STAGE_ATTENTION = 4
+    VINF_STAGE_GN_APPLY = 2,
+    VINF_STAGE_ATTENTION = 3
 };
 int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void* stream);
 /* All blocks, all stages (single worker: no exchanges needed). */
@@ -251,6 +253,13 @@ uint64_t vinf_engine_launches(const vinf_engine* e);
 int vinf_engine_profile(vinf_engine* e, int enable);
 int vinf_engine_kernel_stats(vinf_engine* e, char* names, uint32_t name_cap, double* total_ms,
                              uint64_t* counts, uint32_t cap, uint32_t* n_out);
+
+/* ---- diagnostics ---------------------------------------------------------------
+ * Times the segmented tcgen05 GEMM alone on synthetic bf16 data: out[M,N] (bf16) =
+ * sum over nseg segments of A[M,K] B[N,K]^T (+ bf16 residual); flags = 1 skips the
+ * epilogue's global stores (isolates the main loop). Average ms over iters launches. */
+int vinf_gemm_bench(uint32_t M, uint32_t N, uint32_t K, uint32_t nseg, int flags, int residual,
+                    int iters, float* avg_ms);
 
 #ifdef __cplusplus
 }

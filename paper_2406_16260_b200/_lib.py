@@ -16,8 +16,7 @@ VINF_OK, VINF_ERR, VINF_ERR_CONFIG, VINF_ERR_TRANSPORT, VINF_ERR_IO, VINF_ERR_IN
 VINF_F32, VINF_BF16 = 0, 1
 VINF_BUF_X, VINF_BUF_Y, VINF_BUF_CONV_IN, VINF_BUF_ATTN_IN, VINF_BUF_GN_SUMS = range(5)
 VINF_XCHG_CONV, VINF_XCHG_ATTN = 0, 1
-(VINF_STAGE_STUB, VINF_STAGE_CONV, VINF_STAGE_GN_SQDEV, VINF_STAGE_GN_APPLY,
- VINF_STAGE_ATTENTION) = range(5)
+VINF_STAGE_STUB, VINF_STAGE_CONV, VINF_STAGE_GN_APPLY, VINF_STAGE_ATTENTION = range(4)
 
 
 class VinfError(RuntimeError):
@@ -125,6 +124,8 @@ _SIGS = {
     "vinf_engine_io": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
     "vinf_engine_launches": (C.c_uint64, [_vp]),
     "vinf_engine_profile": (C.c_int, [_vp, C.c_int]),
+    "vinf_gemm_bench": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
+                                  C.c_int, C.POINTER(C.c_float)]),
     "vinf_engine_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.c_uint32, C.POINTER(C.c_double),
                                            _u64p, C.c_uint32, _u32p]),
 }

@@ -111,6 +111,8 @@ int launch_attention_core(const void* qkv, bool bf16, uint32_t HW, uint32_t C, u
                           cudaStream_t s) {
     if (heads == 0 || C % heads != 0 || HW == 0) return int(cudaErrorInvalidValue);
     if (nq == 0) return 0;
+    if (bf16 && ctx_bf16 && hi == nullptr && attention_tc_supported(C, heads, tt))
+        return launch_attention_core_tc(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s);
     const size_t shm = sizeof(float) * kCoreWarps * (C + kMaxTokens);
     if (shm > 200 * 1024) return int(cudaErrorInvalidValue);
     const int out = hi != nullptr ? 2 : (ctx_bf16 ? 1 : 0);

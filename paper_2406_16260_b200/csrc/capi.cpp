@@ -274,6 +274,58 @@ int vinf_attention_parallel(uint32_t frames, uint32_t workers, uint32_t worker,
     });
 }
 
+// ---- diagnostics ----
+
+int vinf_gemm_bench(uint32_t M, uint32_t N, uint32_t K, uint32_t nseg, int flags, int residual,
+                    int iters, float* avg_ms) {
+    return guarded_call([&] {
+        if (!M || !N || !K || !nseg || iters <= 0 || !avg_ms) shape_error("bad gemm bench args");
+        cudaStream_t s = nullptr;
+        const uint64_t arows = uint64_t(M) + uint64_t(nseg) * 64;
+        TmpBuf a(arows * K * 2, s), o(uint64_t(M) * N * 2, s), r(residual ? uint64_t(M) * N * 2 : 0, s);
+        DevMat B;
+        B.alloc(nseg * N, K);
+        cuda_check(launch_fill_seeded(a.p, true, arows * K, 1, 0, 1.0f, s), "fill");
+        cuda_check(launch_fill_seeded(B.hi, true, uint64_t(nseg) * N * K, 2, 0, 0.03f, s), "fill");
+        if (residual) cuda_check(launch_fill_seeded(r.p, true, uint64_t(M) * N, 3, 0, 1.0f, s), "fill");
+        Operand A;
+        A.hi = static_cast<const __nv_bfloat16*>(a.p);
+        A.rows = arows;
+        A.cols = K;
+        A.ld = K;
+        std::vector<int64_t> ar, br;
+        for (uint32_t j = 0; j < nseg; ++j) {
+            ar.push_back(int64_t(j) * 64);
+            br.push_back(int64_t(j) * N);
+        }
+        Epilogue ep;
+        ep.out = o.p;
+        ep.out_ld = N;
+        ep.out_bf16 = true;
+        if (residual) {
+            ep.res = r.p;
+            ep.res_ld = N;
+            ep.res_bf16 = true;
+        }
+        g_gemm_debug_flags = flags;
+        for (int i = 0; i < 2; ++i) gemm(A, ar, B, br, M, N, ep, false, s);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        for (int i = 0; i < iters; ++i) gemm(A, ar, B, br, M, N, ep, false, s);
+        cudaEventRecord(e1, s);
+        cuda_check(cudaEventSynchronize(e1), "gemm bench");
+        g_gemm_debug_flags = 0;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *avg_ms = ms / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        B.release();
+    });
+}
+
 // ---- layout ----
 
 int vinf_layout_create(const vinf_engine_desc* d, vinf_layout** out) {

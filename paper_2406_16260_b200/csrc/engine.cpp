@@ -97,7 +97,6 @@ struct vinf_engine {
 
     void stage_stub(uint32_t b, cudaStream_t s);
     void stage_conv(uint32_t b, cudaStream_t s);
-    void stage_gn_sqdev(uint32_t b, cudaStream_t s);
     void stage_gn_apply(uint32_t b, cudaStream_t s);
     void stage_attention(uint32_t b, double t, cudaStream_t s);
 };
@@ -147,24 +146,14 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
         gemm(A, ar, B.conv, br, int64_t(L.f_clip) * L.hw, C, ep, f32(), s);
     }
     ++launches;
-    double* sums = at<double>(L.off_sums);
+    // GroupNorm statistics of u1 in one pass (sum, sum of squares per group; u1 was just
+    // written and is largely L2-resident); workers all-reduce them before GN_APPLY.
     Span span(this, "gn_stats", s);
-    cuda_check(launch_group_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, C, L.d.groups,
-                                 nullptr, sums, at<double>(L.off_scratch), false, s),
-               "gn sums");
+    cuda_check(launch_group_moment_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, C,
+                                        L.d.groups, at<double>(L.off_sums),
+                                        at<double>(L.off_scratch), s),
+               "gn moments");
     launches += 2;
-}
-
-void vinf_engine::stage_gn_sqdev(uint32_t, cudaStream_t s) {
-    double* sums = at<double>(L.off_sums);
-    double* stats = at<double>(L.off_stats);
-    Span span(this, "gn_stats", s);
-    cuda_check(launch_group_finalize(sums, gn_count(), L.d.groups, stats, s), "gn mean");
-    cuda_check(launch_group_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, L.d.channels,
-                                 L.d.groups, stats, sums + L.d.groups, at<double>(L.off_scratch),
-                                 false, s),
-               "gn sqdev");
-    launches += 3;
 }
 
 void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
@@ -173,7 +162,8 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     double* stats = at<double>(L.off_stats);
     const uint32_t G = L.d.groups;
     Span span(this, "gn_apply", s);
-    cuda_check(launch_group_finalize(sums + G, gn_count(), G, stats + G, s), "gn var");
+    // mean = sum / n, var = sumsq / n - mean^2 over the whole video (n counts all clips)
+    cuda_check(launch_group_moments(sums, gn_count(), G, stats, s), "gn moments");
     auto* u2 = at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E;
     if (f32()) {
         auto* lo = at<__nv_bfloat16>(L.off_u2lo) + uint64_t(L.ha) * L.E;
@@ -263,16 +253,14 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
         e->ws = static_cast<uint8_t*>(workspace);
         const Layout& L = e->L;
         cuda_check(cudaMemsetAsync(e->ws, 0, L.total, s), "workspace memset");
+        std::vector<uint8_t> blob[2];
         for (int b = 0; b < 2; ++b) {
             uint8_t* p = e->at(L.off_tok[b]);
-            const size_t nr = L.tok[b].rows.size() * 2, nb = L.tok[b].biased.size();
-            cuda_check(cudaMemcpyAsync(p, L.tok[b].rows.data(), nr, cudaMemcpyHostToDevice, s), "tok");
-            cuda_check(cudaMemcpyAsync(p + nr, L.tok[b].biased.data(), nb, cudaMemcpyHostToDevice, s), "tok");
-            cuda_check(cudaMemcpyAsync(p + nr + nb, L.tok[b].count.data(), L.tok[b].count.size() * 2,
-                                       cudaMemcpyHostToDevice, s), "tok");
-            e->tt[b].rows = reinterpret_cast<const uint16_t*>(p);
-            e->tt[b].biased = p + nr;
-            e->tt[b].count = reinterpret_cast<const uint16_t*>(p + nr + nb);
+            blob[b].resize(L.tok[b].blob_bytes());
+            L.tok[b].pack(blob[b].data());
+            cuda_check(cudaMemcpyAsync(p, blob[b].data(), blob[b].size(), cudaMemcpyHostToDevice, s),
+                       "tokens");
+            e->tt[b] = L.tok[b].view(p);
         }
         const uint32_t C = L.d.channels;
         e->blocks.resize(L.d.blocks);
@@ -376,7 +364,6 @@ int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void*
         switch (stage) {
             case VINF_STAGE_STUB: e->stage_stub(block, s); break;
             case VINF_STAGE_CONV: e->stage_conv(block, s); break;
-            case VINF_STAGE_GN_SQDEV: e->stage_gn_sqdev(block, s); break;
             case VINF_STAGE_GN_APPLY: e->stage_gn_apply(block, s); break;
             case VINF_STAGE_ATTENTION: e->stage_attention(block, t, s); break;
             default: range_error("unknown stage");
@@ -394,7 +381,6 @@ int vinf_engine_forward(vinf_engine* e, double t, void* stream) {
         for (uint32_t b = 0; b < e->blocks.size(); ++b) {
             e->stage_stub(b, s);
             e->stage_conv(b, s);
-            e->stage_gn_sqdev(b, s);
             e->stage_gn_apply(b, s);
             e->stage_attention(b, t, s);
         }

@@ -1,11 +1,18 @@
 // Persistent, warp-specialised tcgen05 GEMM (sm_100a). See gemm_tc.cuh for the contract.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread issues
-// tcgen05.mma), warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> registers ->
-// bias/residual/convert -> global). Operand tiles are 128 x 64 (A) and BN x 64 (B) bf16,
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread issues
+// tcgen05.mma), warp 2 = TMEM allocator, warps 4..11 = epilogue (TMEM -> registers ->
+// bias/residual/convert -> global): two warps per TMEM lane quadrant, alternating
+// 32-column chunks of each tile. Operand tiles are 128 x 64 (A) and BN x 64 (B) bf16,
 // TMA-loaded with 128B swizzle into a STAGES-deep mbarrier ring. The fp32 accumulator
 // lives in TMEM, double-buffered (2 x BN columns) so the epilogue of tile i overlaps
 // the main loop of tile i+1.
+//
+// Epilogue: per 32-column chunk, tcgen05.ld gives each lane one accumulator row; the warp
+// transposes the 32x32 block through padded shared memory (conflict-free 16 B accesses)
+// so residual loads and output stores are row-coalesced (8 lanes x 4 columns per row,
+// 4 rows per instruction). The next chunk's residual is prefetched (all 8 requests in
+// flight) while the current chunk is stored. Interior tiles take a branch-free path.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -13,6 +20,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gemm_tc.cuh"
@@ -23,24 +31,141 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
 constexpr uint32_t kABytes = kBM * kBK * 2;
+constexpr int kStgPitch = 36;  // floats per staged row (32 + 4 pad: conflict-free 16 B access)
+constexpr uint32_t kStgBytes = kEpiWarps * 32 * kStgPitch * 4;  // a 32x32 fp32 block per epilogue warp
 
 template <int BN>
 struct TileCfg {
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = std::min<int>(8, (200 * 1024) / kStageBytes);
+    static constexpr int kStages =
+        std::min<int>(8, (227 * 1024 - 1024 - 256 - kStgBytes) / kStageBytes);
     static constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;  // TMEM columns per buffer
     static constexpr uint32_t kTmemCols = 2 * kAccStride;
-    static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*bars*/;
+    static constexpr uint32_t kSmemBytes =
+        kStages * kStageBytes + 1024 /*align*/ + 256 /*bars*/ + kStgBytes;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dev::smem_u32(bar)) : "memory");
 }
 
-template <int BN>
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// Epilogue of one 128 x BN tile for the warp owning TMEM lane quadrant q (rows m0..m0+31).
+//   OBF: output (and residual) bf16, else fp32.   RES: residual present.
+template <int BN, bool OBF, bool RES>
+__device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int q, int lane,
+                                              uint32_t stg, int m0, int n0, int half) {
+    using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
+    constexpr int RW = OBF ? 2 : 4;  // residual words per 4 columns
+    const int tr = lane >> 3;        // transposed: row within each group of 4
+    const int tc = (lane & 7) * 4;   // transposed: first of 4 columns
+    const int n_lim = min(p.N, n0 + BN);
+    const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
+    const bool store = !(p.flags & kGemmFlagNoStore);
+    const T* res = static_cast<const T*>(p.res);
+    T* out = static_cast<T*>(p.out);
+    uint32_t rraw[8][RW];
+    auto load_res = [&](int c) {
+        if (!RES) return;
+        const int n = n0 + c + tc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t gm = int64_t(m0) + tr + 4 * i;
+            const bool ok = store && (full || (gm < p.M && n < n_lim));
+            const T* src = res + (ok ? gm * p.res_ld + n : 0);
+            if (OBF) {
+                uint2 w = make_uint2(0u, 0u);
+                if (ok) w = __ldg(reinterpret_cast<const uint2*>(src));
+                rraw[i][0] = w.x;
+                rraw[i][1 % RW] = w.y;
+            } else {
+                uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                if (ok) w = __ldg(reinterpret_cast<const uint4*>(src));
+                rraw[i][0] = w.x;
+                rraw[i][1 % RW] = w.y;
+                rraw[i][2 % RW] = w.z;
+                rraw[i][3 % RW] = w.w;
+            }
+        }
+    };
+    load_res(32 * half);
+#pragma unroll 1
+    for (int c = 32 * half; c < BN; c += 64) {
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(tmem_acc + (uint32_t(q * 32) << 16) + c, r);
+        dev::tmem_wait_ld();
+        if (n0 + c >= n_lim) continue;  // warp-uniform: past the matrix edge
+        const uint32_t srow = stg + uint32_t(lane * kStgPitch * 4);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sts128(srow + 16 * j, r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+        __syncwarp();
+        float cur[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float4 v = lds128(stg + uint32_t(((tr + 4 * i) * kStgPitch + tc) * 4));
+            cur[i][0] = v.x;
+            cur[i][1] = v.y;
+            cur[i][2] = v.z;
+            cur[i][3] = v.w;
+            if (RES) {
+                if (OBF) {
+                    cur[i][0] += __uint_as_float(rraw[i][0] << 16);
+                    cur[i][1] += __uint_as_float(rraw[i][0] & 0xFFFF0000u);
+                    cur[i][2] += __uint_as_float(rraw[i][1 % RW] << 16);
+                    cur[i][3] += __uint_as_float(rraw[i][1 % RW] & 0xFFFF0000u);
+                } else {
+                    cur[i][0] += __uint_as_float(rraw[i][0]);
+                    cur[i][1] += __uint_as_float(rraw[i][1 % RW]);
+                    cur[i][2] += __uint_as_float(rraw[i][2 % RW]);
+                    cur[i][3] += __uint_as_float(rraw[i][3 % RW]);
+                }
+            }
+        }
+        __syncwarp();
+        if (c + 64 < BN && n0 + c + 64 < n_lim) load_res(c + 64);  // prefetch this warp's next chunk
+        if (!store) continue;
+        const int n = n0 + c + tc;
+        float b4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (p.bias && n < n_lim) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n));
+            b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t gm = int64_t(m0) + tr + 4 * i;
+            if (!full && (gm >= p.M || n >= n_lim)) continue;
+            T* dst = out + gm * p.out_ld + n;
+            const float y0 = cur[i][0] + b4[0], y1 = cur[i][1] + b4[1];
+            const float y2 = cur[i][2] + b4[2], y3 = cur[i][3] + b4[3];
+            if (OBF) {
+                const __nv_bfloat162 lo2 = __floats2bfloat162_rn(y0, y1);
+                const __nv_bfloat162 hi2 = __floats2bfloat162_rn(y2, y3);
+                *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<const uint32_t*>(&lo2),
+                                                            *reinterpret_cast<const uint32_t*>(&hi2));
+            } else {
+                *reinterpret_cast<float4*>(dst) = make_float4(y0, y1, y2, y3);
+            }
+        }
+    }
+}
+
+template <int BN, bool OBF, bool RES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
     using Cfg = TileCfg<BN>;
@@ -78,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             dev::mbar_init(&tfull[i], 1);
-            dev::mbar_init(&tempty[i], 4);
+            dev::mbar_init(&tempty[i], kEpiWarps);
         }
         dev::fence_barrier_init();
     }
@@ -142,102 +267,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ===== Epilogue =====
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
-        const int row_in_tile = q * 32 + lane;
+        const int q = warp & 3;            // TMEM lane quadrant this warp may access
+        const int half = (warp - 4) >> 2;  // which alternate 32-column chunks it takes
+        const uint32_t stg =
+            dev::smem_u32(smem + S * Cfg::kStageBytes + 256) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const uint32_t acc = local & 1;
-            const int m0 = (tile / n_tiles) * kBM;
-            const int n0 = (tile % n_tiles) * BN;
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
-            const int64_t gm = int64_t(m0) + row_in_tile;
-            const bool row_ok = gm < p.M;
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                dev::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * Cfg::kAccStride + c,
-                                        r);
-                dev::tmem_wait_ld();
-                const int n_base = n0 + c;
-                const int n_lim = min(p.N, n0 + BN);
-                if (!row_ok || n_base >= n_lim) continue;
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                const bool full_chunk = (n_base + 32 <= n_lim);
-                if (full_chunk) {
-                    if (p.bias) {
-                        const float4* b4 = reinterpret_cast<const float4*>(p.bias + n_base);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 b = __ldg(b4 + j);
-                            v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
-                        }
-                    }
-                    if (p.res) {
-                        if (p.res_bf16) {
-                            const uint4* r4 = reinterpret_cast<const uint4*>(
-                                static_cast<const __nv_bfloat16*>(p.res) + gm * p.res_ld + n_base);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const uint4 w = __ldg(r4 + j);
-                                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                                for (int h = 0; h < 4; ++h) {
-                                    v[8 * j + 2 * h] += __uint_as_float(ws[h] << 16);
-                                    v[8 * j + 2 * h + 1] += __uint_as_float(ws[h] & 0xFFFF0000u);
-                                }
-                            }
-                        } else {
-                            const float4* r4 = reinterpret_cast<const float4*>(
-                                static_cast<const float*>(p.res) + gm * p.res_ld + n_base);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const float4 w = __ldg(r4 + j);
-                                v[4 * j] += w.x; v[4 * j + 1] += w.y; v[4 * j + 2] += w.z; v[4 * j + 3] += w.w;
-                            }
-                        }
-                    }
-                    if (p.out_bf16) {
-                        uint4* o4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
-                                                             gm * p.out_ld + n_base);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            uint32_t w[4];
-#pragma unroll
-                            for (int h = 0; h < 4; ++h) {
-                                const __nv_bfloat162 b2 =
-                                    __floats2bfloat162_rn(v[8 * j + 2 * h], v[8 * j + 2 * h + 1]);
-                                w[h] = *reinterpret_cast<const uint32_t*>(&b2);
-                            }
-                            o4[j] = make_uint4(w[0], w[1], w[2], w[3]);
-                        }
-                    } else {
-                        float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
-                                                               gm * p.out_ld + n_base);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                    }
-                } else {
-                    for (int j = 0; j < 32 && n_base + j < n_lim; ++j) {
-                        const int64_t n = n_base + j;
-                        float x = v[j];
-                        if (p.bias) x += p.bias[n];
-                        if (p.res) {
-                            x += p.res_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(
-                                                  p.res)[gm * p.res_ld + n])
-                                            : static_cast<const float*>(p.res)[gm * p.res_ld + n];
-                        }
-                        if (p.out_bf16)
-                            static_cast<__nv_bfloat16*>(p.out)[gm * p.out_ld + n] =
-                                __float2bfloat16_rn(x);
-                        else
-                            static_cast<float*>(p.out)[gm * p.out_ld + n] = x;
-                    }
-                }
-            }
+            epilogue_tile<BN, OBF, RES>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
+                                        (tile / n_tiles) * kBM + q * 32, (tile % n_tiles) * BN, half);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -266,12 +306,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 int g_num_sms = 0;
 
-template <int BN>
-int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
+template <int BN, bool OBF, bool RES>
+int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     using Cfg = TileCfg<BN>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>,
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(Cfg::kSmemBytes));
         if (e != cudaSuccess) return int(e);
@@ -285,8 +325,18 @@ int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     }
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
     const int grid = std::max(1, std::min(tiles, g_num_sms));
-    gemm_tc_kernel<BN><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
+    gemm_tc_kernel<BN, OBF, RES><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
     return int(cudaGetLastError());
+}
+
+template <int BN>
+int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
+    const bool res = p.res != nullptr;
+    if (res && p.res_bf16 != p.out_bf16) return int(cudaErrorInvalidValue);
+    if (p.out_bf16) return res ? launch_cfg<BN, true, true>(maps, p, stream)
+                               : launch_cfg<BN, true, false>(maps, p, stream);
+    return res ? launch_cfg<BN, false, true>(maps, p, stream)
+               : launch_cfg<BN, false, false>(maps, p, stream);
 }
 
 }  // namespace
@@ -322,7 +372,7 @@ int gemm_pick_block_n(int N) {
 }
 
 int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream) {
-    if (p.M <= 0 || p.N <= 0 || p.K <= 0 || p.nseg <= 0 || p.nseg > kGemmMaxSeg)
+    if (p.M <= 0 || p.N <= 0 || p.N % 8 != 0 || p.K <= 0 || p.nseg <= 0 || p.nseg > kGemmMaxSeg)
         return int(cudaErrorInvalidValue);
     switch (block_n) {
         case 256: return launch<256>(maps, p, stream);

@@ -38,7 +38,10 @@ struct GemmParams {
     void* out;
     int64_t out_ld;
     int32_t out_bf16;
+    int32_t flags;  // kGemmFlag* (diagnostics)
 };
+
+constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic
 
 struct GemmMaps {
     CUtensorMap a[2];

@@ -19,6 +19,7 @@ namespace vinf {
 namespace {
 
 constexpr int kMaxBlocksPerSm = 2;
+constexpr uint32_t kScratchRows = 1024;  // matches the engine layout's kScratchBlocks
 
 template <int VEC, bool BF16>
 __device__ __forceinline__ void load_vec(const void* base, uint64_t idx, float (&v)[VEC]) {
@@ -87,20 +88,102 @@ __global__ void group_sums_kernel(const void* __restrict__ x, uint64_t rows, uin
         partial[uint64_t(blockIdx.x) * groups + g] = sh[g];
 }
 
-__global__ void group_combine_kernel(const double* __restrict__ partial, uint32_t nblocks,
-                                     uint32_t groups, double* __restrict__ sums, int accumulate) {
-    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups;
-         g += gridDim.x * blockDim.x) {
-        double s = accumulate ? sums[g] : 0.0;
-        for (uint32_t b = 0; b < nblocks; ++b) s += partial[uint64_t(b) * groups + g];
-        sums[g] = s;
+// sums[g] (+)= sum_b partial[b][g]: one block per output, strided per-thread sums then a
+// fixed-shape tree (deterministic for a given nblocks).
+__global__ void __launch_bounds__(256)
+    group_combine_kernel(const double* __restrict__ partial, uint32_t nblocks, uint32_t groups,
+                         double* __restrict__ sums, int accumulate) {
+    __shared__ double red[256];
+    const uint32_t g = blockIdx.x;
+    double s = 0.0;
+    for (uint32_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[uint64_t(b) * groups + g];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) sums[g] = (accumulate ? sums[g] : 0.0) + red[0];
 }
 
 __global__ void group_finalize_kernel(const double* __restrict__ sums, double count,
                                       uint32_t groups, double* __restrict__ stats) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g < groups) stats[g] = sums[g] / count;
+}
+
+// One streaming pass computing both per-group sum and sum of squares. Thread keeps VEC
+// channels; 4 rows in flight per iteration (16 B loads) for memory-level parallelism;
+// per-channel fp32 partials -> smem -> per-group f64 partial per block (no atomics;
+// combined in block order by group_combine_kernel -> deterministic).
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+    group_moments_partial_kernel(const void* __restrict__ x, uint64_t rows, uint32_t C,
+                                 uint32_t groups, double* __restrict__ partial /* [grid][2G] */) {
+    constexpr int VEC = 8, UNR = 4;
+    extern __shared__ float shm[];  // [R][2][C]
+    const uint32_t CC = C / VEC;
+    const uint32_t R = blockDim.x / CC;
+    const uint32_t cc = threadIdx.x % CC;
+    const uint32_t rl = threadIdx.x / CC;
+    float s[VEC], q[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) s[k] = q[k] = 0.f;
+    if (rl < R) {
+        const uint64_t rstride = uint64_t(gridDim.x) * R;
+        uint64_t r = uint64_t(blockIdx.x) * R + rl;
+        for (; r + (UNR - 1) * rstride < rows; r += UNR * rstride) {
+            float v[UNR][VEC];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) load_vec<VEC, BF16>(x, (r + u * rstride) * C + cc * VEC, v[u]);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) {
+                    s[k] += v[u][k];
+                    q[k] = fmaf(v[u][k], v[u][k], q[k]);
+                }
+        }
+        for (; r < rows; r += rstride) {
+            float v[VEC];
+            load_vec<VEC, BF16>(x, r * C + cc * VEC, v);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                s[k] += v[k];
+                q[k] = fmaf(v[k], v[k], q[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            shm[(rl * 2 + 0) * C + cc * VEC + k] = s[k];
+            shm[(rl * 2 + 1) * C + cc * VEC + k] = q[k];
+        }
+    }
+    __syncthreads();
+    // per group: f64 sum over its channels and the R row lanes
+    const uint32_t gs = C / groups;
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (uint32_t l = 0; l < R; ++l)
+            for (uint32_t ch = g * gs; ch < (g + 1) * gs; ++ch) {
+                a += double(shm[(l * 2 + 0) * C + ch]);
+                b += double(shm[(l * 2 + 1) * C + ch]);
+            }
+        partial[uint64_t(blockIdx.x) * 2 * groups + g] = a;
+        partial[uint64_t(blockIdx.x) * 2 * groups + groups + g] = b;
+    }
+}
+
+// (sum, sum of squares) -> (mean, variance) in f64.
+__global__ void group_moments_kernel(const double* __restrict__ sums, double count,
+                                     uint32_t groups, double* __restrict__ stats) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < groups) {
+        const double m = sums[g] / count;
+        const double v = sums[groups + g] / count - m * m;
+        stats[g] = m;
+        stats[groups + g] = v > 0.0 ? v : 0.0;
+    }
 }
 
 template <int VEC, bool IN_BF16, bool OUT_BF16, bool SPLIT>
@@ -127,12 +210,20 @@ __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, ui
         bt[k] = beta[ch];
     }
     const uint64_t rstride = uint64_t(gridDim.x) * R;
-    for (uint64_t r = uint64_t(blockIdx.x) * R + rl; r < rows; r += rstride) {
+    constexpr int UNR = 4;  // rows in flight per lane
+    for (uint64_t r0 = uint64_t(blockIdx.x) * R + rl; r0 < rows; r0 += UNR * rstride) {
+      float vin[UNR][VEC];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+          if (r0 + u * rstride < rows) load_vec<VEC, IN_BF16>(x, (r0 + u * rstride) * C + cc * VEC, vin[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint64_t r = r0 + u * rstride;
+        if (r >= rows) break;
         const uint64_t idx = r * C + cc * VEC;
         float v[VEC];
-        load_vec<VEC, IN_BF16>(x, idx, v);
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) v[k] = fmaf(v[k] - mu[k], sc[k], bt[k]);
+        for (int k = 0; k < VEC; ++k) v[k] = fmaf(vin[u][k] - mu[k], sc[k], bt[k]);
         if (OUT_BF16) {
             if (VEC == 8) {
                 uint32_t w[4];
@@ -170,6 +261,7 @@ __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, ui
                 for (int k = 0; k < VEC; ++k) { hi[idx + k] = h[k]; lo[idx + k] = l[k]; }
             }
         }
+      }
     }
 }
 
@@ -211,7 +303,7 @@ int launch_group_sums(const void* x, bool bf16, uint64_t rows, uint32_t C, uint3
     } else {
         grid = 0;
     }
-    group_combine_kernel<<<(groups + 127) / 128, 128, 0, s>>>(scratch, uint32_t(grid), groups, sums,
+    group_combine_kernel<<<groups, 256, 0, s>>>(scratch, uint32_t(grid), groups, sums,
                                                              accumulate ? 1 : 0);
     return int(cudaGetLastError());
 }
@@ -219,6 +311,39 @@ int launch_group_sums(const void* x, bool bf16, uint64_t rows, uint32_t C, uint3
 int launch_group_finalize(const double* sums, double count, uint32_t groups, double* stats,
                           cudaStream_t s) {
     group_finalize_kernel<<<(groups + 127) / 128, 128, 0, s>>>(sums, count, groups, stats);
+    return int(cudaGetLastError());
+}
+
+int launch_group_moment_sums(const void* x, bool bf16, uint64_t rows, uint32_t C,
+                             uint32_t groups, double* sums, double* scratch, cudaStream_t s) {
+    if (groups == 0 || C % groups != 0 || C % 8 != 0 || C / 8 > 256)
+        return int(cudaErrorInvalidValue);
+    const uint32_t CC = C / 8;
+    const uint32_t R = 256 / CC;
+    const int block = int(CC * R);
+    int grid = int(std::min<uint64_t>((rows + R - 1) / R, uint64_t(num_sms()) * 4));
+    grid = std::min<int>(grid, int(kScratchRows / 2));
+    if (grid < 1) grid = 1;
+    const size_t shm = sizeof(float) * 2 * C * R;
+    if (shm > 48 * 1024) {
+        cudaFuncSetAttribute(group_moments_partial_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+        cudaFuncSetAttribute(group_moments_partial_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm));
+    }
+    if (bf16)
+        group_moments_partial_kernel<true><<<grid, block, shm, s>>>(x, rows, C, groups, scratch);
+    else
+        group_moments_partial_kernel<false><<<grid, block, shm, s>>>(x, rows, C, groups, scratch);
+    // combine [grid][2G] in block order
+    group_combine_kernel<<<2 * groups, 256, 0, s>>>(scratch, uint32_t(grid),
+                                                                  2 * groups, sums, 0);
+    return int(cudaGetLastError());
+}
+
+int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
+                         cudaStream_t s) {
+    group_moments_kernel<<<(groups + 127) / 128, 128, 0, s>>>(sums, count, groups, stats);
     return int(cudaGetLastError());
 }
 
@@ -233,7 +358,7 @@ int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, u
     const int block = block_for(C, vec, &R);
     if (block == 0) return int(cudaErrorInvalidValue);
     int grid = int((rows + R - 1) / R);
-    const int cap = num_sms() * 8;
+    const int cap = num_sms() * 4;
     if (grid > cap) grid = cap;
     const bool split = hi != nullptr;
 #define GA(V, IB, OB, SP)                                                                     \

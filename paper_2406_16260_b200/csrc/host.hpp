@@ -29,6 +29,7 @@ struct Error : std::runtime_error {
     throw Error(VINF_ERR_TRANSPORT, m);
 }
 void cuda_check(int err, const char* what);
+extern int g_gemm_debug_flags;  // ORed into every GEMM's flags (diagnostics only)
 
 // ---- plan.cpp (pure host) ----
 std::vector<uint32_t> build_local_window(uint32_t a, uint32_t frames, uint32_t n_local);
@@ -40,17 +41,27 @@ void predict_sync_traffic(uint32_t frames, uint32_t workers, uint32_t halo, uint
                           uint32_t worker, uint64_t frame_bytes, uint64_t out[3]);
 void predict_groupnorm_traffic(uint32_t frames, uint32_t workers, uint32_t groups, uint64_t out[3]);
 
-// Host token table for nq queries (kMaxTokens slots each).
+// Host token table for nq queries (kMaxTokens slots each): the reference's explicit
+// token lists (window first, then globals; duplicates kept) plus, per block of kQBlock
+// queries, the sorted distinct K/V frames they touch and each token's column in it.
 struct HostTokens {
     std::vector<uint16_t> rows;
     std::vector<uint8_t> biased;
     std::vector<uint16_t> count;
-    uint32_t nq = 0;
+    std::vector<uint8_t> col;
+    std::vector<uint16_t> kv_frames;
+    std::vector<uint16_t> kv_count;
+    uint32_t nq = 0, nqb = 0;
+    bool kv_ok = true;
     void resize(uint32_t n) {
         nq = n;
+        nqb = (n + kQBlock - 1) / kQBlock;
         rows.assign(size_t(n) * kMaxTokens, 0);
         biased.assign(size_t(n) * kMaxTokens, 0);
         count.assign(n, 0);
+        col.assign(size_t(n) * kMaxTokens, 0);
+        kv_frames.assign(size_t(nqb) * kKvMax, 0);
+        kv_count.assign(nqb, 0);
     }
     void push(uint32_t a, uint32_t row, bool b) {
         const uint16_t k = count[a];
@@ -59,6 +70,12 @@ struct HostTokens {
         biased[size_t(a) * kMaxTokens + k] = b ? 1 : 0;
         count[a] = k + 1;
     }
+    // Builds the per-block K/V lists; call after all push()es.
+    void finalize();
+    // One device blob: rows | biased | col | count | kv_frames | kv_count.
+    size_t blob_bytes() const;
+    void pack(uint8_t* dst) const;
+    TokenTable view(const uint8_t* dev_base) const;
 };
 
 // Device copy of a HostTokens table (one allocation).

@@ -33,6 +33,13 @@ int launch_group_sums(const void* x, bool bf16, uint64_t rows, uint32_t C, uint3
 // stats[g] = sums[g] / count  (count = elements per group, across all clips)
 int launch_group_finalize(const double* sums, double count, uint32_t groups, double* stats,
                           cudaStream_t s);
+// One pass: sums = [sum x (groups) | sum x^2 (groups)] over the clip (C % 8 == 0, C <= 2048).
+// scratch: >= 2 * groups * min(4 * SMs, 512) doubles.
+int launch_group_moment_sums(const void* x, bool bf16, uint64_t rows, uint32_t C,
+                             uint32_t groups, double* sums, double* scratch, cudaStream_t s);
+// sums = [sum x (groups) | sum x^2 (groups)] -> stats = [mean | variance]
+int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
+                         cudaStream_t s);
 // y = gamma * (x - mean_g) / sqrt(var_g + eps) + beta; optional hi/lo split output.
 int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
                        const double* means, const double* vars, const float* gamma,
@@ -41,17 +48,30 @@ int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, u
 
 // ---- attention.cu ----
 constexpr int kMaxTokens = 160;  // n_local + 1 + n_global upper bound
+constexpr int kQBlock = 32;      // queries per tensor-core attention CTA
+constexpr int kKvMax = 64;       // distinct K/V frames per query block (tensor-core path)
 
 struct TokenTable {
-    const uint16_t* rows;   // [nq][kMaxTokens] key/value frame row (in QKV frame units)
-    const uint8_t* biased;  // [nq][kMaxTokens] 1 if this token's logit gets +bias
-    const uint16_t* count;  // [nq]
+    const uint16_t* rows;       // [nq][kMaxTokens] key/value frame row (in QKV frame units)
+    const uint8_t* biased;      // [nq][kMaxTokens] 1 if this token's logit gets +bias
+    const uint16_t* count;      // [nq]
+    const uint8_t* col;         // [nq][kMaxTokens] token -> column of its block's K/V list
+    const uint16_t* kv_frames;  // [nqb][kKvMax] K/V frame row of each column
+    const uint16_t* kv_count;   // [nqb]
+    int kv_ok;                  // every block's K/V list fits kKvMax
 };
 
 // (hi/lo non-null: only the split bf16 planes are written, the fp32-mode GEMM operand)
 // ctx[a, p, :] = softmax-attention of query frame a at position p over its token list.
 // qkv: [(frames) * HW, 3C] with Q in cols [0,C), K in [C,2C), V in [2C,3C);
 // query frame a lives at QKV frame row q_frame0 + a. ctx: [nq * HW, C].
+// attention_tc.cu: bf16 tensor-core core (head dim % 64 == 0, <= kKvMax K/V frames per
+// 32-query block); launch_attention_core dispatches to it when supported.
+bool attention_tc_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
+int launch_attention_core_tc(const void* qkv, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
+                             uint32_t q_frame0, TokenTable tt, float scale, float bias, void* ctx,
+                             cudaStream_t s);
+
 int launch_attention_core(const void* qkv, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
                           uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale, float bias,
                           void* ctx, bool ctx_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,

@@ -34,19 +34,14 @@ int num_sms() {
 // ---- device helpers ----------------------------------------------------------
 
 void DevTokens::upload(const HostTokens& h, cudaStream_t s) {
-    const size_t nr = h.rows.size() * sizeof(uint16_t), nb = h.biased.size(),
-                 nc = h.count.size() * sizeof(uint16_t);
-    if (!buf) cuda_check(cudaMallocAsync(&buf, nr + nb + nc + 64, s), "cudaMallocAsync(tokens)");
-    uint8_t* p = static_cast<uint8_t*>(buf);
-    cuda_check(cudaMemcpyAsync(p, h.rows.data(), nr, cudaMemcpyHostToDevice, s), "tokens");
-    cuda_check(cudaMemcpyAsync(p + nr, h.biased.data(), nb, cudaMemcpyHostToDevice, s), "tokens");
-    cuda_check(cudaMemcpyAsync(p + nr + nb, h.count.data(), nc, cudaMemcpyHostToDevice, s),
-               "tokens");
-    // pageable sources: make sure the host vectors may be released afterwards
+    const size_t n = h.blob_bytes();
+    std::vector<uint8_t> blob(n);
+    h.pack(blob.data());
+    if (!buf) cuda_check(cudaMallocAsync(&buf, n, s), "cudaMallocAsync(tokens)");
+    cuda_check(cudaMemcpyAsync(buf, blob.data(), n, cudaMemcpyHostToDevice, s), "tokens");
+    // pageable source: the host blob must outlive the copy
     cuda_check(cudaStreamSynchronize(s), "tokens sync");
-    tt.rows = reinterpret_cast<const uint16_t*>(p);
-    tt.biased = p + nr;
-    tt.count = reinterpret_cast<const uint16_t*>(p + nr + nb);
+    tt = h.view(static_cast<const uint8_t*>(buf));
 }
 
 void DevTokens::release() {
@@ -73,6 +68,8 @@ void DevMat::release() {
 }
 
 // ---- GEMM dispatch ------------------------------------------------------------
+
+int g_gemm_debug_flags = 0;
 
 void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
           const std::vector<int64_t>& b_rows, int64_t M, int64_t N, const Epilogue& ep, bool split,
@@ -120,6 +117,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         p.out = ep.out;
         p.out_ld = ep.out_ld;
         p.out_bf16 = ep.out_bf16;
+        p.flags = g_gemm_debug_flags;
         cuda_check(gemm_tc_launch(maps, p, bn, s), "gemm_tc_launch");
     }
 }
@@ -259,8 +257,10 @@ void attention_generic(const void* src, vinf_dtype dt, uint32_t frames, uint32_t
     e1.out_ld = 3 * C;
     e1.out_bf16 = !f32;
     gemm(A.op, {0}, p->wqkv, {0}, int64_t(rows), 3 * C, e1, f32, s);
+    HostTokens tk = tok;
+    tk.finalize();
     DevTokens dt_tok;
-    dt_tok.upload(tok, s);
+    dt_tok.upload(tk, s);
     const uint64_t qrows = uint64_t(nq) * hw;
     TmpBuf ctx(qrows * C * 4, s);  // bf16 ctx or hi+lo planes
     auto* hi = static_cast<__nv_bfloat16*>(ctx.p);

@@ -84,6 +84,71 @@ void predict_groupnorm_traffic(uint32_t frames, uint32_t workers, uint32_t group
 }
 
 // ---------------------------------------------------------------------------
+// Token tables
+
+void HostTokens::finalize() {
+    kv_ok = true;
+    for (uint32_t qb = 0; qb < nqb; ++qb) {
+        std::vector<uint16_t> uniq;
+        const uint32_t a1 = std::min<uint32_t>(nq, (qb + 1) * kQBlock);
+        for (uint32_t a = qb * kQBlock; a < a1; ++a)
+            for (uint32_t i = 0; i < count[a]; ++i) uniq.push_back(rows[size_t(a) * kMaxTokens + i]);
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        if (uniq.size() > size_t(kKvMax)) {
+            kv_ok = false;
+            kv_count[qb] = 0;
+            continue;
+        }
+        kv_count[qb] = uint16_t(uniq.size());
+        for (size_t r = 0; r < uniq.size(); ++r) kv_frames[size_t(qb) * kKvMax + r] = uniq[r];
+        for (uint32_t a = qb * kQBlock; a < a1; ++a)
+            for (uint32_t i = 0; i < count[a]; ++i) {
+                const uint16_t row = rows[size_t(a) * kMaxTokens + i];
+                col[size_t(a) * kMaxTokens + i] =
+                    uint8_t(std::lower_bound(uniq.begin(), uniq.end(), row) - uniq.begin());
+            }
+    }
+}
+
+size_t HostTokens::blob_bytes() const {
+    return rows.size() * 2 + biased.size() + col.size() + count.size() * 2 +
+           kv_frames.size() * 2 + kv_count.size() * 2 + 64;
+}
+
+void HostTokens::pack(uint8_t* dst) const {
+    size_t o = 0;
+    auto put = [&](const void* src, size_t n) {
+        if (n) std::memcpy(dst + o, src, n);
+        o += n;
+    };
+    put(rows.data(), rows.size() * 2);
+    put(kv_frames.data(), kv_frames.size() * 2);
+    put(count.data(), count.size() * 2);
+    put(kv_count.data(), kv_count.size() * 2);
+    put(biased.data(), biased.size());
+    put(col.data(), col.size());
+}
+
+TokenTable HostTokens::view(const uint8_t* base) const {
+    TokenTable t{};
+    size_t o = 0;
+    t.rows = reinterpret_cast<const uint16_t*>(base + o);
+    o += rows.size() * 2;
+    t.kv_frames = reinterpret_cast<const uint16_t*>(base + o);
+    o += kv_frames.size() * 2;
+    t.count = reinterpret_cast<const uint16_t*>(base + o);
+    o += count.size() * 2;
+    t.kv_count = reinterpret_cast<const uint16_t*>(base + o);
+    o += kv_count.size() * 2;
+    t.biased = base + o;
+    o += biased.size();
+    t.col = base + o;
+    t.kv_ok = kv_ok ? 1 : 0;
+    return t;
+}
+
+// ---------------------------------------------------------------------------
 // Engine layout
 
 namespace {
@@ -150,6 +215,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
                 tok[b].push(a, ha + g - start, b == 0);
             for (uint32_t j = 0; j < d.n_global; ++j) tok[b].push(a, g_frame[j], b == 1);
         }
+        tok[b].finalize();
     }
 
     // Workspace regions.
@@ -176,9 +242,8 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     off_stats = take(sizeof(double) * 2 * d.groups);
     scratch_elems = uint64_t(kScratchBlocks) * d.groups;
     off_scratch = take(sizeof(double) * scratch_elems);
-    const uint64_t tbytes = uint64_t(f_clip) * kMaxTokens * 3 + uint64_t(f_clip) * 2;
-    off_tok[0] = take(tbytes);
-    off_tok[1] = take(tbytes);
+    off_tok[0] = take(tok[0].blob_bytes());
+    off_tok[1] = take(tok[1].blob_bytes());
     total = off;
 
     build_exchanges();

@@ -155,15 +155,15 @@ class LocalGroup:
                 dst_ws, src_ws = by_worker[w].ws, by_worker[x.peer].ws
                 dst_ws[x.offset:x.offset + x.bytes].copy_(src_ws[s.offset:s.offset + s.bytes])
 
-    def allreduce_sums(self, engines: list[ClipEngine], k: int) -> None:
+    def allreduce_sums(self, engines: list[ClipEngine]) -> None:
         if len(engines) == 1:
             return
         ordered = sorted(engines, key=lambda e: e.layout.desc.worker)
-        total = ordered[0].gn_sums[k].clone()
+        total = ordered[0].gn_sums.clone()
         for e in ordered[1:]:
-            total += e.gn_sums[k]
+            total += e.gn_sums
         for e in ordered:
-            e.gn_sums[k].copy_(total)
+            e.gn_sums.copy_(total)
 
 
 class DistGroup:
@@ -178,16 +178,16 @@ class DistGroup:
                 for x in e.layout.exchange(stage)]
         self.t.exchange(msgs)
 
-    def allreduce_sums(self, engines: list[ClipEngine], k: int) -> None:
+    def allreduce_sums(self, engines: list[ClipEngine]) -> None:
         (e,) = engines
-        self.t.allreduce_sum_(e.gn_sums[k])
+        self.t.allreduce_sum_(e.gn_sums)
 
 
 def forward(t: float, engines: list[ClipEngine], group=None) -> None:
     """All blocks of eps_theta_worker for every engine in `engines` (pipeline.cpp:150-170):
-    stub -> [conv halo sync] -> conv + residual + GN partial sums -> [sum all-reduce]
-    -> GN sq-dev partials -> [sum all-reduce] -> GN apply -> [attention halo + global
-    sync] -> dual-scope attention + residual."""
+    stub -> [conv halo sync] -> conv + residual with fused GN (sum, sum^2) partials ->
+    [one all-reduce of 2*groups f64] -> GN apply -> [attention halo + global sync] ->
+    dual-scope attention + residual."""
     blocks = engines[0].layout.desc.blocks
     if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1:
         engines[0].forward_single(t)
@@ -199,10 +199,7 @@ def forward(t: float, engines: list[ClipEngine], group=None) -> None:
         group.exchange(engines, _lib.VINF_XCHG_CONV)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_CONV, t)
-        group.allreduce_sums(engines, 0)
-        for e in engines:
-            e.stage(b, _lib.VINF_STAGE_GN_SQDEV, t)
-        group.allreduce_sums(engines, 1)
+        group.allreduce_sums(engines)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_GN_APPLY, t)
         group.exchange(engines, _lib.VINF_XCHG_ATTN)

@@ -1,0 +1,18 @@
+"""GEMM microbenchmark (diagnostic): main loop vs epilogue cost at the bench shapes.
+    python scripts/gemm_micro.py [shape ...]   (conv, qkv, o, sq8k; default all)"""
+import ctypes as C, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2406_16260_b200 import _lib
+L = _lib.load()
+M = 24 * 40 * 64
+SHAPES = {"conv": (640, 640, 3, 1), "qkv": (1920, 640, 1, 0), "o": (640, 640, 1, 1), "sq8k": (8192, 8192, 1, 0)}
+names = [a for a in sys.argv[1:] if a in SHAPES] or list(SHAPES)
+iters = 3 if "--once" in sys.argv else 20
+for name in names:
+    N, K, nseg, res = SHAPES[name]
+    m = M if name != "sq8k" else 8192
+    for flags in ((0,) if "--once" in sys.argv else (0, 1)):
+        ms = C.c_float()
+        _lib.check(L.vinf_gemm_bench(m, N, K, nseg, flags, res, iters, C.byref(ms)))
+        tf = 2.0 * m * N * K * nseg / (ms.value * 1e-3) / 1e12
+        print(f"{name:5s} M={m} N={N} K={K}x{nseg} res={res} nostore={flags}: {ms.value*1000:8.1f} us  {tf:7.1f} TFLOP/s")

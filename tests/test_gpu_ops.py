@@ -172,6 +172,23 @@ def test_attention_full_and_degenerate(ops, oracle):
     assert normwise(deg, want) <= TOL_F32
 
 
+@pytest.mark.parametrize("F,C,heads,nl,ng", [(80, 64, 1, 16, 16), (40, 128, 2, 16, 16),
+                                              (64, 128, 1, 32, 24), (33, 64, 1, 4, 3)])
+def test_dual_scope_tensor_core_path(ops, oracle, F, C, heads, nl, ng):
+    # bf16 mode with head dim % 64 == 0 runs the mma.sync core; several 32-query blocks,
+    # ragged last block, multi-head, wide windows.
+    x = oracle.tensor_from_seed((F, 2, 2, C), 70)
+    bp = oracle.build_block(C, weight_seed=71)
+    sc = float(np.float32(1) / np.sqrt(np.float32(C // heads)))
+    for t in (700.0, 900.0):
+        want = oracle.dual_scope(to_np(dev(x, torch.bfloat16)), t, bp.wq, bp.wk, bp.wv, bp.wo,
+                                 sc, nl, ng, 10.0, 800.0, heads=heads)
+        got = to_np(ops.dual_scope_reference(dev(x, torch.bfloat16), t,
+                                             _attn(ops, bp, C, heads=heads),
+                                             ops.DualScopeConfig(nl, ng, 10.0, 800.0)))
+        assert normwise(got, want) <= TOL_BF16, normwise(got, want)
+
+
 def test_t_star_is_strict(ops, oracle):
     F, H, W, C = 24, 2, 2, 32
     x = dev(oracle.tensor_from_seed((F, H, W, C), 60))
