@@ -1,18 +1,19 @@
 // Tensor-core dual-scope attention core for the bf16 mode (mma.sync m16n8k16 bf16 ->
 // fp32). Per spatial position p and block of 32 query frames:
 //
-//   S  = Q K^T            [32 x R]   over the head dim in 64-wide chunks (cp.async double
-//                                    buffer, ldmatrix from XOR-swizzled smem)
+//   S  = Q K^T            [32 x R]   over the head dim in 64-wide chunks
 //   P  = token softmax    [32 x R]   the reference's explicit token list per query
 //                                    (window then globals, duplicates kept, +bias on the
 //                                    flagged side): p_r = sum_{i: col_i = r} e^{l_i - m} / Z
 //   ctx = P V             [32 x d]   in 64-wide output chunks, staged through smem for
-//                                    128-byte row stores
+//                                    16-byte row stores
 //
 // R = the distinct K/V frames the block's queries touch (<= 64; window band + globals).
-// tcgen05 needs M >= 64 and this tile has M = 32 queries (24 at the VideoCrafter2 clip), so
-// the dense S/PV tiles run on the warp-level tensor path; the kernel is bound by reading
-// Q/K/V once and writing ctx once (SURVEY §7 "attention-core tile shape").
+// The kernel is bound by reading Q/K/V once and writing ctx once, so the
+// whole per-CTA load sequence (Q+K chunks of every head, then V chunks) streams through
+// one kStages-deep cp.async ring with a fixed prefetch distance; the V loads of a head
+// are in flight while its softmax runs. tcgen05 needs M >= 64 and this tile has M = 32
+// queries (24 at the VideoCrafter2 clip), so S and PV use the warp-level tensor path.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -24,11 +25,13 @@ namespace vinf {
 
 namespace {
 
-constexpr int kDC = 64;  // head-dim chunk (one 128-byte swizzle row)
-constexpr int kTcThreads = 128;
+constexpr int kDC = 64;        // head-dim chunk (one 128-byte swizzle row)
+constexpr int kTcWarps = 8;
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr int kStages = 4;     // cp.async ring depth (prefetch distance kStages - 1)
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-    // byte offset of 16B chunk `chunk` of a 128-byte row
+    // byte offset of 16B chunk `chunk` of a 128-byte row (XOR swizzle: ldmatrix conflict-free)
     return row * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
@@ -68,213 +71,237 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-struct TcSmem {
-    alignas(128) uint8_t q[2][kQBlock * 128];   // Q chunk (also output staging in phase 3)
-    alignas(128) uint8_t kv[2][kKvMax * 128];   // K chunk (phase 1) / V chunk (phase 3)
-    alignas(128) uint8_t pb[kQBlock * 128];     // P as bf16 (A operand of P V)
-    float s[kQBlock][kKvMax + 4];               // logits
-    float pf[kQBlock][kKvMax];                  // un-normalised weights (duplicates summed)
-    float zinv[kQBlock];
-    uint32_t qrow[kQBlock];                     // QKV row index of each query (this position)
-    uint32_t kvrow[kKvMax];                     // QKV row index of each K/V column
+// Dynamic smem layout (bytes), RP = padded K/V rows (multiple of 16, <= kKvMax):
+//   ring[kStages] : Q chunk (32 x 128 B) + K-or-V chunk (RP x 128 B)
+//   pb            : P as bf16, 32 x 128 B (A operand of P V)
+//   sp            : S, then P (fp32), 32 x (kKvMax + 4)
+//   ost           : output staging 32 x 128 B
+//   zinv[32], qrow[32], kvrow[kKvMax]
+struct Lay {
+    uint32_t stage, ring, pb, sp, ost, zinv, qrow, kvrow, total;
+    __host__ __device__ explicit Lay(uint32_t RP) {
+        stage = kQBlock * 128 + RP * 128;
+        ring = 0;
+        pb = ring + kStages * stage;
+        sp = pb + kQBlock * 128;
+        ost = sp + kQBlock * (kKvMax + 4) * 4;
+        zinv = ost + kQBlock * 128;
+        qrow = zinv + kQBlock * 4;
+        kvrow = qrow + kQBlock * 4;
+        total = kvrow + kKvMax * 4;
+    }
 };
 
 __global__ void __launch_bounds__(kTcThreads)
     attention_core_tc_kernel(const __nv_bfloat16* __restrict__ qkv, uint32_t HW, uint32_t C,
                              uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt,
                              float scale, float bias, __nv_bfloat16* __restrict__ ctx) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
+    extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t p = blockIdx.x, qb = blockIdx.y;
     const uint32_t a0 = qb * kQBlock;
     const uint32_t nqh = min(uint32_t(kQBlock), nq - a0);
     const uint32_t R = tt.kv_count[qb];
-    const uint32_t RP = (R + 15) & ~15u;  // padded K/V columns (multiple of 16)
-    const uint32_t NT = RP / 8;           // n8 tiles of S
+    const uint32_t RP = (R + 15) & ~15u;  // padded K/V rows (multiple of 16)
+    const Lay L(RP);
     const uint32_t d = C / heads;
+    const uint32_t nch = d / kDC;          // chunks per head and phase
+    const uint32_t nload = heads * 2 * nch;  // load sequence: per head, Q+K chunks then V chunks
     const uint64_t ld = 3ull * C;
+    uint32_t* qrow = reinterpret_cast<uint32_t*>(sm + L.qrow);
+    uint32_t* kvrow = reinterpret_cast<uint32_t*>(sm + L.kvrow);
+    float* sp = reinterpret_cast<float*>(sm + L.sp);
+    float* zinv = reinterpret_cast<float*>(sm + L.zinv);
+    constexpr int SP = kKvMax + 4;  // fp32 pitch of S / P rows
 
-    if (tid < kQBlock) sm.qrow[tid] = (q_frame0 + a0 + min(uint32_t(tid), nqh - 1)) * HW + p;
+    if (tid < kQBlock) qrow[tid] = (q_frame0 + a0 + min(uint32_t(tid), nqh - 1)) * HW + p;
     if (tid < kKvMax)
-        sm.kvrow[tid] = uint32_t(tt.kv_frames[qb * kKvMax + min(uint32_t(tid), R - 1)]) * HW + p;
+        kvrow[tid] = uint32_t(tt.kv_frames[qb * kKvMax + min(uint32_t(tid), R - 1)]) * HW + p;
     __syncthreads();
 
-    const uint32_t q_s = dev::smem_u32(sm.q[0]);
-    const uint32_t kv_s = dev::smem_u32(sm.kv[0]);
-    const uint32_t pb_s = dev::smem_u32(sm.pb);
-    const int mt = warp & 1;         // 16-row m tile of this warp
-    const int half = warp >> 1;      // which half of the n tiles
-
-    // loads of one 64-wide chunk: Q rows (phase 1 only) and K or V rows
-    auto load_chunk = [&](int buf, uint32_t col0, bool with_q, uint32_t kv_col0) {
-        if (with_q) {
-            for (int i = tid; i < kQBlock * 8; i += kTcThreads) {
-                const uint32_t r = i >> 3, c = i & 7;
-                cp_async16(q_s + buf * (kQBlock * 128) + swz(r, c),
-                           qkv + uint64_t(sm.qrow[r]) * ld + col0 + c * 8);
-            }
+    const uint32_t sbase = dev::smem_u32(sm);
+    // Each thread copies the same (row, 16 B chunk) of every Q / K / V chunk: Q is
+    // 32 rows x 8 chunks = one item per thread; K/V has RP rows x 8 = up to two.
+    static_assert(kQBlock * 8 == kTcThreads, "one Q item per thread");
+    const uint32_t it_r = tid >> 3, it_c = tid & 7;
+    const __nv_bfloat16* q_src = qkv + uint64_t(qrow[it_r]) * ld + it_c * 8;
+    const uint32_t q_dst = swz(it_r, it_c);
+    const bool kv0 = it_r < RP, kv1 = it_r + 32 < RP;  // never write past this CTA's RP rows
+    const __nv_bfloat16* kv_src0 = qkv + uint64_t(kvrow[min(it_r, RP - 1)]) * ld + it_c * 8;
+    const __nv_bfloat16* kv_src1 = qkv + uint64_t(kvrow[min(it_r + 32, RP - 1)]) * ld + it_c * 8;
+    const uint32_t kv_dst0 = kQBlock * 128 + swz(it_r, it_c), kv_dst1 = kQBlock * 128 + swz(it_r + 32, it_c);
+    auto issue = [&](uint32_t li) {  // load item li of the sequence into ring slot li % kStages
+        if (li < nload) {
+            const uint32_t h = li / (2 * nch), w = li % (2 * nch);
+            const bool qk = w < nch;
+            const uint32_t col = h * d + (qk ? w : w - nch) * kDC;
+            const uint32_t st = sbase + L.ring + (li % kStages) * L.stage;
+            if (qk) cp_async16(st + q_dst, q_src + col);
+            const uint32_t kvc = (qk ? C : 2 * C) + col;
+            if (kv0) cp_async16(st + kv_dst0, kv_src0 + kvc);
+            if (kv1) cp_async16(st + kv_dst1, kv_src1 + kvc);
         }
-        for (int i = tid; i < int(RP) * 8; i += kTcThreads) {
-            const uint32_t r = i >> 3, c = i & 7;
-            cp_async16(kv_s + buf * (kKvMax * 128) + swz(r, c),
-                       qkv + uint64_t(sm.kvrow[r]) * ld + kv_col0 + c * 8);
-        }
-        cp_commit();
+        cp_commit();  // always commit (possibly empty) so group counting stays uniform
     };
+    for (uint32_t li = 0; li < kStages - 1; ++li) issue(li);
 
+    const int mt = warp & 1;              // S: 16-row m tile;  PV: 16-row m tile
+    const int wq = warp >> 1;             // 0..3
+    const int NT = int(RP) / 8;           // n8 tiles of S (2..8)
+    uint32_t li = 0;
     for (uint32_t h = 0; h < heads; ++h) {
-        const uint32_t hc0 = h * d;
-        const uint32_t nch = d / kDC;
         // ---------------- phase 1: S = Q K^T ----------------
-        float acc[4][4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[j][k] = 0.f;
-        const int nt_per = int(NT) / 2;          // n tiles per warp (1..4)
-        const int nt0 = half * nt_per;
-        load_chunk(0, hc0, true, C + hc0);
-        for (uint32_t ch = 0; ch < nch; ++ch) {
-            if (ch + 1 < nch) {
-                load_chunk((ch + 1) & 1, hc0 + (ch + 1) * kDC, true, C + hc0 + (ch + 1) * kDC);
-                cp_wait<1>();
-            } else {
-                cp_wait<0>();
-            }
+        // warp: m tile mt (16 queries) x n8 tiles wq and wq + 4 of the RP key columns
+        float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        for (uint32_t ch = 0; ch < nch; ++ch, ++li) {
+            issue(li + kStages - 1);
+            cp_wait<kStages - 1>();
             __syncthreads();
-            const int buf = ch & 1;
-            const uint32_t qa = q_s + buf * (kQBlock * 128);
-            const uint32_t ka = kv_s + buf * (kKvMax * 128);
+            const uint32_t qa = sbase + L.ring + (li % kStages) * L.stage;
+            const uint32_t ka = qa + kQBlock * 128;
 #pragma unroll
             for (int kk = 0; kk < kDC / 16; ++kk) {
                 uint32_t a[4];
-                {
-                    const uint32_t row = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                    const uint32_t chunk = kk * 2 + (lane >> 4);
-                    ldsm_x4(qa + swz(row, chunk), a[0], a[1], a[2], a[3]);
-                }
+                ldsm_x4(qa + swz(mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, kk * 2 + (lane >> 4)),
+                        a[0], a[1], a[2], a[3]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (j < nt_per) {
+                for (int j = 0; j < 2; ++j) {
+                    const int nt = wq + 4 * j;
+                    if (nt < NT) {
                         uint32_t b0, b1;
-                        const uint32_t row = (nt0 + j) * 8 + (lane & 7);
-                        const uint32_t chunk = kk * 2 + ((lane >> 3) & 1);
-                        ldsm_x2(ka + swz(row, chunk), b0, b1);
+                        ldsm_x2(ka + swz(nt * 8 + (lane & 7), kk * 2 + ((lane >> 3) & 1)), b0, b1);
                         mma_bf16(acc[j], a[0], a[1], a[2], a[3], b0, b1);
                     }
                 }
             }
             __syncthreads();
         }
-        // ---------------- phase 2: token softmax -> P ----------------
         {
-            const int g = lane >> 2, tq = lane & 3;
+            const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (j < nt_per) {
-                    const int col = (nt0 + j) * 8 + tq * 2;
-                    sm.s[mt * 16 + g][col] = acc[j][0];
-                    sm.s[mt * 16 + g][col + 1] = acc[j][1];
-                    sm.s[mt * 16 + g + 8][col] = acc[j][2];
-                    sm.s[mt * 16 + g + 8][col + 1] = acc[j][3];
+            for (int j = 0; j < 2; ++j) {
+                const int nt = wq + 4 * j;
+                if (nt < NT) {
+                    const int col = nt * 8 + t4 * 2;
+                    sp[(mt * 16 + g) * SP + col] = acc[j][0];
+                    sp[(mt * 16 + g) * SP + col + 1] = acc[j][1];
+                    sp[(mt * 16 + g + 8) * SP + col] = acc[j][2];
+                    sp[(mt * 16 + g + 8) * SP + col + 1] = acc[j][3];
                 }
             }
         }
-        for (int i = tid; i < kQBlock * kKvMax; i += kTcThreads) (&sm.pf[0][0])[i] = 0.f;
         __syncthreads();
-        for (uint32_t a = warp; a < nqh; a += kTcThreads / 32) {
-            const uint32_t qa = a0 + a;
-            const int n = tt.count[qa];
-            const uint8_t* cols = tt.col + size_t(qa) * kMaxTokens;
-            const uint8_t* flg = tt.biased + size_t(qa) * kMaxTokens;
-            float m = -INFINITY;
-            for (int i = lane; i < n; i += 32)
-                m = fmaxf(m, scale * sm.s[a][cols[i]] + (flg[i] ? bias : 0.f));
+        // ---------------- phase 2: token softmax -> P (in place over S) ----------------
+        for (uint32_t a = warp; a < uint32_t(kQBlock); a += kTcWarps) {
+            float* row = sp + a * SP;
+            if (a < nqh) {
+                const uint32_t qa = a0 + a;
+                const int n = tt.count[qa];
+                const uint8_t* cols = tt.col + size_t(qa) * kMaxTokens;
+                const uint8_t* flg = tt.biased + size_t(qa) * kMaxTokens;
+                // each lane holds up to kMaxTokens/32 = 5 token logits
+                float lg[(kMaxTokens + 31) / 32];
+                int cl[(kMaxTokens + 31) / 32];
+                float m = -INFINITY;
+                const int nk = (n + 31) >> 5;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            float z = 0.f;
-            for (int i = lane; i < n; i += 32) {
-                const float e = expf(scale * sm.s[a][cols[i]] + (flg[i] ? bias : 0.f) - m);
-                z += e;
-                atomicAdd(&sm.pf[a][cols[i]], e);
+                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
+                    const int i = lane + 32 * k;
+                    cl[k] = 0;
+                    lg[k] = -INFINITY;
+                    if (k < nk && i < n) {
+                        cl[k] = int(cols[i]);
+                        lg[k] = scale * row[cl[k]] + (flg[i] ? bias : 0.f);
+                    }
+                    m = fmaxf(m, lg[k]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                float z = 0.f;
+#pragma unroll
+                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
+                    lg[k] = (k < nk && lane + 32 * k < n) ? expf(lg[k] - m) : 0.f;
+                    z += lg[k];
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+                __syncwarp();
+                for (int c = lane; c < kKvMax; c += 32) row[c] = 0.f;  // S row consumed
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k)
+                    if (k < nk && lane + 32 * k < n) atomicAdd(&row[cl[k]], lg[k]);
+                if (lane == 0) zinv[a] = 1.0f / z;
+            } else {
+                for (int c = lane; c < kKvMax; c += 32) row[c] = 0.f;
+                if (lane == 0) zinv[a] = 0.f;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-            if (lane == 0) sm.zinv[a] = 1.0f / z;
         }
         __syncthreads();
         for (int i = tid; i < kQBlock * int(RP) / 8; i += kTcThreads) {
             const uint32_t r = i / (RP / 8), c = i % (RP / 8);  // 8 bf16 per 16B chunk
-            const float zi = r < nqh ? sm.zinv[r] : 0.f;
+            const float zi = zinv[r];
+            const float* src = sp + r * SP + c * 8;
             uint32_t w[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const __nv_bfloat162 b2 = __floats2bfloat162_rn(sm.pf[r][c * 8 + 2 * k] * zi,
-                                                                sm.pf[r][c * 8 + 2 * k + 1] * zi);
+                const __nv_bfloat162 b2 = __floats2bfloat162_rn(src[2 * k] * zi, src[2 * k + 1] * zi);
                 w[k] = *reinterpret_cast<const uint32_t*>(&b2);
             }
-            *reinterpret_cast<uint4*>(sm.pb + swz(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(sm + L.pb + swz(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         __syncthreads();
         // ---------------- phase 3: ctx = P V ----------------
-        load_chunk(0, 0, false, 2 * C + hc0);
-        for (uint32_t ch = 0; ch < nch; ++ch) {
-            if (ch + 1 < nch) {
-                load_chunk((ch + 1) & 1, 0, false, 2 * C + hc0 + (ch + 1) * kDC);
-                cp_wait<1>();
-            } else {
-                cp_wait<0>();
-            }
+        // warp: m tile mt, n8 tiles 2wq, 2wq+1 of each 64-wide chunk; its P fragments
+        // (A operand) are loaded once per head and reused for every V chunk.
+        const uint32_t pb_s = sbase + L.pb;
+        uint32_t pa[4][4];  // k16 steps of RP (<= 64)
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq)
+            if (kq < int(RP / 16))
+                ldsm_x4(pb_s + swz(mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, kq * 2 + (lane >> 4)),
+                        pa[kq][0], pa[kq][1], pa[kq][2], pa[kq][3]);
+        for (uint32_t ch = 0; ch < nch; ++ch, ++li) {
+            issue(li + kStages - 1);
+            cp_wait<kStages - 1>();
             __syncthreads();
-            const uint32_t va = kv_s + (ch & 1) * (kKvMax * 128);
-            float o[4][4];
+            const uint32_t va = sbase + L.ring + (li % kStages) * L.stage + kQBlock * 128;
+            float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) o[j][k] = 0.f;
-            for (uint32_t kk = 0; kk < RP / 16; ++kk) {
-                uint32_t a[4];
-                {
-                    const uint32_t row = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                    const uint32_t chunk = kk * 2 + (lane >> 4);
-                    ldsm_x4(pb_s + swz(row, chunk), a[0], a[1], a[2], a[3]);
-                }
-#pragma unroll
-                for (int jp = 0; jp < 2; ++jp) {
-                    // two n8 tiles (16 output columns) per x4.trans load
+            for (int kq = 0; kq < 4; ++kq) {
+                if (kq < int(RP / 16)) {
                     uint32_t b[4];
-                    const uint32_t row = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                    const uint32_t chunk = half * 4 + jp * 2 + (lane >> 4);
-                    ldsm_x4_t(va + swz(row, chunk), b[0], b[1], b[2], b[3]);
-                    mma_bf16(o[jp * 2], a[0], a[1], a[2], a[3], b[0], b[1]);
-                    mma_bf16(o[jp * 2 + 1], a[0], a[1], a[2], a[3], b[2], b[3]);
+                    // (k lo, tile 2wq), (k hi, tile 2wq), (k lo, tile 2wq+1), (k hi, tile 2wq+1)
+                    ldsm_x4_t(va + swz(kq * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, 2 * wq + (lane >> 4)),
+                              b[0], b[1], b[2], b[3]);
+                    mma_bf16(o[0], pa[kq][0], pa[kq][1], pa[kq][2], pa[kq][3], b[0], b[1]);
+                    mma_bf16(o[1], pa[kq][0], pa[kq][1], pa[kq][2], pa[kq][3], b[2], b[3]);
                 }
             }
-            // stage the 32 x 64 bf16 chunk in the (free) Q buffer, then 16B row stores
-            uint8_t* ost = sm.q[0];
             {
-                const int g = lane >> 2, tq = lane & 3;
+                const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t col = half * 32 + j * 8 + tq * 2;
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t col = (2 * wq + j) * 8 + t4 * 2;
                     const __nv_bfloat162 lo2 = __floats2bfloat162_rn(o[j][0], o[j][1]);
                     const __nv_bfloat162 hi2 = __floats2bfloat162_rn(o[j][2], o[j][3]);
-                    const uint32_t r0 = mt * 16 + g, r1 = r0 + 8;
-                    *reinterpret_cast<__nv_bfloat162*>(ost + swz(r0, col >> 3) + (col & 7) * 2) = lo2;
-                    *reinterpret_cast<__nv_bfloat162*>(ost + swz(r1, col >> 3) + (col & 7) * 2) = hi2;
+                    const uint32_t r0 = mt * 16 + g;
+                    *reinterpret_cast<__nv_bfloat162*>(sm + L.ost + swz(r0, col >> 3) + (col & 7) * 2) = lo2;
+                    *reinterpret_cast<__nv_bfloat162*>(sm + L.ost + swz(r0 + 8, col >> 3) + (col & 7) * 2) = hi2;
                 }
             }
             __syncthreads();
+            const uint32_t c0 = h * d + ch * kDC;
             for (int i = tid; i < int(nqh) * 8; i += kTcThreads) {
                 const uint32_t r = i >> 3, c = i & 7;
-                const uint4 v = *reinterpret_cast<const uint4*>(ost + swz(r, c));
-                *reinterpret_cast<uint4*>(ctx + (uint64_t(a0 + r) * HW + p) * C + hc0 + ch * kDC +
-                                          c * 8) = v;
+                const uint4 v = *reinterpret_cast<const uint4*>(sm + L.ost + swz(r, c));
+                *reinterpret_cast<uint4*>(ctx + (uint64_t(a0 + r) * HW + p) * C + c0 + c * 8) = v;
             }
-            __syncthreads();
+            // the ring slot just consumed is refilled by the next iteration's issue() only
+            // after the __syncthreads at its top; the staging buffer likewise
         }
     }
+    cp_wait<0>();
 }
 
 }  // namespace
@@ -287,11 +314,11 @@ int launch_attention_core_tc(const void* qkv, uint32_t HW, uint32_t C, uint32_t 
                              uint32_t q_frame0, TokenTable tt, float scale, float bias, void* ctx,
                              cudaStream_t s) {
     const uint32_t nqb = (nq + kQBlock - 1) / kQBlock;
-    const size_t shm = sizeof(TcSmem);
+    const size_t shm = Lay((uint32_t(tt.max_kv) + 15) & ~15u).total;  // largest K/V list here
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attention_core_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(shm));
+                             int(Lay(kKvMax).total));
         attr = true;
     }
     dim3 grid(HW, nqb);

@@ -59,6 +59,7 @@ struct TokenTable {
     const uint16_t* kv_frames;  // [nqb][kKvMax] K/V frame row of each column
     const uint16_t* kv_count;   // [nqb]
     int kv_ok;                  // every block's K/V list fits kKvMax
+    int max_kv;                 // largest K/V list over the blocks
 };
 
 // (hi/lo non-null: only the split bf16 planes are written, the fp32-mode GEMM operand)

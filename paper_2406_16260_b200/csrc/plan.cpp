@@ -145,6 +145,8 @@ TokenTable HostTokens::view(const uint8_t* base) const {
     o += biased.size();
     t.col = base + o;
     t.kv_ok = kv_ok ? 1 : 0;
+    t.max_kv = 0;
+    for (uint16_t c : kv_count) t.max_kv = std::max<int>(t.max_kv, c);
     return t;
 }
 
