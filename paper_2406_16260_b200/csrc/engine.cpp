@@ -141,18 +141,21 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     ep.out = at(L.off_u1);
     ep.out_ld = C;
     ep.out_bf16 = !f32();
+    // GroupNorm statistics of u1 fused into the GEMM epilogue: per-column (sum, sum of
+    // squares) of the stored values, folded into per-group sums; workers all-reduce the
+    // 2 * groups sums before GN_APPLY.
+    const uint64_t rows = uint64_t(L.f_clip) * L.hw;
+    float* colpart = at<float>(L.off_colstats);
+    ep.colpart = colpart;
     {
         Span span(this, "conv_gemm", s);
-        gemm(A, ar, B.conv, br, int64_t(L.f_clip) * L.hw, C, ep, f32(), s);
+        gemm(A, ar, B.conv, br, int64_t(rows), C, ep, f32(), s);
     }
     ++launches;
-    // GroupNorm statistics of u1 in one pass (sum, sum of squares per group; u1 was just
-    // written and is largely L2-resident); workers all-reduce them before GN_APPLY.
     Span span(this, "gn_stats", s);
-    cuda_check(launch_group_moment_sums(at(L.off_u1), !f32(), uint64_t(L.f_clip) * L.hw, C,
-                                        L.d.groups, at<double>(L.off_sums),
-                                        at<double>(L.off_scratch), s),
-               "gn moments");
+    cuda_check(launch_colpart_to_groups(colpart, uint32_t((rows + 31) / 32), C, L.d.groups,
+                                        at<double>(L.off_sums), at<double>(L.off_scratch), s),
+               "gn fold");
     launches += 2;
 }
 

@@ -37,7 +37,7 @@ constexpr uint32_t kABytes = kBM * kBK * 2;
 constexpr int kStgPitch = 36;  // floats per staged row (32 + 4 pad: conflict-free 16 B access)
 constexpr uint32_t kStgBytes = kEpiWarps * 32 * kStgPitch * 4;  // a 32x32 fp32 block per epilogue warp
 
-template <int BN>
+template <int BN, bool ST = false>
 struct TileCfg {
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -68,7 +68,7 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 
 // Epilogue of one 128 x BN tile for the warp owning TMEM lane quadrant q (rows m0..m0+31).
 //   OBF: output (and residual) bf16, else fp32.   RES: residual present.
-template <int BN, bool OBF, bool RES>
+template <int BN, bool OBF, bool RES, bool ST>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int q, int lane,
                                               uint32_t stg, int m0, int n0, int half) {
     using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
@@ -146,29 +146,55 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
             const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n));
             b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
         }
+        float cs[4] = {0.f, 0.f, 0.f, 0.f}, cq[4] = {0.f, 0.f, 0.f, 0.f};  // column stats
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int64_t gm = int64_t(m0) + tr + 4 * i;
             if (!full && (gm >= p.M || n >= n_lim)) continue;
             T* dst = out + gm * p.out_ld + n;
-            const float y0 = cur[i][0] + b4[0], y1 = cur[i][1] + b4[1];
-            const float y2 = cur[i][2] + b4[2], y3 = cur[i][3] + b4[3];
+            float y[4] = {cur[i][0] + b4[0], cur[i][1] + b4[1], cur[i][2] + b4[2], cur[i][3] + b4[3]};
             if (OBF) {
-                const __nv_bfloat162 lo2 = __floats2bfloat162_rn(y0, y1);
-                const __nv_bfloat162 hi2 = __floats2bfloat162_rn(y2, y3);
+                const __nv_bfloat162 lo2 = __floats2bfloat162_rn(y[0], y[1]);
+                const __nv_bfloat162 hi2 = __floats2bfloat162_rn(y[2], y[3]);
                 *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<const uint32_t*>(&lo2),
                                                             *reinterpret_cast<const uint32_t*>(&hi2));
+                if (ST) {  // statistics of the stored (rounded) values
+                    y[0] = __low2float(lo2); y[1] = __high2float(lo2);
+                    y[2] = __low2float(hi2); y[3] = __high2float(hi2);
+                }
             } else {
-                *reinterpret_cast<float4*>(dst) = make_float4(y0, y1, y2, y3);
+                *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+            }
+            if (ST) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    cs[k] += y[k];
+                    cq[k] = fmaf(y[k], y[k], cq[k]);
+                }
+            }
+        }
+        if (ST) {
+            // lanes l, l^8, l^16, l^24 hold the same 4 columns for different rows
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], 8);
+                cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], 16);
+                cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 8);
+                cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 16);
+            }
+            if (tr == 0 && n < n_lim && m0 < p.M) {  // this warp owns (row block, 4 columns)
+                float* part = p.colpart + int64_t(m0 >> 5) * 2 * p.N + n;
+                *reinterpret_cast<float4*>(part) = make_float4(cs[0], cs[1], cs[2], cs[3]);
+                *reinterpret_cast<float4*>(part + p.N) = make_float4(cq[0], cq[1], cq[2], cq[3]);
             }
         }
     }
 }
 
-template <int BN, bool OBF, bool RES>
+template <int BN, bool OBF, bool RES, bool ST>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
-    using Cfg = TileCfg<BN>;
+    using Cfg = TileCfg<BN, ST>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -276,8 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t acc = local & 1;
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
-            epilogue_tile<BN, OBF, RES>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
-                                        (tile / n_tiles) * kBM + q * 32, (tile % n_tiles) * BN, half);
+            epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
+                                            (tile / n_tiles) * kBM + q * 32, (tile % n_tiles) * BN,
+                                            half);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -306,12 +333,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 int g_num_sms = 0;
 
-template <int BN, bool OBF, bool RES>
+template <int BN, bool OBF, bool RES, bool ST = false>
 int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
-    using Cfg = TileCfg<BN>;
+    using Cfg = TileCfg<BN, ST>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES>,
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES, ST>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(Cfg::kSmemBytes));
         if (e != cudaSuccess) return int(e);
@@ -325,7 +352,7 @@ int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     }
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
     const int grid = std::max(1, std::min(tiles, g_num_sms));
-    gemm_tc_kernel<BN, OBF, RES><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
+    gemm_tc_kernel<BN, OBF, RES, ST><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
     return int(cudaGetLastError());
 }
 
@@ -333,6 +360,11 @@ template <int BN>
 int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     const bool res = p.res != nullptr;
     if (res && p.res_bf16 != p.out_bf16) return int(cudaErrorInvalidValue);
+    if (p.colpart) {  // fused GroupNorm statistics: the conv flavour (residual present)
+        if (!res) return int(cudaErrorInvalidValue);
+        return p.out_bf16 ? launch_cfg<BN, true, true, true>(maps, p, stream)
+                          : launch_cfg<BN, false, true, true>(maps, p, stream);
+    }
     if (p.out_bf16) return res ? launch_cfg<BN, true, true>(maps, p, stream)
                                : launch_cfg<BN, true, false>(maps, p, stream);
     return res ? launch_cfg<BN, false, true>(maps, p, stream)

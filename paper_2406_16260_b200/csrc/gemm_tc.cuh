@@ -39,6 +39,11 @@ struct GemmParams {
     int64_t out_ld;
     int32_t out_bf16;
     int32_t flags;  // kGemmFlag* (diagnostics)
+    // Optional per-column statistics of the stored output (GroupNorm fused into the
+    // conv epilogue), one partial per 32-row block, each written exactly once (no atomics,
+    // deterministic): colpart[(rb*2 + 0)*N + n] = sum over the block's rows of out[m,n],
+    // colpart[(rb*2 + 1)*N + n] = sum of squares. fp32 [ceil(M/32)][2][N].
+    float* colpart;
 };
 
 constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic

@@ -341,6 +341,54 @@ int launch_group_moment_sums(const void* x, bool bf16, uint64_t rows, uint32_t C
     return int(cudaGetLastError());
 }
 
+// Per-(32-row block, column) partials fp32 [blocks][2][C] -> per-group sums f64 [2][groups],
+// deterministically: (1) each thread owns one of the 2C statistic columns (coalesced) and
+// sums a fixed segment of row blocks into f64 segment partials; (2) one CTA per (statistic,
+// group) folds segments x group columns with a fixed tree.
+constexpr uint32_t kColSegs = 256;
+
+__global__ void __launch_bounds__(128)
+    colpart_segments_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C,
+                            double* __restrict__ seg /* [kColSegs][2C] */) {
+    const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;  // over 2C
+    if (col >= 2 * C) return;
+    const uint32_t per = (blocks + kColSegs - 1) / kColSegs;
+    const uint32_t b0 = blockIdx.y * per, b1 = min(blocks, b0 + per);
+    double a = 0.0;
+#pragma unroll 4
+    for (uint32_t b = b0; b < b1; ++b) a += double(part[uint64_t(b) * 2 * C + col]);
+    seg[uint64_t(blockIdx.y) * 2 * C + col] = a;
+}
+
+__global__ void __launch_bounds__(256)
+    colseg_to_groups_kernel(const double* __restrict__ seg, uint32_t C, uint32_t groups,
+                            double* __restrict__ sums) {
+    __shared__ double red[256];
+    const uint32_t which = blockIdx.x / groups, g = blockIdx.x % groups, gs = C / groups;
+    double a = 0.0;
+    const uint32_t n = kColSegs * gs;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+        a += seg[uint64_t(i / gs) * 2 * C + which * C + g * gs + i % gs];
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[which * groups + g] = red[0];
+}
+
+uint64_t colpart_scratch_elems(uint32_t C) { return uint64_t(kColSegs) * 2 * C; }
+
+int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,
+                             double* sums, double* scratch, cudaStream_t s) {
+    if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
+    dim3 g1((2 * C + 127) / 128, kColSegs);
+    colpart_segments_kernel<<<g1, 128, 0, s>>>(part, blocks, C, scratch);
+    colseg_to_groups_kernel<<<2 * groups, 256, 0, s>>>(scratch, C, groups, sums);
+    return int(cudaGetLastError());
+}
+
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
                          cudaStream_t s) {
     group_moments_kernel<<<(groups + 127) / 128, 128, 0, s>>>(sums, count, groups, stats);

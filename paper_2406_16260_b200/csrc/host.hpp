@@ -113,6 +113,7 @@ struct Epilogue {
     void* out = nullptr;
     int64_t out_ld = 0;
     bool out_bf16 = false;
+    float* colpart = nullptr;  // fused per-(32-row block, column) (sum, sum of squares)
 };
 
 // out[m, n] = sum_s A[m + a_rows[s]] . B[n + b_rows[s]] (+ bias, + res); M x N, K = A.cols.

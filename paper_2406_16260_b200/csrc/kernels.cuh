@@ -37,6 +37,12 @@ int launch_group_finalize(const double* sums, double count, uint32_t groups, dou
 // scratch: >= 2 * groups * min(4 * SMs, 512) doubles.
 int launch_group_moment_sums(const void* x, bool bf16, uint64_t rows, uint32_t C,
                              uint32_t groups, double* sums, double* scratch, cudaStream_t s);
+// Fold per-(32-row block, column) partials fp32 [blocks][2][C] (sum, sum of squares) into
+// per-group sums f64 [2][groups], in a fixed order (deterministic).
+// scratch: colpart_scratch_elems(C) doubles.
+uint64_t colpart_scratch_elems(uint32_t C);
+int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,
+                             double* sums, double* scratch, cudaStream_t s);
 // sums = [sum x (groups) | sum x^2 (groups)] -> stats = [mean | variance]
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
                          cudaStream_t s);

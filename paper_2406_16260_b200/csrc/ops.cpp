@@ -118,6 +118,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         p.out_ld = ep.out_ld;
         p.out_bf16 = ep.out_bf16;
         p.flags = g_gemm_debug_flags;
+        if (c0 + kGemmMaxSeg >= segs.size()) p.colpart = ep.colpart;  // final output only
         cuda_check(gemm_tc_launch(maps, p, bn, s), "gemm_tc_launch");
     }
 }

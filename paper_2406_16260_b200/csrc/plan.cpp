@@ -242,8 +242,10 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     off_ctxlo = f32 ? take(clip * 2) : 0;
     off_sums = take(sizeof(double) * 2 * d.groups);
     off_stats = take(sizeof(double) * 2 * d.groups);
-    scratch_elems = uint64_t(kScratchBlocks) * d.groups;
+    scratch_elems = std::max<uint64_t>(uint64_t(kScratchBlocks) * d.groups,
+                                       uint64_t(256) * 2 * d.channels);  // colpart segments
     off_scratch = take(sizeof(double) * scratch_elems);
+    off_colstats = take(sizeof(float) * 2 * d.channels * ((uint64_t(f_clip) * hw + 31) / 32));
     off_tok[0] = take(tok[0].blob_bytes());
     off_tok[1] = take(tok[1].blob_bytes());
     total = off;
