@@ -227,7 +227,11 @@ __global__ void __launch_bounds__(kTcThreads)
                 for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
                 __syncwarp();
                 for (int c = lane; c < kKvMax; c += 32) row[c] = 0.f;  // S row consumed
-                __syncwarp();
+                // Duplicate tokens (a frame in both the window and the global set) add into
+                // the same column. The window list and the global list are each duplicate-
+                // free, so a column receives at most two additions onto 0, and fp32 addition
+                // of two operands is commutative: the result is order-independent
+                // (bitwise reproducible).
 #pragma unroll
                 for (int k = 0; k < (kMaxTokens + 31) / 32; ++k)
                     if (k < nk && lane + 32 * k < n) atomicAdd(&row[cl[k]], lg[k]);

@@ -316,10 +316,23 @@ int vinf_gemm_bench(uint32_t M, uint32_t N, uint32_t K, uint32_t nseg, int flags
         for (int i = 0; i < iters; ++i) gemm(A, ar, B, br, M, N, ep, false, s);
         cudaEventRecord(e1, s);
         cuda_check(cudaEventSynchronize(e1), "gemm bench");
-        g_gemm_debug_flags = 0;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e1);
         *avg_ms = ms / iters;
+        if (flags & 2) {  // determinism check: compare 5 further runs against this output
+            const size_t nb = uint64_t(M) * N * 2;
+            std::vector<uint8_t> ref(nb), cur(nb);
+            cuda_check(cudaMemcpy(ref.data(), o.p, nb, cudaMemcpyDeviceToHost), "copy");
+            uint64_t bad = 0;
+            for (int rep = 0; rep < 5; ++rep) {
+                gemm(A, ar, B, br, M, N, ep, false, s);
+                cuda_check(cudaMemcpy(cur.data(), o.p, nb, cudaMemcpyDeviceToHost), "copy");
+                for (size_t i = 0; i < nb; i += 2)
+                    bad += (ref[i] != cur[i] || ref[i + 1] != cur[i + 1]) ? 1 : 0;
+            }
+            *avg_ms = -float(bad);  // report mismatching elements instead of time
+        }
+        g_gemm_debug_flags = 0;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         B.release();
@@ -356,6 +369,8 @@ int vinf_layout_region(const vinf_layout* l, int which, uint64_t* offset, uint64
             case VINF_BUF_CONV_IN: fb = L.E * 2; off = L.off_u0; n = uint64_t(L.cf) * fb; break;
             case VINF_BUF_ATTN_IN: fb = L.E * 2; off = L.off_u2; n = uint64_t(L.af) * fb; break;
             case VINF_BUF_GN_SUMS: fb = 0; off = L.off_sums; n = 2 * 8 * uint64_t(L.d.groups); break;
+            case VINF_BUF_QKV: fb = L.E * 3 * L.es; off = L.off_qkv; n = uint64_t(L.af) * fb; break;
+            case VINF_BUF_CTX: fb = L.E * 2; off = L.off_ctx; n = uint64_t(L.f_clip) * fb; break;
             default: range_error("unknown region");
         }
         if (offset) *offset = off;

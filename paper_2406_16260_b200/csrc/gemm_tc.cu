@@ -151,6 +151,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         for (int i = 0; i < 8; ++i) {
             const int64_t gm = int64_t(m0) + tr + 4 * i;
             if (!full && (gm >= p.M || n >= n_lim)) continue;
+            // BN not a multiple of 32 (e.g. 240): the last chunk of an interior tile would
+            // spill into the next tile's columns
+            if (BN % 32 != 0 && n >= n_lim) continue;
             T* dst = out + gm * p.out_ld + n;
             float y[4] = {cur[i][0] + b4[0], cur[i][1] + b4[1], cur[i][2] + b4[2], cur[i][3] + b4[3]};
             if (OBF) {

@@ -101,6 +101,35 @@ def test_conv_large_gemm_vs_torch(ops):
     assert normwise(to_np(got16), want.cpu().numpy()) <= TOL_BF16
 
 
+@pytest.mark.parametrize("N,K,nseg", [(1920, 640, 1), (960, 320, 1), (1280, 640, 1), (640, 640, 3),
+                                       (1536, 256, 2), (192, 128, 1)])
+def test_gemm_every_tile_width_deterministic(lib, N, K, nseg):
+    # every N-tile choice (BN = 240, 192, 256, 160, ...) must write each output exactly once:
+    # repeated runs are bitwise identical (a spill into a neighbour tile races)
+    import ctypes as C
+    v = C.c_float()
+    from paper_2406_16260_b200 import _lib
+    _lib.check(lib.vinf_gemm_bench(8192, N, K, nseg, 2, 0, 2, C.byref(v)))
+    assert v.value == 0.0, f"{int(-v.value)} elements differ between runs"
+
+
+@pytest.mark.parametrize("C", [320, 640])
+def test_dual_scope_production_channels(ops, oracle, C):
+    # C = 320 / 640 (VideoCrafter2 levels): the fused Q/K/V GEMM runs with N = 3C = 960 / 1920
+    x = oracle.tensor_from_seed((24, 2, 2, C), 80)
+    bp = oracle.build_block(C, weight_seed=81)
+    sc = float(np.float32(1) / np.sqrt(np.float32(C)))
+    p = _attn(ops, bp, C)
+    cfg = ops.DualScopeConfig(16, 16, 10.0, 800.0)
+    want = oracle.dual_scope(x, 900.0, bp.wq, bp.wk, bp.wv, bp.wo, sc, 16, 16, 10.0, 800.0)
+    got = to_np(ops.dual_scope_reference(dev(x), 900.0, p, cfg))
+    assert normwise(got, want) <= TOL_F32, normwise(got, want)
+    want16 = oracle.dual_scope(to_np(dev(x, torch.bfloat16)), 900.0, bp.wq, bp.wk, bp.wv, bp.wo,
+                               sc, 16, 16, 10.0, 800.0)
+    got16 = to_np(ops.dual_scope_reference(dev(x, torch.bfloat16), 900.0, p, cfg))
+    assert normwise(got16, want16) <= TOL_BF16, normwise(got16, want16)
+
+
 @pytest.mark.parametrize("mode", ["f32", "bf16"])
 @pytest.mark.parametrize("groups", [1, 2, 32])
 def test_group_norm(ops, oracle, mode, groups):

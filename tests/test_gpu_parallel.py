@@ -144,6 +144,29 @@ def test_engine_single_worker_vs_oracle(mods, oracle, dtype, tol, t):
     assert normwise(got, want) <= tol, normwise(got, want)
 
 
+@pytest.mark.parametrize("C", [320, 640])
+def test_engine_production_channels(mods, oracle, C):
+    # the bench's channel counts (VideoCrafter2 levels) through the whole fused block,
+    # both modes, vs the CPU oracle; and the bf16 engine is bitwise reproducible
+    _, _, en, _ = mods
+    kw = dict(frames=24, height=2, width=4, channels=C, groups=32, n_local=16, n_global=16)
+    x = oracle.tensor_from_seed((24, 2, 4, C), 0)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    for dtype, tol in ((torch.float32, TOL_F32), (torch.bfloat16, TOL_BF16)):
+        e = _engine(mods, dtype, **kw)
+        e.init_weights(1)
+        xd = dev(x, dtype)
+        e.x.copy_(xd)
+        en.forward(900.0, [e])
+        y1 = e.y.clone()
+        want = oracle.block_forward(to_np(xd), bp, 900.0, 32)
+        assert normwise(to_np(y1), want) <= tol, (dtype, normwise(to_np(y1), want))
+        e.x.copy_(xd)
+        en.forward(900.0, [e])
+        torch.cuda.synchronize()
+        assert torch.equal(e.y, y1)
+
+
 def test_engine_set_block_equals_init_weights(mods, oracle):
     _, _, en, _ = mods
     bp = oracle.build_block(64, 3, weight_seed=5)
@@ -157,6 +180,23 @@ def test_engine_set_block_equals_init_weights(mods, oracle):
         en.forward(900.0, [e])
     torch.cuda.synchronize()
     assert torch.equal(e1.y, e2.y)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_engine_is_deterministic(mods, oracle, dtype):
+    # no atomics on the value path: repeated runs (and two engines) agree bitwise
+    _, _, en, _ = mods
+    x = dev(oracle.tensor_from_seed((24, 4, 8, 64), 8), dtype)
+    outs = []
+    for _ in range(2):
+        e = _engine(mods, dtype, **BLOCK)
+        e.init_weights(2)
+        for _ in range(2):
+            e.x.copy_(x)
+            en.forward(900.0, [e])
+            outs.append(e.y.clone())
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, outs[0]) for o in outs[1:])
 
 
 @pytest.mark.parametrize("n", [2, 3, 4, 6])
