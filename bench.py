@@ -365,6 +365,17 @@ def run_ours(args):
             roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": ach / hbm, "traffic": None, "peak_source": f"{src} HBM copy",
                     "work_per_launch": w_}
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture of this
+    # workload (dram__bytes_read.sum + dram__bytes_write.sum per launch)
+    if roof is not None and args.dtype == "bf16":
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f).get(roof["kernel"])
+            if tr:
+                roof["traffic"] = tr["dram_bytes"]
+                roof["traffic_source"] = tr["source"]
+        except (OSError, ValueError):
+            pass
     # whole-block roofline: all tensor work of the step at the sustained tensor peak
     flops_step = sum(work[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm"))
     block_roof = {"flops_per_step": flops_step,
