@@ -244,8 +244,14 @@ enum {
 int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void* stream);
 /* All blocks, all stages (single worker: no exchanges needed). */
 int vinf_engine_forward(vinf_engine* e, double t, void* stream);
-/* Where the current block input / final output live (device pointers). */
+/* Where the clip x (block-stack input, never overwritten by the blocks) and the stack's
+ * output y (= eps) live (device pointers). */
 int vinf_engine_io(const vinf_engine* e, void** x, void** y);
+/* euler_update_inplace (pipeline.cpp:93-100): x -= lambda * y. */
+int vinf_engine_euler(vinf_engine* e, double lambda, void* stream);
+/* worker_denoise (pipeline.cpp:174-191) for one worker: for t in timestep_grid(steps)
+ * (1000 j / steps, j = steps..1): y = eps_theta(x, t); x -= y / steps. Result in x. */
+int vinf_engine_denoise(vinf_engine* e, uint32_t steps, void* stream);
 /* Number of kernel launches this engine has enqueued so far. */
 uint64_t vinf_engine_launches(const vinf_engine* e);
 /* Per-kernel timing: with profiling on, CUDA events are recorded on the launching

@@ -122,6 +122,8 @@ _SIGS = {
     "vinf_engine_stage": (C.c_int, [_vp, C.c_uint32, C.c_int, C.c_double, _vp]),
     "vinf_engine_forward": (C.c_int, [_vp, C.c_double, _vp]),
     "vinf_engine_io": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
+    "vinf_engine_euler": (C.c_int, [_vp, C.c_double, _vp]),
+    "vinf_engine_denoise": (C.c_int, [_vp, C.c_uint32, _vp]),
     "vinf_engine_launches": (C.c_uint64, [_vp]),
     "vinf_engine_profile": (C.c_int, [_vp, C.c_int]),
     "vinf_gemm_bench": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int,

@@ -162,7 +162,35 @@ __global__ void cast_kernel(const void* __restrict__ in, int in_bf16, void* __re
     }
 }
 
+// x = x - lambda * eps in f64 arithmetic, rounded to the storage type
+// (euler_update_inplace, pipeline.cpp:93-100).
+template <bool BF16>
+__global__ void euler_kernel(void* __restrict__ x, const void* __restrict__ eps, uint64_t n,
+                             double lambda) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (BF16) {
+            auto* px = static_cast<__nv_bfloat16*>(x);
+            const double v = double(__bfloat162float(px[i])) -
+                             lambda * double(__bfloat162float(static_cast<const __nv_bfloat16*>(eps)[i]));
+            px[i] = __float2bfloat16_rn(float(v));
+        } else {
+            auto* px = static_cast<float*>(x);
+            px[i] = float(double(px[i]) - lambda * double(static_cast<const float*>(eps)[i]));
+        }
+    }
+}
+
 }  // namespace
+
+int launch_euler(void* x, const void* eps, bool bf16, uint64_t n, double lambda, cudaStream_t s) {
+    if (n == 0) return 0;
+    if (bf16)
+        euler_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(x, eps, n, lambda);
+    else
+        euler_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(x, eps, n, lambda);
+    return int(cudaGetLastError());
+}
 
 int grid_for(uint64_t work_items, int block) {
     const uint64_t want = (work_items + block - 1) / block;

@@ -89,8 +89,12 @@ struct vinf_engine {
     T* at(uint64_t off) const { return reinterpret_cast<T*>(ws + off); }
     bool f32() const { return L.f32; }
     uint64_t clip_elems() const { return uint64_t(L.f_clip) * L.E; }
-    void* x_of(uint32_t b) const { return at(b % 2 == 0 ? L.off_x : L.off_y); }
-    void* y_of(uint32_t b) const { return at(b % 2 == 0 ? L.off_y : L.off_x); }
+    // Block b writes Y if an even number of blocks follow it, else TMP, so the last block
+    // always writes Y and X (the clip being denoised) is never overwritten.
+    void* y_of(uint32_t b) const {
+        return at((blocks.size() - 1 - b) % 2 == 0 ? L.off_y : L.off_tmp);
+    }
+    void* x_of(uint32_t b) const { return b == 0 ? at(L.off_x) : y_of(b - 1); }
     double gn_count() const {  // elements per group over the whole video
         return double(uint64_t(L.d.frames) * L.hw * L.d.channels / L.d.groups);
     }
@@ -390,11 +394,47 @@ int vinf_engine_forward(vinf_engine* e, double t, void* stream) {
     });
 }
 
+int vinf_engine_euler(vinf_engine* e, double lambda, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        auto s = static_cast<cudaStream_t>(stream);
+        vinf_engine::Span span(e, "euler", s);
+        cuda_check(launch_euler(e->at(e->L.off_x), e->at(e->L.off_y), !e->f32(), e->clip_elems(),
+                                lambda, s),
+                   "euler");
+        e->launches += 1;
+    });
+}
+
+int vinf_engine_denoise(vinf_engine* e, uint32_t steps, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        if (steps == 0) config_error("denoising needs at least one step");
+        if (e->L.d.workers != 1)
+            config_error("vinf_engine_denoise runs a single worker; use the staged loop for workers > 1");
+        auto s = static_cast<cudaStream_t>(stream);
+        // worker_denoise (pipeline.cpp:174-191): t_j = 1000 j / steps, j = steps..1
+        for (uint32_t j = steps; j >= 1; --j) {
+            const double t = 1000.0 * j / steps;
+            for (uint32_t b = 0; b < e->blocks.size(); ++b) {
+                e->stage_stub(b, s);
+                e->stage_conv(b, s);
+                e->stage_gn_apply(b, s);
+                e->stage_attention(b, t, s);
+            }
+            cuda_check(launch_euler(e->at(e->L.off_x), e->at(e->L.off_y), !e->f32(),
+                                    e->clip_elems(), 1.0 / steps, s),
+                       "euler");
+            e->launches += 1;
+        }
+    });
+}
+
 int vinf_engine_io(const vinf_engine* e, void** x, void** y) {
     return guarded_call([&] {
         if (!e) shape_error("null engine");
         if (x) *x = e->at(e->L.off_x);
-        if (y) *y = e->blocks.size() % 2 == 1 ? e->at(e->L.off_y) : e->at(e->L.off_x);
+        if (y) *y = e->at(e->L.off_y);
     });
 }
 

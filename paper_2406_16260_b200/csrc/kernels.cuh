@@ -21,6 +21,8 @@ int launch_split(const void* in, bool in_bf16, uint64_t n, __nv_bfloat16* hi, __
                  cudaStream_t s);
 int launch_cast(const void* in, bool in_bf16, void* out, bool out_bf16, uint64_t n,
                 cudaStream_t s);
+// x -= lambda * eps (f64 arithmetic), euler_update_inplace (pipeline.cpp:93-100)
+int launch_euler(void* x, const void* eps, bool bf16, uint64_t n, double lambda, cudaStream_t s);
 
 // ---- groupnorm.cu ----
 // Scratch needed by launch_group_sums (doubles).

@@ -33,7 +33,7 @@ struct Layout {
     std::vector<uint32_t> g_frame;  // attn-buffer frame of each global token
     HostTokens tok[2];              // [bias_global]
 
-    uint64_t off_x = 0, off_y = 0, off_u0 = 0, off_u0lo = 0, off_u0f = 0, off_u1 = 0;
+    uint64_t off_x = 0, off_y = 0, off_tmp = 0, off_u0 = 0, off_u0lo = 0, off_u0f = 0, off_u1 = 0;
     uint64_t off_u2 = 0, off_u2lo = 0, off_u2f = 0, off_qkv = 0, off_ctx = 0, off_ctxlo = 0;
     uint64_t off_sums = 0, off_stats = 0, off_scratch = 0, off_colstats = 0, off_tok[2] = {0, 0};
     uint64_t scratch_elems = 0, total = 0;

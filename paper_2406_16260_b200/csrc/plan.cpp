@@ -230,6 +230,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     const uint64_t clip = uint64_t(f_clip) * E;
     off_x = take(clip * es);
     off_y = take(clip * es);
+    off_tmp = d.blocks > 1 ? take(clip * es) : off_y;  // intermediate block outputs
     off_u0 = take(uint64_t(cf) * E * 2);  // bf16 plane (bf16 mode) / hi plane (f32 mode)
     off_u0lo = f32 ? take(uint64_t(cf) * E * 2) : 0;
     off_u0f = f32 ? take(clip * 4) : 0;

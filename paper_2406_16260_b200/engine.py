@@ -114,6 +114,13 @@ class ClipEngine:
     def forward_single(self, t: float) -> None:
         _lib.check(_lib.load().vinf_engine_forward(self._h, C.c_double(t), self._stream()))
 
+    def euler(self, lam: float) -> None:
+        """x -= lam * y (euler_update_inplace, pipeline.cpp:93-100)."""
+        _lib.check(_lib.load().vinf_engine_euler(self._h, C.c_double(lam), self._stream()))
+
+    def denoise_single(self, steps: int) -> None:
+        _lib.check(_lib.load().vinf_engine_denoise(self._h, steps, self._stream()))
+
     def launches(self) -> int:
         return int(_lib.load().vinf_engine_launches(self._h))
 
@@ -205,3 +212,23 @@ def forward(t: float, engines: list[ClipEngine], group=None) -> None:
         group.exchange(engines, _lib.VINF_XCHG_ATTN)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_ATTENTION, t)
+
+
+def timestep_grid(steps: int) -> list[float]:
+    """pipeline.cpp:75-81: t_j = 1000 j / steps for j = steps..1 (descending)."""
+    if steps <= 0:
+        raise _lib.ConfigError("denoising needs at least one step")
+    return [1000.0 * j / steps for j in range(steps, 0, -1)]
+
+
+def denoise(steps: int, engines: list[ClipEngine], group=None) -> None:
+    """worker_denoise (pipeline.cpp:174-191) on every engine's clip (x, in place): for each
+    t of the timestep grid, y = eps_theta(x, t) through the block stack (with the context
+    sync when clip-parallel), then x -= y / steps."""
+    if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1:
+        engines[0].denoise_single(steps)
+        return
+    for t in timestep_grid(steps):
+        forward(t, engines, group)
+        for e in engines:
+            e.euler(1.0 / steps)

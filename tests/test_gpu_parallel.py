@@ -242,6 +242,30 @@ def test_engine_two_blocks(mods, oracle):
     assert normwise(to_np(e.y), want) <= TOL_F32
 
 
+@pytest.mark.parametrize("blocks,steps,n", [(1, 4, 1), (2, 3, 1), (1, 3, 2), (2, 2, 4)])
+def test_denoise_matches_reference_execute_run(mods, reference, blocks, steps, n):
+    # The reference's whole public run path (execute_run -> worker_denoise, runner.cpp:26-73,
+    # pipeline.cpp:174-191): `steps` Euler steps of a `blocks`-block stack, from the seeded
+    # latent, sequential (reference) vs clip-parallel over n engines (here).
+    _, _, en, _ = mods
+    F, H, W, Cc = 16, 4, 4, 32
+    wall, x0 = reference.execute_run(F, H, W, Cc, groups=4, n_local=8, n_global=4, blocks=blocks,
+                                     steps=steps, want_x0=True)
+    from paper_2406_16260_b200 import ops
+    x = ops.tensor_from_seed((F, H, W, Cc), 0)
+    engines = []
+    fc = F // n
+    for w in range(n):
+        e = _engine(mods, torch.float32, frames=F, workers=n, worker=w, height=H, width=W,
+                    channels=Cc, groups=4, n_local=8, n_global=4, blocks=blocks)
+        e.init_weights(1)
+        e.x.copy_(x[w * fc:(w + 1) * fc])
+        engines.append(e)
+    en.denoise(steps, engines)
+    got = torch.cat([e.x for e in engines])
+    assert normwise(to_np(got), x0) <= TOL_F32, normwise(to_np(got), x0)
+
+
 def test_engine_matches_reference_run_path(mods, reference):
     # The reference's own public run path, one Euler step of one block (runner.cpp:26-41):
     # x0 = x - (1/steps) * eps_theta(x, t=1000)
