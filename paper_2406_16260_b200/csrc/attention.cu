@@ -105,14 +105,14 @@ __global__ void __launch_bounds__(kCoreWarps * 32)
 
 }  // namespace
 
-int launch_attention_core(const void* qkv, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
+int launch_attention_core(const void* qkv, uint64_t qkv_rows, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
                           uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale, float bias,
                           void* ctx, bool ctx_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,
                           cudaStream_t s) {
     if (heads == 0 || C % heads != 0 || HW == 0) return int(cudaErrorInvalidValue);
     if (nq == 0) return 0;
     if (bf16 && ctx_bf16 && hi == nullptr && attention_tc_supported(C, heads, tt))
-        return launch_attention_core_tc(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s);
+        return launch_attention_core_tc(qkv, qkv_rows, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s);
     const size_t shm = sizeof(float) * kCoreWarps * (C + kMaxTokens);
     if (shm > 200 * 1024) return int(cudaErrorInvalidValue);
     const int out = hi != nullptr ? 2 : (ctx_bf16 ? 1 : 0);

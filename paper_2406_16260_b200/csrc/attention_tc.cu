@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -308,17 +309,310 @@ __global__ void __launch_bounds__(kTcThreads)
     cp_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------------
+// Lean ring kernel (the default). Same load sequence, smem layout and arithmetic as the
+// kernel above (so the same bits), restructured for instruction count, which is what bounds
+// the kernel above (ncu: ~76% issue-slot utilisation, HMMA ~4% of instructions):
+//   * the K/V row count is a template parameter (launch-wide max), so every S/PV tile loop
+//     is unrolled without per-tile branches;
+//   * ldmatrix addresses are per-lane constants plus immediates (the swizzle XOR depends
+//     only on lane bits);
+//   * the load sequence advances incrementally (no divisions), one barrier per chunk;
+//   * Q rows past the block's queries and K/V pad rows are never loaded (pad rows of every
+//     ring slot are zeroed once), and ctx staging is double-buffered.
+template <int NTL, int NS>
+struct LeanLay {
+    static constexpr uint32_t RP = NTL * 8;
+    static constexpr uint32_t SP = RP + 4;
+    static constexpr uint32_t stage = kQBlock * 128 + RP * 128;
+    static constexpr uint32_t pb = NS * stage;
+    static constexpr uint32_t sp = pb + kQBlock * 128;
+    static constexpr uint32_t ost = sp + kQBlock * SP * 4;
+    static constexpr uint32_t zinv = ost + 2 * kQBlock * 128;
+    static constexpr uint32_t total = zinv + kQBlock * 4;
+};
+
+template <int NTL, int NS>
+__global__ void __launch_bounds__(kTcThreads, 3)
+    attention_core_lean_kernel(const __nv_bfloat16* __restrict__ qkv, uint32_t HW, uint32_t C,
+                               uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt,
+                               float scale, float bias, __nv_bfloat16* __restrict__ ctx) {
+    using LL = LeanLay<NTL, NS>;
+    constexpr uint32_t RP = LL::RP;
+    constexpr int SP = int(LL::SP);
+    static_assert(NTL % 2 == 0 && NTL <= 8, "K/V rows padded to a multiple of 16, at most 64");
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t p = blockIdx.x, qb = blockIdx.y;
+    const uint32_t a0 = qb * kQBlock;
+    const uint32_t nqh = min(uint32_t(kQBlock), nq - a0);
+    const uint32_t R = tt.kv_count[qb];
+    const uint32_t d = C / heads, nch = d / kDC;
+    const uint64_t ld = 3ull * C;
+    const uint32_t sbase = dev::smem_u32(sm);
+    float* sp = reinterpret_cast<float*>(sm + LL::sp);
+    float* zinv = reinterpret_cast<float*>(sm + LL::zinv);
+
+    // K/V pad rows [R, RP) of every slot are never loaded: zero them once (P is 0 there
+    // and must meet finite V values)
+    for (uint32_t i = tid; i < (RP - R) * 8; i += kTcThreads) {
+        const uint32_t off = kQBlock * 128 + swz(R + (i >> 3), i & 7);
+#pragma unroll
+        for (int st = 0; st < NS; ++st)
+            *reinterpret_cast<uint4*>(sm + st * LL::stage + off) = make_uint4(0, 0, 0, 0);
+    }
+
+    // this thread's 16-byte pieces of every Q / K / V chunk
+    const uint32_t lr = tid >> 3, lp = tid & 7;
+    const bool q_ok = lr < nqh, k0_ok = lr < R, k1_ok = NTL > 4 && lr + 32 < R;
+    const uint16_t* kvf = tt.kv_frames + qb * kKvMax;
+    const __nv_bfloat16* q_src = qkv + uint64_t((q_frame0 + a0 + min(lr, nqh - 1)) * HW + p) * ld + lp * 8;
+    const __nv_bfloat16* k_src0 = qkv + uint64_t(uint32_t(kvf[min(lr, R - 1)]) * HW + p) * ld + lp * 8;
+    const __nv_bfloat16* k_src1 =
+        qkv + uint64_t(uint32_t(kvf[min(lr + 32, R - 1)]) * HW + p) * ld + lp * 8;
+    const uint32_t q_dst = swz(lr, lp);
+    const uint32_t kv_dst0 = kQBlock * 128 + swz(lr, lp);
+    const uint32_t kv_dst1 = kQBlock * 128 + swz(lr + 32, lp);
+    uint32_t ld_h = 0, ld_w = 0, ld_slot = 0;
+    auto issue = [&]() {
+        if (ld_h < heads) {
+            const bool qk = ld_w < nch;
+            const uint32_t col = ld_h * d + (qk ? ld_w : ld_w - nch) * kDC;
+            const uint32_t st = sbase + ld_slot * LL::stage;
+            if (qk && q_ok) cp_async16(st + q_dst, q_src + col);
+            const uint32_t kc = (qk ? C : 2 * C) + col;
+            if (k0_ok) cp_async16(st + kv_dst0, k_src0 + kc);
+            if (NTL > 4 && k1_ok) cp_async16(st + kv_dst1, k_src1 + kc);
+            if (++ld_w == 2 * nch) {
+                ld_w = 0;
+                ++ld_h;
+            }
+        }
+        cp_commit();
+        ld_slot = ld_slot + 1 == NS ? 0 : ld_slot + 1;
+    };
+#pragma unroll
+    for (int i = 0; i < NS - 1; ++i) issue();
+
+    // per-lane ldmatrix offsets: the XOR swizzle only involves lane bits
+    const int mt = warp & 1, wq = warp >> 1;
+    const uint32_t r7 = lane & 7, hi = lane >> 4, b1 = (lane >> 3) & 1;
+    uint32_t a_off[4], b_off[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        a_off[kk] = (mt * 16 + r7 + b1 * 8) * 128 + (((kk * 2 + hi) ^ r7) << 4);
+        b_off[kk] = kQBlock * 128 + r7 * 128 + (((kk * 2 + b1) ^ r7) << 4);
+    }
+    const uint32_t v_off = kQBlock * 128 + (r7 + b1 * 8) * 128 + (((2 * wq + hi) ^ r7) << 4);
+    const int g = lane >> 2, t4 = lane & 3;
+
+    uint32_t cslot = 0, och = 0;
+    for (uint32_t h = 0; h < heads; ++h) {
+        // ---------------- S = Q K^T ----------------
+        float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        for (uint32_t ch = 0; ch < nch; ++ch) {
+            cp_wait<NS - 2>();
+            __syncthreads();
+            issue();
+            const uint32_t st = sbase + cslot * LL::stage;
+            cslot = cslot + 1 == NS ? 0 : cslot + 1;
+#pragma unroll
+            for (int kk = 0; kk < kDC / 16; ++kk) {
+                uint32_t a[4];
+                ldsm_x4(st + a_off[kk], a[0], a[1], a[2], a[3]);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (4 * j < NTL && wq + 4 * j < NTL) {
+                        uint32_t b0, b1r;
+                        ldsm_x2(st + b_off[kk] + (wq + 4 * j) * 1024, b0, b1r);
+                        mma_bf16(acc[j], a[0], a[1], a[2], a[3], b0, b1r);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int nt = wq + 4 * j;
+            if (4 * j < NTL && nt < NTL) {
+                const int col = nt * 8 + t4 * 2;
+                *reinterpret_cast<float2*>(&sp[(mt * 16 + g) * SP + col]) = make_float2(acc[j][0], acc[j][1]);
+                *reinterpret_cast<float2*>(&sp[(mt * 16 + g + 8) * SP + col]) = make_float2(acc[j][2], acc[j][3]);
+            }
+        }
+        __syncthreads();
+        // ---------------- token softmax -> P (in place over S) ----------------
+        for (uint32_t a = warp; a < uint32_t(kQBlock); a += kTcWarps) {
+            float* row = sp + a * SP;
+            if (a < nqh) {
+                const uint32_t qa = a0 + a;
+                const int n = tt.count[qa];
+                const uint8_t* cols = tt.col + size_t(qa) * kMaxTokens;
+                const uint8_t* flg = tt.biased + size_t(qa) * kMaxTokens;
+                float lg[(kMaxTokens + 31) / 32];
+                int cl[(kMaxTokens + 31) / 32];
+                float m = -INFINITY;
+                const int nk = (n + 31) >> 5;
+#pragma unroll
+                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
+                    const int i = lane + 32 * k;
+                    cl[k] = 0;
+                    lg[k] = -INFINITY;
+                    if (k < nk && i < n) {
+                        cl[k] = int(cols[i]);
+                        lg[k] = scale * row[cl[k]] + (flg[i] ? bias : 0.f);
+                    }
+                    m = fmaxf(m, lg[k]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                float z = 0.f;
+#pragma unroll
+                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
+                    lg[k] = (k < nk && lane + 32 * k < n) ? expf(lg[k] - m) : 0.f;
+                    z += lg[k];
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+                __syncwarp();
+                for (int c = lane; c < SP; c += 32) row[c] = 0.f;
+                __syncwarp();
+                // duplicate tokens: at most two commutative additions per column
+#pragma unroll
+                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k)
+                    if (k < nk && lane + 32 * k < n) atomicAdd(&row[cl[k]], lg[k]);
+                if (lane == 0) zinv[a] = 1.0f / z;
+            } else {
+                for (int c = lane; c < SP; c += 32) row[c] = 0.f;
+                if (lane == 0) zinv[a] = 0.f;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i0 = 0; i0 < int(kQBlock * RP / 8); i0 += kTcThreads) {
+            const int i = i0 + tid;
+            if (i < int(kQBlock * RP / 8)) {
+                const uint32_t r = i / (RP / 8), c = i % (RP / 8);
+                const float zi = zinv[r];
+                const float4 s0 = *reinterpret_cast<const float4*>(sp + r * SP + c * 8);
+                const float4 s1 = *reinterpret_cast<const float4*>(sp + r * SP + c * 8 + 4);
+                const __nv_bfloat162 w0 = __floats2bfloat162_rn(s0.x * zi, s0.y * zi);
+                const __nv_bfloat162 w1 = __floats2bfloat162_rn(s0.z * zi, s0.w * zi);
+                const __nv_bfloat162 w2 = __floats2bfloat162_rn(s1.x * zi, s1.y * zi);
+                const __nv_bfloat162 w3 = __floats2bfloat162_rn(s1.z * zi, s1.w * zi);
+                *reinterpret_cast<uint4*>(sm + LL::pb + swz(r, c)) =
+                    make_uint4(*reinterpret_cast<const uint32_t*>(&w0), *reinterpret_cast<const uint32_t*>(&w1),
+                               *reinterpret_cast<const uint32_t*>(&w2), *reinterpret_cast<const uint32_t*>(&w3));
+            }
+        }
+        __syncthreads();
+        uint32_t pa[NTL / 2][4];
+#pragma unroll
+        for (int kq = 0; kq < NTL / 2; ++kq)
+            ldsm_x4(sbase + LL::pb + (mt * 16 + r7 + b1 * 8) * 128 + (((kq * 2 + hi) ^ r7) << 4),
+                    pa[kq][0], pa[kq][1], pa[kq][2], pa[kq][3]);
+        // ---------------- ctx = P V ----------------
+        for (uint32_t ch = 0; ch < nch; ++ch, ++och) {
+            cp_wait<NS - 2>();
+            __syncthreads();
+            if (ch > 0) {  // chunk ch-1 is staged: row stores of this block's queries
+                const uint8_t* ost = sm + LL::ost + ((och - 1) & 1) * (kQBlock * 128);
+                const uint32_t c0 = h * d + (ch - 1) * kDC;
+                if (tid < int(nqh) * 8) {
+                    const uint32_t r = tid >> 3, c = tid & 7;
+                    *reinterpret_cast<uint4*>(ctx + (uint64_t(a0 + r) * HW + p) * C + c0 + c * 8) =
+                        *reinterpret_cast<const uint4*>(ost + swz(r, c));
+                }
+            }
+            issue();
+            const uint32_t st = sbase + cslot * LL::stage;
+            cslot = cslot + 1 == NS ? 0 : cslot + 1;
+            float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+            for (int kq = 0; kq < NTL / 2; ++kq) {
+                uint32_t b[4];
+                ldsm_x4_t(st + v_off + kq * 2048, b[0], b[1], b[2], b[3]);
+                mma_bf16(o[0], pa[kq][0], pa[kq][1], pa[kq][2], pa[kq][3], b[0], b[1]);
+                mma_bf16(o[1], pa[kq][0], pa[kq][1], pa[kq][2], pa[kq][3], b[2], b[3]);
+            }
+            uint8_t* ost = sm + LL::ost + (och & 1) * (kQBlock * 128);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t col = (2 * wq + j) * 8 + t4 * 2;
+                const uint32_t r0 = mt * 16 + g;
+                *reinterpret_cast<__nv_bfloat162*>(ost + swz(r0, col >> 3) + (col & 7) * 2) =
+                    __floats2bfloat162_rn(o[j][0], o[j][1]);
+                *reinterpret_cast<__nv_bfloat162*>(ost + swz(r0 + 8, col >> 3) + (col & 7) * 2) =
+                    __floats2bfloat162_rn(o[j][2], o[j][3]);
+            }
+        }
+        __syncthreads();
+        {
+            const uint8_t* ost = sm + LL::ost + ((och - 1) & 1) * (kQBlock * 128);
+            const uint32_t c0 = h * d + (nch - 1) * kDC;
+            if (tid < int(nqh) * 8) {
+                const uint32_t r = tid >> 3, c = tid & 7;
+                *reinterpret_cast<uint4*>(ctx + (uint64_t(a0 + r) * HW + p) * C + c0 + c * 8) =
+                    *reinterpret_cast<const uint4*>(ost + swz(r, c));
+            }
+        }
+    }
+    cp_wait<0>();
+}
+
+template <int NTL, int NS>
+int launch_lean(const void* qkv, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
+                uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx,
+                cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attention_core_lean_kernel<NTL, NS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(LeanLay<NTL, NS>::total));
+        attr = true;
+    }
+    dim3 grid(HW, (nq + kQBlock - 1) / kQBlock);
+    attention_core_lean_kernel<NTL, NS><<<grid, kTcThreads, LeanLay<NTL, NS>::total, s>>>(
+        static_cast<const __nv_bfloat16*>(qkv), HW, C, heads, nq, q_frame0, tt, scale, bias,
+        static_cast<__nv_bfloat16*>(ctx));
+    return int(cudaGetLastError());
+}
+
 }  // namespace
+
+int g_attn_variant = -1;  // -1: unread; 0 lean ring kernel (default); 1 original ring kernel
 
 bool attention_tc_supported(uint32_t C, uint32_t heads, const TokenTable& tt) {
     return heads > 0 && C % heads == 0 && (C / heads) % kDC == 0 && tt.kv_ok;
 }
 
-int launch_attention_core_tc(const void* qkv, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
+int launch_attention_core_tc(const void* qkv, uint64_t qkv_rows, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
                              uint32_t q_frame0, TokenTable tt, float scale, float bias, void* ctx,
                              cudaStream_t s) {
     const uint32_t nqb = (nq + kQBlock - 1) / kQBlock;
-    const size_t shm = Lay((uint32_t(tt.max_kv) + 15) & ~15u).total;  // largest K/V list here
+    const uint32_t RPmax = (uint32_t(tt.max_kv) + 15) & ~15u;
+    if (g_attn_variant < 0) {
+        const char* v = getenv("VINF_ATTN_VARIANT");
+        g_attn_variant = v ? atoi(v) : 0;
+    }
+    if (g_attn_variant != 1) {
+        static int ns = -1;
+        if (ns < 0) {
+            const char* e = getenv("VINF_ATTN_STAGES");
+            ns = e ? atoi(e) : 6;
+        }
+#define LEAN(NTL)                                                                                \
+    (ns == 4   ? launch_lean<NTL, 4>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s)    \
+     : ns == 8 ? launch_lean<NTL, 8>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s)    \
+               : launch_lean<NTL, 6>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s))
+        switch (RPmax) {
+            case 16: return LEAN(2);
+            case 32: return LEAN(4);
+            case 48: return LEAN(6);
+            case 64: return LEAN(8);
+            default: break;
+        }
+#undef LEAN
+    }
+    const size_t shm = Lay(RPmax).total;  // largest K/V list here
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attention_core_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -219,7 +219,7 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
     {
     Span span(this, "attn_core", s);
-    cuda_check(launch_attention_core(qkv, !f32(), L.hw, C, L.d.heads, L.f_clip, L.ha,
+    cuda_check(launch_attention_core(qkv, uint64_t(L.af) * hw, !f32(), L.hw, C, L.d.heads, L.f_clip, L.ha,
                                      tt[bias_global ? 1 : 0], L.scale, L.d.bias, ctx, !f32(),
                                      f32() ? ctx : nullptr, ctxlo, s),
                "attention core");

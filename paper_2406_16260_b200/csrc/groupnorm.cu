@@ -186,6 +186,8 @@ __global__ void group_moments_kernel(const double* __restrict__ sums, double cou
     }
 }
 
+constexpr uint32_t kMaxGroupsApply = 1024;
+
 template <int VEC, bool IN_BF16, bool OUT_BF16, bool SPLIT>
 __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, uint32_t C,
                                    uint32_t groups, const double* __restrict__ means,
@@ -193,21 +195,34 @@ __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, ui
                                    const float* __restrict__ gamma, const float* __restrict__ beta,
                                    float eps, void* __restrict__ y, __nv_bfloat16* __restrict__ hi,
                                    __nv_bfloat16* __restrict__ lo) {
+    // per-channel (mean, scale, shift) built once per CTA in shared memory: the f64
+    // 1/sqrt per group and the f64 gamma product per channel (ops.cpp:152-160) are computed
+    // by a few threads instead of every thread redoing them for its 8 channels
+    extern __shared__ float tab[];  // [3][C]
+    __shared__ double inv_s[kMaxGroupsApply];
+    const uint32_t gs = C / groups;
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x)
+        inv_s[g] = 1.0 / sqrt(vars[g] + double(eps));  // ops.cpp:152
+    __syncthreads();
+    for (uint32_t ch = threadIdx.x; ch < C; ch += blockDim.x) {
+        const uint32_t g = ch / gs;
+        tab[ch] = float(means[g]);
+        tab[C + ch] = float(double(gamma[ch]) * inv_s[g]);
+        tab[2 * C + ch] = beta[ch];
+    }
+    __syncthreads();
     const uint32_t CC = C / VEC;
     const uint32_t R = blockDim.x / CC;
     const uint32_t cc = threadIdx.x % CC;
     const uint32_t rl = threadIdx.x / CC;
     if (rl >= R) return;
-    const uint32_t gs = C / groups;
     float mu[VEC], sc[VEC], bt[VEC];
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
         const uint32_t ch = cc * VEC + k;
-        const uint32_t g = ch / gs;
-        const double inv = 1.0 / sqrt(vars[g] + double(eps));  // ops.cpp:152
-        mu[k] = float(means[g]);
-        sc[k] = float(double(gamma[ch]) * inv);
-        bt[k] = beta[ch];
+        mu[k] = tab[ch];
+        sc[k] = tab[C + ch];
+        bt[k] = tab[2 * C + ch];
     }
     const uint64_t rstride = uint64_t(gridDim.x) * R;
     constexpr int UNR = 4;  // rows in flight per lane
@@ -409,9 +424,12 @@ int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, u
     const int cap = num_sms() * 4;
     if (grid > cap) grid = cap;
     const bool split = hi != nullptr;
+    if (groups > kMaxGroupsApply) return int(cudaErrorInvalidValue);
+    const size_t shm = sizeof(float) * 3 * C;
+    if (shm > 48 * 1024) return int(cudaErrorInvalidValue);
 #define GA(V, IB, OB, SP)                                                                     \
     if (vec == V && in_bf16 == IB && out_bf16 == OB && split == SP) {                         \
-        group_apply_kernel<V, IB, OB, SP><<<grid, block, 0, s>>>(x, rows, C, groups, means,   \
+        group_apply_kernel<V, IB, OB, SP><<<grid, block, shm, s>>>(x, rows, C, groups, means, \
                                                                  vars, gamma, beta, eps, y,   \
                                                                  hi, lo);                     \
         return int(cudaGetLastError());                                                       \

@@ -77,11 +77,12 @@ struct TokenTable {
 // attention_tc.cu: bf16 tensor-core core (head dim % 64 == 0, <= kKvMax K/V frames per
 // 32-query block); launch_attention_core dispatches to it when supported.
 bool attention_tc_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
-int launch_attention_core_tc(const void* qkv, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
+int launch_attention_core_tc(const void* qkv, uint64_t qkv_rows, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
                              uint32_t q_frame0, TokenTable tt, float scale, float bias, void* ctx,
                              cudaStream_t s);
 
-int launch_attention_core(const void* qkv, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
+// qkv_rows: rows of the QKV buffer (bounds of the TMA map the bf16 pipeline kernel reads it by)
+int launch_attention_core(const void* qkv, uint64_t qkv_rows, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
                           uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale, float bias,
                           void* ctx, bool ctx_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,
                           cudaStream_t s);

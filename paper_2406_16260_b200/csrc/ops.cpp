@@ -138,11 +138,18 @@ void check_tensor(const vinf_tensor* t, const char* what) {
 
 uint64_t numel(const vinf_tensor* t) { return uint64_t(t->f) * t->h * t->w * t->c; }
 
+static bool tmp_sync() {
+    static int v = -1;
+    if (v < 0) v = getenv("VINF_TMP_SYNC") ? 1 : 0;
+    return v == 1;
+}
 TmpBuf::TmpBuf(size_t bytes, cudaStream_t s) : s_(s) {
-    if (bytes) cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    if (bytes && tmp_sync()) cuda_check(cudaMalloc(&p, bytes + 4096), "cudaMalloc");
+    else if (bytes) cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
 }
 TmpBuf::~TmpBuf() {
-    if (p) cudaFreeAsync(p, s_);
+    if (p && tmp_sync()) { cudaStreamSynchronize(s_); cudaFree(p); }
+    else if (p) cudaFreeAsync(p, s_);
 }
 
 // Operand view of a [rows, C] activation; fp32 inputs are split into hi/lo planes.
@@ -266,7 +273,7 @@ void attention_generic(const void* src, vinf_dtype dt, uint32_t frames, uint32_t
     TmpBuf ctx(qrows * C * 4, s);  // bf16 ctx or hi+lo planes
     auto* hi = static_cast<__nv_bfloat16*>(ctx.p);
     auto* lo = hi + qrows * C;
-    cuda_check(launch_attention_core(qkv.p, !f32, hw, C, p->heads, nq, q0, dt_tok.tt, p->scale,
+    cuda_check(launch_attention_core(qkv.p, rows, !f32, hw, C, p->heads, nq, q0, dt_tok.tt, p->scale,
                                      bias, hi, !f32, f32 ? hi : nullptr, f32 ? lo : nullptr, s),
                "attention core");
     Operand O;
