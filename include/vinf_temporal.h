@@ -206,7 +206,8 @@ typedef struct {
     uint64_t bytes;
 } vinf_xfer;
 /* Transfers of one exchange stage in a deadlock-free order (every send has exactly one
- * matching receive with the same tag on the peer). */
+ * matching receive with the same tag on the peer). out = NULL with cap = 0 only sets
+ * *count (size query). */
 int vinf_layout_exchange(const vinf_layout* l, int stage, vinf_xfer* out, uint32_t cap,
                          uint32_t* count);
 /* Logical bytes the reference's sync would move for this worker per block
@@ -249,6 +250,17 @@ int vinf_engine_forward(vinf_engine* e, double t, void* stream);
 int vinf_engine_io(const vinf_engine* e, void** x, void** y);
 /* euler_update_inplace (pipeline.cpp:93-100): x -= lambda * y. */
 int vinf_engine_euler(vinf_engine* e, double lambda, void* stream);
+/* Sync ablation (the reference's `ablate` run key, pipeline.cpp:150-170; values are its
+ * LayerKind numbers, metrics.hpp:11). The driver must skip that kind's exchange (or the
+ * all-reduce, for groupnorm); the engine then uses zero context frames (conv: halo
+ * slots; attention: halo + remote global slots) or clip-local GroupNorm statistics. */
+enum {
+    VINF_ABLATE_NONE = 0,
+    VINF_ABLATE_CONV = 1,
+    VINF_ABLATE_GROUPNORM = 2,
+    VINF_ABLATE_ATTENTION = 3
+};
+int vinf_engine_set_ablation(vinf_engine* e, int kind);
 /* worker_denoise (pipeline.cpp:174-191) for one worker: for t in timestep_grid(steps)
  * (1000 j / steps, j = steps..1): y = eps_theta(x, t); x -= y / steps. Result in x. */
 int vinf_engine_denoise(vinf_engine* e, uint32_t steps, void* stream);

@@ -371,3 +371,86 @@ class Reference:
                                            workers, C.c_uint64(seed), C.c_uint64(weight_seed),
                                            _p(x0, _f32p), C.byref(wall)))
         return (wall.value, x0) if want_x0 else wall.value
+
+
+class ReferenceRunAPI:
+    """The reference's OWN run-level C API (include/vinf.h:27-75) as exported by
+    oracle/_ref/libvinf_ref.so (its capi.cpp compiled in) — the checker for
+    include/vinf_run.h. Methods return (status, value) so tests can compare codes."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = C.CDLL(path)
+        vp = C.c_void_p
+        sigs = {
+            "vinf_config_create": (C.c_int, [C.POINTER(vp)]),
+            "vinf_config_destroy": (None, [vp]),
+            "vinf_config_load_file": (C.c_int, [vp, C.c_char_p]),
+            "vinf_config_set": (C.c_int, [vp, C.c_char_p, C.c_char_p]),
+            "vinf_config_validate": (C.c_int, [vp]),
+            "vinf_config_digest": (C.c_int, [vp, _u64p]),
+            "vinf_config_canonical": (C.c_int, [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+            "vinf_run": (C.c_int, [vp, C.c_char_p, C.c_char_p, _f64p]),
+            "vinf_verify": (C.c_int, [C.c_char_p, C.c_char_p, C.c_double, _f64p, _u64p]),
+            "vinf_bench": (C.c_int, [vp, _u32p, C.c_size_t, C.c_char_p, C.c_char_p, C.c_size_t,
+                                     C.POINTER(C.c_size_t)]),
+            "vinf_validate_schedule": (C.c_int, [C.c_uint32, C.c_int, C.POINTER(C.c_int), _u32p,
+                                                 _u64p, C.c_char_p, C.c_size_t]),
+            "vinf_last_error": (C.c_char_p, []),
+        }
+        for n, (r, a) in sigs.items():
+            f = getattr(L, n)
+            f.restype, f.argtypes = r, a
+        self.lib = L
+
+    def config(self, values: dict | None = None, path: str | None = None):
+        h = C.c_void_p()
+        assert self.lib.vinf_config_create(C.byref(h)) == 0
+        rc = 0
+        if path is not None:
+            rc = self.lib.vinf_config_load_file(h, path.encode())
+        for k, v in (values or {}).items():
+            if rc == 0:
+                rc = self.lib.vinf_config_set(h, str(k).encode(), str(v).encode())
+        return h, rc
+
+    def free(self, h):
+        self.lib.vinf_config_destroy(h)
+
+    def canonical(self, h) -> str:
+        buf = C.create_string_buffer(8192)
+        n = C.c_size_t()
+        assert self.lib.vinf_config_canonical(h, buf, 8192, C.byref(n)) == 0
+        return buf.value.decode()
+
+    def digest(self, h) -> int:
+        d = C.c_uint64()
+        assert self.lib.vinf_config_digest(h, C.byref(d)) == 0
+        return d.value
+
+    def run(self, h, out_path=None, metrics_path=None):
+        wall = C.c_double()
+        rc = self.lib.vinf_run(h, out_path.encode() if out_path else None,
+                               metrics_path.encode() if metrics_path else None, C.byref(wall))
+        return rc, wall.value
+
+    def verify(self, a, b, tol):
+        md, bad = C.c_double(), C.c_uint64()
+        rc = self.lib.vinf_verify(a.encode(), b.encode(), tol, C.byref(md), C.byref(bad))
+        return rc, md.value, bad.value
+
+    def bench(self, h, sweep, metrics_path=None):
+        arr = (C.c_uint32 * max(1, len(sweep)))(*sweep)
+        buf = C.create_string_buffer(1 << 16)
+        n = C.c_size_t()
+        rc = self.lib.vinf_bench(h, arr, len(sweep), metrics_path.encode() if metrics_path else None,
+                                 buf, 1 << 16, C.byref(n))
+        return rc, buf.value.decode()
+
+    def validate_schedule(self, workers, literal):
+        done, rounds, transfers = C.c_int(), C.c_uint32(), C.c_uint64()
+        buf = C.create_string_buffer(4096)
+        rc = self.lib.vinf_validate_schedule(workers, int(literal), C.byref(done), C.byref(rounds),
+                                             C.byref(transfers), buf, 4096)
+        return rc, bool(done.value), rounds.value, transfers.value, buf.value.decode()

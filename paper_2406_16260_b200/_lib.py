@@ -17,6 +17,7 @@ VINF_F32, VINF_BF16 = 0, 1
 VINF_BUF_X, VINF_BUF_Y, VINF_BUF_CONV_IN, VINF_BUF_ATTN_IN, VINF_BUF_GN_SUMS = range(5)
 VINF_XCHG_CONV, VINF_XCHG_ATTN = 0, 1
 VINF_STAGE_STUB, VINF_STAGE_CONV, VINF_STAGE_GN_APPLY, VINF_STAGE_ATTENTION = range(4)
+VINF_ABLATE_NONE, VINF_ABLATE_CONV, VINF_ABLATE_GROUPNORM, VINF_ABLATE_ATTENTION = range(4)
 
 
 class VinfError(RuntimeError):
@@ -123,6 +124,21 @@ _SIGS = {
     "vinf_engine_forward": (C.c_int, [_vp, C.c_double, _vp]),
     "vinf_engine_io": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
     "vinf_engine_euler": (C.c_int, [_vp, C.c_double, _vp]),
+    "vinf_engine_set_ablation": (C.c_int, [_vp, C.c_int]),
+    # run-level API (include/vinf_run.h)
+    "vinf_config_create": (C.c_int, [C.POINTER(_vp)]),
+    "vinf_config_destroy": (None, [_vp]),
+    "vinf_config_load_file": (C.c_int, [_vp, C.c_char_p]),
+    "vinf_config_set": (C.c_int, [_vp, C.c_char_p, C.c_char_p]),
+    "vinf_config_validate": (C.c_int, [_vp]),
+    "vinf_config_digest": (C.c_int, [_vp, _u64p]),
+    "vinf_config_canonical": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "vinf_run": (C.c_int, [_vp, C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]),
+    "vinf_verify": (C.c_int, [C.c_char_p, C.c_char_p, C.c_double, C.POINTER(C.c_double), _u64p]),
+    "vinf_bench": (C.c_int, [_vp, _u32p, C.c_size_t, C.c_char_p, C.c_char_p, C.c_size_t,
+                             C.POINTER(C.c_size_t)]),
+    "vinf_validate_schedule": (C.c_int, [C.c_uint32, C.c_int, C.POINTER(C.c_int), _u32p, _u64p,
+                                         C.c_char_p, C.c_size_t]),
     "vinf_engine_denoise": (C.c_int, [_vp, C.c_uint32, _vp]),
     "vinf_engine_launches": (C.c_uint64, [_vp]),
     "vinf_engine_profile": (C.c_int, [_vp, C.c_int]),

@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libvinf_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["gemm_tc.cu", "elementwise.cu", "groupnorm.cu", "attention.cu", "attention_tc.cu", "plan.cpp", "ops.cpp",
-           "engine.cpp", "capi.cpp"]
+           "engine.cpp", "capi.cpp", "runapi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
@@ -30,6 +30,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "--expt-
 def _headers_mtime() -> float:
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
     hs.append(os.path.join(ROOT, "include", "vinf_temporal.h"))
+    hs.append(os.path.join(ROOT, "include", "vinf_run.h"))
     return max(os.path.getmtime(h) for h in hs)
 
 

@@ -386,6 +386,7 @@ int vinf_layout_exchange(const vinf_layout* l, int stage, vinf_xfer* out, uint32
         const auto& xs = stage == VINF_XCHG_CONV ? l->L.xconv : l->L.xattn;
         if (stage != VINF_XCHG_CONV && stage != VINF_XCHG_ATTN) range_error("unknown stage");
         if (count) *count = uint32_t(xs.size());
+        if (!out && cap == 0) return;  // size query
         if (xs.size() > cap) range_error("output capacity too small");
         if (!xs.empty()) std::memcpy(out, xs.data(), xs.size() * sizeof(vinf_xfer));
     });

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 
@@ -47,8 +48,27 @@ struct vinf_engine {
     Layout L;
     uint8_t* ws = nullptr;
     std::vector<EngineBlock> blocks;
-    TokenTable tt[2];
+    TokenTable tt[4];  // [ablated attention sync * 2 + bias_global]
     uint64_t launches = 0;
+
+    // The single-worker block stack is a fixed launch sequence per timestep regime (the
+    // only t dependence is the strict t > t_star bias flag, ops.cpp:298), so it is captured
+    // once per regime into a CUDA graph and replayed: no per-kernel launch gaps. Captured
+    // on a private stream (the caller's may be the legacy stream), launched on the caller's.
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t nlaunch = 0;
+        int calls = 0;
+    };
+    Graph graphs[2];
+    cudaStream_t cap_stream = nullptr;
+    bool use_graphs = getenv("VINF_NO_GRAPH") == nullptr;
+    void drop_graphs() {
+        for (auto& g : graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            g = Graph{};
+        }
+    }
 
     // Optional per-kernel timing: CUDA events recorded on the launching stream around
     // each kernel (group), aggregated by name on request (vinf_engine_kernel_stats).
@@ -95,8 +115,18 @@ struct vinf_engine {
         return at((blocks.size() - 1 - b) % 2 == 0 ? L.off_y : L.off_tmp);
     }
     void* x_of(uint32_t b) const { return b == 0 ? at(L.off_x) : y_of(b - 1); }
-    double gn_count() const {  // elements per group over the whole video
-        return double(uint64_t(L.d.frames) * L.hw * L.d.channels / L.d.groups);
+    double gn_count() const {  // elements per group over the whole video (or the clip)
+        const uint64_t f = ablate == VINF_ABLATE_GROUPNORM ? L.f_clip : L.d.frames;
+        return double(f * L.hw * L.d.channels / L.d.groups);
+    }
+
+    // Sync ablation (pipeline.cpp:150-170 with `ablate`): the driver skips that kind's
+    // exchange and the engine stands in zero context frames (conv / attention: the
+    // receive slots are zeroed before use) or clip-local statistics (groupnorm).
+    int ablate = VINF_ABLATE_NONE;
+    void zero_recv_slots(const std::vector<vinf_xfer>& xs, cudaStream_t s) {
+        for (const vinf_xfer& x : xs)
+            if (!x.send) cuda_check(cudaMemsetAsync(ws + x.offset, 0, x.bytes, s), "ablation zero");
     }
 
     void stage_stub(uint32_t b, cudaStream_t s);
@@ -126,6 +156,7 @@ void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
 void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     const EngineBlock& B = blocks.at(b);
     const uint32_t C = L.d.channels;
+    if (ablate == VINF_ABLATE_CONV) zero_recv_slots(L.xconv, s);
     Operand A;
     A.hi = at<__nv_bfloat16>(L.off_u0);
     A.lo = f32() ? at<__nv_bfloat16>(L.off_u0lo) : nullptr;
@@ -190,6 +221,7 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
 void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     const EngineBlock& B = blocks.at(b);
     const uint32_t C = L.d.channels;
+    if (ablate == VINF_ABLATE_ATTENTION) zero_recv_slots(L.xattn, s);
     const uint64_t hw = L.hw;
     Operand A;
     A.hi = at<__nv_bfloat16>(L.off_u2);
@@ -213,14 +245,16 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     project(L.ha, L.f_clip, true);                           // own frames: Q, K, V
     project(L.ha - L.npre_a, L.npre_a, false);               // pre halo: K, V
     project(L.ha + L.f_clip, L.npost_a, false);              // post halo: K, V
-    project(2 * L.ha + L.f_clip, L.n_remote, false);         // remote global frames: K, V
+    const bool abl = ablate == VINF_ABLATE_ATTENTION;
+    // remote global frames (+ the zero null frame the ablated tables point at): K, V
+    project(2 * L.ha + L.f_clip, L.n_remote + (abl ? 1 : 0), false);
     const bool bias_global = t > L.d.t_star;                  // ops.cpp:298
     auto* ctx = at<__nv_bfloat16>(L.off_ctx);
     auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
     {
     Span span(this, "attn_core", s);
     cuda_check(launch_attention_core(qkv, uint64_t(L.af) * hw, !f32(), L.hw, C, L.d.heads, L.f_clip, L.ha,
-                                     tt[bias_global ? 1 : 0], L.scale, L.d.bias, ctx, !f32(),
+                                     tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale, L.d.bias, ctx, !f32(),
                                      f32() ? ctx : nullptr, ctxlo, s),
                "attention core");
     }
@@ -260,8 +294,8 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
         e->ws = static_cast<uint8_t*>(workspace);
         const Layout& L = e->L;
         cuda_check(cudaMemsetAsync(e->ws, 0, L.total, s), "workspace memset");
-        std::vector<uint8_t> blob[2];
-        for (int b = 0; b < 2; ++b) {
+        std::vector<uint8_t> blob[4];
+        for (int b = 0; b < 4; ++b) {
             uint8_t* p = e->at(L.off_tok[b]);
             blob[b].resize(L.tok[b].blob_bytes());
             L.tok[b].pack(blob[b].data());
@@ -285,6 +319,8 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
 
 void vinf_engine_destroy(vinf_engine* e) {
     if (!e) return;
+    e->drop_graphs();
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     for (cudaEvent_t ev : e->pool) cudaEventDestroy(ev);
     for (auto& B : e->blocks) {
         if (B.f32) cudaFree(B.f32);
@@ -300,6 +336,7 @@ int vinf_engine_set_block(vinf_engine* e, uint32_t block, const float* stub_a,
                           const float* gamma, const float* beta, const float* wq, const float* wk,
                           const float* wv, const float* wo, void* stream) {
     return guarded_call([&] {
+        if (e) e->drop_graphs();
         if (!e) shape_error("null engine");
         if (block >= e->blocks.size()) range_error("block index out of range");
         auto s = static_cast<cudaStream_t>(stream);
@@ -328,6 +365,7 @@ int vinf_engine_set_block(vinf_engine* e, uint32_t block, const float* stub_a,
 int vinf_engine_init_weights(vinf_engine* e, uint64_t weight_seed, void* stream) {
     return guarded_call([&] {
         if (!e) shape_error("null engine");
+        e->drop_graphs();
         auto s = static_cast<cudaStream_t>(stream);
         const uint32_t C = e->L.d.channels, taps = e->L.d.taps;
         const float mat = 1.0f / std::sqrt(float(C));  // pipeline.cpp:44
@@ -378,19 +416,74 @@ int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void*
     });
 }
 
+namespace {
+
+void run_stack(vinf_engine* e, double t, cudaStream_t s) {
+    for (uint32_t b = 0; b < e->blocks.size(); ++b) {
+        e->stage_stub(b, s);
+        e->stage_conv(b, s);
+        e->stage_gn_apply(b, s);
+        e->stage_attention(b, t, s);
+    }
+}
+
+// One pass of the block stack: replayed from the regime's graph once it has been seen
+// twice (the first pass runs eagerly and sets every lazily-initialised kernel attribute).
+void forward_stack(vinf_engine* e, double t, cudaStream_t s) {
+    if (e->profiling || !e->use_graphs) {
+        run_stack(e, t, s);
+        return;
+    }
+    auto& g = e->graphs[t > e->L.d.t_star ? 1 : 0];
+    if (!g.exec && g.calls++ >= 1) {
+        if (!e->cap_stream)
+            cuda_check(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking), "capture stream");
+        const uint64_t l0 = e->launches;
+        cuda_check(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            run_stack(e, t, e->cap_stream);
+        } catch (...) {
+            cudaGraph_t broken = nullptr;
+            cudaStreamEndCapture(e->cap_stream, &broken);
+            if (broken) cudaGraphDestroy(broken);
+            e->launches = l0;
+            throw;
+        }
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamEndCapture(e->cap_stream, &graph), "end capture");
+        const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(ie, "graph instantiate");
+        g.nlaunch = e->launches - l0;
+        e->launches = l0;
+    }
+    if (g.exec) {
+        cuda_check(cudaGraphLaunch(g.exec, s), "graph launch");
+        e->launches += g.nlaunch;
+    } else {
+        run_stack(e, t, s);
+    }
+}
+
+}  // namespace
+
 int vinf_engine_forward(vinf_engine* e, double t, void* stream) {
     return guarded_call([&] {
         if (!e) shape_error("null engine");
         if (e->L.d.workers != 1)
             config_error("vinf_engine_forward runs a single worker; use vinf_engine_stage with a "
                          "transport for workers > 1");
-        auto s = static_cast<cudaStream_t>(stream);
-        for (uint32_t b = 0; b < e->blocks.size(); ++b) {
-            e->stage_stub(b, s);
-            e->stage_conv(b, s);
-            e->stage_gn_apply(b, s);
-            e->stage_attention(b, t, s);
-        }
+        forward_stack(e, t, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int vinf_engine_set_ablation(vinf_engine* e, int kind) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        if (kind < VINF_ABLATE_NONE || kind > VINF_ABLATE_ATTENTION)
+            config_error("ablation kind must be none, conv, groupnorm or attention");
+        e->ablate = kind;
+        e->drop_graphs();
     });
 }
 
@@ -416,12 +509,7 @@ int vinf_engine_denoise(vinf_engine* e, uint32_t steps, void* stream) {
         // worker_denoise (pipeline.cpp:174-191): t_j = 1000 j / steps, j = steps..1
         for (uint32_t j = steps; j >= 1; --j) {
             const double t = 1000.0 * j / steps;
-            for (uint32_t b = 0; b < e->blocks.size(); ++b) {
-                e->stage_stub(b, s);
-                e->stage_conv(b, s);
-                e->stage_gn_apply(b, s);
-                e->stage_attention(b, t, s);
-            }
+            forward_stack(e, t, s);
             cuda_check(launch_euler(e->at(e->L.off_x), e->at(e->L.off_y), !e->f32(),
                                     e->clip_elems(), 1.0 / steps, s),
                        "euler");

@@ -207,15 +207,20 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
             g_frame[j] = 2 * ha + f_clip + n_remote++;
     }
     cf = hc + f_clip + hc;
-    af = 2 * ha + f_clip + n_remote;
+    null_frame = 2 * ha + f_clip + n_remote;
+    af = null_frame + 1;
 
-    // Token lists (clip_parallel.cpp:285-305): window first, then the global set.
-    for (int b = 0; b < 2; ++b) {
+    // Token lists (clip_parallel.cpp:285-305): window first, then the global set. With
+    // the attention sync ablated the reference attends zero stand-ins for every global
+    // token (clip_parallel.cpp:118-121, 315-318), own members included: tables 2, 3 point
+    // all global tokens at the never-written null frame.
+    for (int b = 0; b < 4; ++b) {
         tok[b].resize(f_clip);
         for (uint32_t a = 0; a < f_clip; ++a) {
             for (uint32_t g : build_local_window(start + a, d.frames, d.n_local))
-                tok[b].push(a, ha + g - start, b == 0);
-            for (uint32_t j = 0; j < d.n_global; ++j) tok[b].push(a, g_frame[j], b == 1);
+                tok[b].push(a, ha + g - start, (b & 1) == 0);
+            for (uint32_t j = 0; j < d.n_global; ++j)
+                tok[b].push(a, b >= 2 ? null_frame : g_frame[j], (b & 1) == 1);
         }
         tok[b].finalize();
     }
@@ -247,8 +252,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
                                        uint64_t(256) * 2 * d.channels);  // colpart segments
     off_scratch = take(sizeof(double) * scratch_elems);
     off_colstats = take(sizeof(float) * 2 * d.channels * ((uint64_t(f_clip) * hw + 31) / 32));
-    off_tok[0] = take(tok[0].blob_bytes());
-    off_tok[1] = take(tok[1].blob_bytes());
+    for (int b = 0; b < 4; ++b) off_tok[b] = take(tok[b].blob_bytes());
     total = off;
 
     build_exchanges();

@@ -25,6 +25,8 @@ from ._lib import EngineDesc
 from .transport import Msg, Transport
 
 _TORCH_DT = {_lib.VINF_F32: torch.float32, _lib.VINF_BF16: torch.bfloat16}
+_ABLATE = {None: _lib.VINF_ABLATE_NONE, "none": _lib.VINF_ABLATE_NONE, "conv": _lib.VINF_ABLATE_CONV,
+           "groupnorm": _lib.VINF_ABLATE_GROUPNORM, "attention": _lib.VINF_ABLATE_ATTENTION}
 
 
 def make_desc(frames, workers=1, worker=0, height=32, width=32, channels=320, taps=3, groups=32,
@@ -118,6 +120,12 @@ class ClipEngine:
         """x -= lam * y (euler_update_inplace, pipeline.cpp:93-100)."""
         _lib.check(_lib.load().vinf_engine_euler(self._h, C.c_double(lam), self._stream()))
 
+    def set_ablation(self, kind: str | None) -> None:
+        """Sync ablation (the reference's `ablate` key): None | "conv" | "groupnorm" |
+        "attention". forward()/denoise() must be given the same kind so the group skips
+        that exchange."""
+        _lib.check(_lib.load().vinf_engine_set_ablation(self._h, _ABLATE[kind]))
+
     def denoise_single(self, steps: int) -> None:
         _lib.check(_lib.load().vinf_engine_denoise(self._h, steps, self._stream()))
 
@@ -190,26 +198,30 @@ class DistGroup:
         self.t.allreduce_sum_(e.gn_sums)
 
 
-def forward(t: float, engines: list[ClipEngine], group=None) -> None:
+def forward(t: float, engines: list[ClipEngine], group=None, ablate: str | None = None) -> None:
     """All blocks of eps_theta_worker for every engine in `engines` (pipeline.cpp:150-170):
     stub -> [conv halo sync] -> conv + residual with fused GN (sum, sum^2) partials ->
     [one all-reduce of 2*groups f64] -> GN apply -> [attention halo + global sync] ->
-    dual-scope attention + residual."""
+    dual-scope attention + residual. `ablate` skips that kind's sync (engines configured
+    with set_ablation(ablate))."""
     blocks = engines[0].layout.desc.blocks
-    if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1:
+    if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1 and not ablate:
         engines[0].forward_single(t)
         return
     group = group or LocalGroup()
     for b in range(blocks):
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_STUB, t)
-        group.exchange(engines, _lib.VINF_XCHG_CONV)
+        if ablate != "conv":
+            group.exchange(engines, _lib.VINF_XCHG_CONV)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_CONV, t)
-        group.allreduce_sums(engines)
+        if ablate != "groupnorm":
+            group.allreduce_sums(engines)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_GN_APPLY, t)
-        group.exchange(engines, _lib.VINF_XCHG_ATTN)
+        if ablate != "attention":
+            group.exchange(engines, _lib.VINF_XCHG_ATTN)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_ATTENTION, t)
 
@@ -221,14 +233,14 @@ def timestep_grid(steps: int) -> list[float]:
     return [1000.0 * j / steps for j in range(steps, 0, -1)]
 
 
-def denoise(steps: int, engines: list[ClipEngine], group=None) -> None:
+def denoise(steps: int, engines: list[ClipEngine], group=None, ablate: str | None = None) -> None:
     """worker_denoise (pipeline.cpp:174-191) on every engine's clip (x, in place): for each
     t of the timestep grid, y = eps_theta(x, t) through the block stack (with the context
     sync when clip-parallel), then x -= y / steps."""
-    if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1:
+    if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1 and not ablate:
         engines[0].denoise_single(steps)
         return
     for t in timestep_grid(steps):
-        forward(t, engines, group)
+        forward(t, engines, group, ablate)
         for e in engines:
             e.euler(1.0 / steps)

@@ -8,11 +8,11 @@ import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "vinf_temporal.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("vinf_temporal.h", "vinf_run.h")]
 
 
 def header_functions():
-    txt = open(HEADER).read()
+    txt = "".join(open(h).read() for h in HEADERS)
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(vinf_[a-z0-9_]+)\s*\(", txt)))
 
