@@ -38,6 +38,11 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-hw", type=int, default=8, help="spatial crop side for CPU arms")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "vc2"],
+                    help="cfg2: BASELINE configs[1]/[2] (default, the headline); vc2: configs[3], "
+                         "the VideoCrafter2-shaped level stack over --frames frames (strong scaling)")
+    ap.add_argument("--frames", type=int, default=2304,
+                    help="vc2 workload: total frames (2300 rounded up to a multiple of 8 GPUs)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the torch.distributed/NCCL exchange path even with one rank")
     return ap.parse_args()
@@ -421,10 +426,109 @@ def run_ours(args):
     return 0
 
 
+VC2_LEVELS = [(320, 40, 64), (640, 20, 32), (1280, 10, 16), (1280, 5, 8)]  # (C, H, W), SURVEY §8(a)
+
+
+def run_vc2(args):
+    """BASELINE configs[3]: the VideoCrafter2-shaped temporal-layer stack, one dual-scope
+    block per level (C, HxW) = (320, 40x64), (640, 20x32), (1280, 10x16), (1280, 5x8), over
+    --frames frames split into N clips (strong scaling; 2300 -> 2304 so 8 divides it). A step
+    = every level's block over this GPU's clip, with the 3-step sync per level when N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_16260_b200 import engine as en
+    from paper_2406_16260_b200 import ops
+    from paper_2406_16260_b200.transport import DistTransport
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(world, 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = en.DistGroup(DistTransport())
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    F = args.frames
+    if F % n:
+        raise SystemExit(f"--frames {F} must be a multiple of the GPU count {n}")
+    fc = F // n
+    engines = []
+    for li, (c, h, w) in enumerate(VC2_LEVELS):
+        desc = en.make_desc(F, n, rank, h, w, c, TAPS, GROUPS, HEADS, N_LOCAL, N_GLOBAL, BIAS,
+                            T_STAR, 1e-5, 0.0, 1, dtype)
+        e = en.ClipEngine(en.Layout(desc), device=dev)
+        e.init_weights(1 + li)
+        e.x.copy_(ops.tensor_from_seed((fc, h, w, c), li, first_elem=rank * fc * h * w * c,
+                                       dtype=dtype, device=dev))
+        engines.append(e)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        for e in engines:
+            en.forward(T_STEP, [e], group)
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(engines) + 1)]
+           for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    with clocks:
+        barrier()
+        for k in range(args.steps):
+            evs[k][0].record(stream)
+            for li, e in enumerate(engines):
+                en.forward(T_STEP, [e], group)
+                evs[k][li + 1].record(stream)
+        barrier()
+    total_ms = evs[0][0].elapsed_time(evs[-1][-1])
+    ms_t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = F * args.steps / (ms / 1000.0)
+    level_ms = [sum(evs[k][li].elapsed_time(evs[k][li + 1]) for k in range(args.steps)) / args.steps
+                for li in range(len(engines))]
+    hbm, tf_burst, tf_sus, src = peaks()
+    flops = [14.0 * fc * h * w * c * c for (c, h, w) in VC2_LEVELS]  # conv 6MC^2 + qkv 6MC^2 + o 2MC^2
+    levels = [{"channels": c, "height": h, "width": w, "ms": m,
+               "achieved_tflops": fl / (m / 1000.0) / 1e12,
+               "frac_of_sustained": fl / (m / 1000.0) / 1e12 / tf_sus}
+              for (c, h, w), m, fl in zip(VC2_LEVELS, level_ms, flops)]
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": args.dtype, "data": "synthetic (tensor_from_seed / build_model seeds)",
+                "config": {"workload": "BASELINE configs[3]: VideoCrafter2-shaped temporal stack, one "
+                                       "dual-scope block per level", "frames": F, "frames_per_gpu": fc,
+                           "levels": [list(x) for x in VC2_LEVELS], "groups": GROUPS,
+                           "n_local": N_LOCAL, "n_global": N_GLOBAL, "t": T_STEP,
+                           "parallelism": f"clip-parallel x{n}",
+                           "note": "2300 frames rounded to 2304 (the reference requires N | F)"},
+                "block_roofline": {"flops_per_step": sum(flops),
+                                   "achieved_tflops": sum(flops) / (ms / args.steps / 1000.0) / 1e12,
+                                   "frac_of_sustained": sum(flops) / (ms / args.steps / 1000.0) / 1e12 / tf_sus},
+                "levels": levels, "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "vc2":
+        return run_vc2(args)
     return run_ours(args)
 
 
