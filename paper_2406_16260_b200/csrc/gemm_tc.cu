@@ -68,43 +68,58 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 
 // Epilogue of one 128 x BN tile for the warp owning TMEM lane quadrant q (rows m0..m0+31).
 //   OBF: output (and residual) bf16, else fp32.   RES: residual present.
+// Each 32 x 32 accumulator chunk is transposed through the warp's padded smem block so a
+// lane then owns 8 consecutive columns of 4 rows (rows tr + 8i): residual loads and output
+// stores are 16-byte (bf16) row segments, 4 lanes covering a row's 64 bytes.
+template <bool OBF>
+struct EpiRes {
+    static constexpr int W = OBF ? 4 : 8;  // 32-bit words of 8 residual values
+    uint32_t w[4][W];
+};
+
+template <int BN, bool OBF, bool RES>
+__device__ __forceinline__ void epi_load_res(const GemmParams& p, EpiRes<OBF>& rr, int lane, int m0,
+                                             int n0, int c, bool full, int n_lim) {
+    if (!RES) return;
+    using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
+    const T* res = static_cast<const T*>(p.res);
+    const int tr = lane >> 2, n = n0 + c + (lane & 3) * 8;
+    const bool store = !(p.flags & kGemmFlagNoStore);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gm = int64_t(m0) + tr + 8 * i;
+        const bool ok = store && (full || (gm < p.M && n < n_lim)) && n < n_lim;
+        const T* src = res + (ok ? gm * p.res_ld + n : 0);
+        uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
+        if (ok) {
+            a = __ldg(reinterpret_cast<const uint4*>(src));
+            if (!OBF) b = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+        }
+        rr.w[i][0] = a.x;
+        rr.w[i][1] = a.y;
+        rr.w[i][2] = a.z;
+        rr.w[i][3] = a.w;
+        if (!OBF) {
+            rr.w[i][4 % EpiRes<OBF>::W] = b.x;
+            rr.w[i][5 % EpiRes<OBF>::W] = b.y;
+            rr.w[i][6 % EpiRes<OBF>::W] = b.z;
+            rr.w[i][7 % EpiRes<OBF>::W] = b.w;
+        }
+    }
+}
+
 template <int BN, bool OBF, bool RES, bool ST>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int q, int lane,
-                                              uint32_t stg, int m0, int n0, int half) {
+                                              uint32_t stg, int m0, int n0, int half,
+                                              EpiRes<OBF>& rr) {
     using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
-    constexpr int RW = OBF ? 2 : 4;  // residual words per 4 columns
-    const int tr = lane >> 3;        // transposed: row within each group of 4
-    const int tc = (lane & 7) * 4;   // transposed: first of 4 columns
+    const int tr = lane >> 2;        // transposed: rows tr + 8i
+    const int tc = (lane & 3) * 8;   // transposed: first of 8 columns
     const int n_lim = min(p.N, n0 + BN);
     const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
     const bool store = !(p.flags & kGemmFlagNoStore);
-    const T* res = static_cast<const T*>(p.res);
     T* out = static_cast<T*>(p.out);
-    uint32_t rraw[8][RW];
-    auto load_res = [&](int c) {
-        if (!RES) return;
-        const int n = n0 + c + tc;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t gm = int64_t(m0) + tr + 4 * i;
-            const bool ok = store && (full || (gm < p.M && n < n_lim));
-            const T* src = res + (ok ? gm * p.res_ld + n : 0);
-            if (OBF) {
-                uint2 w = make_uint2(0u, 0u);
-                if (ok) w = __ldg(reinterpret_cast<const uint2*>(src));
-                rraw[i][0] = w.x;
-                rraw[i][1 % RW] = w.y;
-            } else {
-                uint4 w = make_uint4(0u, 0u, 0u, 0u);
-                if (ok) w = __ldg(reinterpret_cast<const uint4*>(src));
-                rraw[i][0] = w.x;
-                rraw[i][1 % RW] = w.y;
-                rraw[i][2 % RW] = w.z;
-                rraw[i][3 % RW] = w.w;
-            }
-        }
-    };
-    load_res(32 * half);
+    // rr already holds this warp's first chunk (loaded before the accumulator was ready)
 #pragma unroll 1
     for (int c = 32 * half; c < BN; c += 64) {
         uint32_t r[32];
@@ -115,80 +130,92 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
 #pragma unroll
         for (int j = 0; j < 8; ++j) sts128(srow + 16 * j, r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
         __syncwarp();
-        float cur[8][4];
+        float cur[4][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float4 v = lds128(stg + uint32_t(((tr + 4 * i) * kStgPitch + tc) * 4));
-            cur[i][0] = v.x;
-            cur[i][1] = v.y;
-            cur[i][2] = v.z;
-            cur[i][3] = v.w;
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t a = stg + uint32_t(((tr + 8 * i) * kStgPitch + tc) * 4);
+            const float4 v0 = lds128(a), v1 = lds128(a + 16);
+            cur[i][0] = v0.x; cur[i][1] = v0.y; cur[i][2] = v0.z; cur[i][3] = v0.w;
+            cur[i][4] = v1.x; cur[i][5] = v1.y; cur[i][6] = v1.z; cur[i][7] = v1.w;
             if (RES) {
-                if (OBF) {
-                    cur[i][0] += __uint_as_float(rraw[i][0] << 16);
-                    cur[i][1] += __uint_as_float(rraw[i][0] & 0xFFFF0000u);
-                    cur[i][2] += __uint_as_float(rraw[i][1 % RW] << 16);
-                    cur[i][3] += __uint_as_float(rraw[i][1 % RW] & 0xFFFF0000u);
-                } else {
-                    cur[i][0] += __uint_as_float(rraw[i][0]);
-                    cur[i][1] += __uint_as_float(rraw[i][1 % RW]);
-                    cur[i][2] += __uint_as_float(rraw[i][2 % RW]);
-                    cur[i][3] += __uint_as_float(rraw[i][3 % RW]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (OBF) {
+                        const uint32_t w = rr.w[i][k >> 1];
+                        cur[i][k] += __uint_as_float((k & 1) ? (w & 0xFFFF0000u) : (w << 16));
+                    } else {
+                        cur[i][k] += __uint_as_float(rr.w[i][k % EpiRes<OBF>::W]);
+                    }
                 }
             }
         }
         __syncwarp();
-        if (c + 64 < BN && n0 + c + 64 < n_lim) load_res(c + 64);  // prefetch this warp's next chunk
+        if (c + 64 < BN && n0 + c + 64 < n_lim)
+            epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, c + 64, full, n_lim);  // next chunk
         if (!store) continue;
         const int n = n0 + c + tc;
-        float b4[4] = {0.f, 0.f, 0.f, 0.f};
+        float b8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (p.bias && n < n_lim) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n));
-            b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + n));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + n) + 1);
+            b8[0] = b0.x; b8[1] = b0.y; b8[2] = b0.z; b8[3] = b0.w;
+            b8[4] = b1.x; b8[5] = b1.y; b8[6] = b1.z; b8[7] = b1.w;
         }
-        float cs[4] = {0.f, 0.f, 0.f, 0.f}, cq[4] = {0.f, 0.f, 0.f, 0.f};  // column stats
+        float cs[8], cq[8];  // column stats of the stored values
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t gm = int64_t(m0) + tr + 4 * i;
+        for (int k = 0; k < 8; ++k) cs[k] = cq[k] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t gm = int64_t(m0) + tr + 8 * i;
             if (!full && (gm >= p.M || n >= n_lim)) continue;
             // BN not a multiple of 32 (e.g. 240): the last chunk of an interior tile would
             // spill into the next tile's columns
             if (BN % 32 != 0 && n >= n_lim) continue;
             T* dst = out + gm * p.out_ld + n;
-            float y[4] = {cur[i][0] + b4[0], cur[i][1] + b4[1], cur[i][2] + b4[2], cur[i][3] + b4[3]};
+            float y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = cur[i][k] + b8[k];
             if (OBF) {
-                const __nv_bfloat162 lo2 = __floats2bfloat162_rn(y[0], y[1]);
-                const __nv_bfloat162 hi2 = __floats2bfloat162_rn(y[2], y[3]);
-                *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<const uint32_t*>(&lo2),
-                                                            *reinterpret_cast<const uint32_t*>(&hi2));
-                if (ST) {  // statistics of the stored (rounded) values
-                    y[0] = __low2float(lo2); y[1] = __high2float(lo2);
-                    y[2] = __low2float(hi2); y[3] = __high2float(hi2);
+                uint32_t w[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+                    w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+                    if (ST) {  // statistics of the stored (rounded) values
+                        y[2 * h] = __low2float(b2);
+                        y[2 * h + 1] = __high2float(b2);
+                    }
                 }
+                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
             } else {
                 *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+                *reinterpret_cast<float4*>(dst + 4) = make_float4(y[4], y[5], y[6], y[7]);
             }
             if (ST) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 8; ++k) {
                     cs[k] += y[k];
                     cq[k] = fmaf(y[k], y[k], cq[k]);
                 }
             }
         }
         if (ST) {
-            // lanes l, l^8, l^16, l^24 hold the same 4 columns for different rows
+            // lanes l ^ {4, 8, 16} hold the same 8 columns for the block's other rows
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 8; ++k) {
+                cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], 4);
                 cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], 8);
                 cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], 16);
+                cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 4);
                 cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 8);
                 cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 16);
             }
-            if (tr == 0 && n < n_lim && m0 < p.M) {  // this warp owns (row block, 4 columns)
+            if (tr == 0 && n < n_lim && m0 < p.M) {  // this warp owns (row block, 8 columns)
                 float* part = p.colpart + int64_t(m0 >> 5) * 2 * p.N + n;
                 *reinterpret_cast<float4*>(part) = make_float4(cs[0], cs[1], cs[2], cs[3]);
+                *reinterpret_cast<float4*>(part + 4) = make_float4(cs[4], cs[5], cs[6], cs[7]);
                 *reinterpret_cast<float4*>(part + p.N) = make_float4(cq[0], cq[1], cq[2], cq[3]);
+                *reinterpret_cast<float4*>(part + p.N + 4) = make_float4(cq[4], cq[5], cq[6], cq[7]);
             }
         }
     }
@@ -301,13 +328,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stg =
             dev::smem_u32(smem + S * Cfg::kStageBytes + 256) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0;
+        EpiRes<OBF> rr;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const uint32_t acc = local & 1;
+            const int m0 = (tile / n_tiles) * kBM + q * 32, n0 = (tile % n_tiles) * BN;
+            {  // the residual does not depend on the accumulator: fetch it while the MMA runs
+                const int n_lim = min(p.N, n0 + BN);
+                const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
+                if (n0 + 32 * half < n_lim)
+                    epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, 32 * half, full, n_lim);
+            }
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
-            epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
-                                            (tile / n_tiles) * kBM + q * 32, (tile % n_tiles) * BN,
-                                            half);
+            epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0, n0,
+                                            half, rr);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
