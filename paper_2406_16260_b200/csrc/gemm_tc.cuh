@@ -59,7 +59,11 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
                    uint64_t ld_elems, uint32_t box_rows);
 
 // Launches the GEMM on `stream`; picks the N tile. Returns 0 or a cudaError_t.
-int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream);
+// pair: the CTA-pair (cta_group::2) kernel; its B maps must have box rows = block_n / 2.
+int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream,
+                   bool pair = false);
+// Whether a GEMM of this shape uses the CTA-pair kernel (VINF_GEMM_PAIR=0/1 overrides).
+bool gemm_use_pair(int M, int N, int block_n);
 
 // Largest supported N tile for a given N (used to build B tensor maps).
 int gemm_pick_block_n(int N);

@@ -79,13 +79,15 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
     if (M <= 0 || N <= 0) return;
     if (split && (!A.lo || !B.lo)) shape_error("gemm: split mode needs lo planes");
     const int bn = gemm_pick_block_n(int(N));
+    const bool pair = gemm_use_pair(int(M), int(N), bn);
+    const uint32_t b_box = uint32_t(pair ? bn / 2 : bn);  // the pair kernel loads half of B per CTA
     GemmMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     cuda_check(make_tmap_bf16(&maps.a[0], A.hi, A.rows, A.cols, A.ld, 128), "tmap A");
-    cuda_check(make_tmap_bf16(&maps.b[0], B.hi, B.rows, B.K, B.K, uint32_t(bn)), "tmap B");
+    cuda_check(make_tmap_bf16(&maps.b[0], B.hi, B.rows, B.K, B.K, b_box), "tmap B");
     if (split) {
         cuda_check(make_tmap_bf16(&maps.a[1], A.lo, A.rows, A.cols, A.ld, 128), "tmap A.lo");
-        cuda_check(make_tmap_bf16(&maps.b[1], B.lo, B.rows, B.K, B.K, uint32_t(bn)), "tmap B.lo");
+        cuda_check(make_tmap_bf16(&maps.b[1], B.lo, B.rows, B.K, B.K, b_box), "tmap B.lo");
     } else {
         maps.a[1] = maps.a[0];
         maps.b[1] = maps.b[0];
@@ -119,7 +121,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         p.out_bf16 = ep.out_bf16;
         p.flags = g_gemm_debug_flags;
         if (c0 + kGemmMaxSeg >= segs.size()) p.colpart = ep.colpart;  // final output only
-        cuda_check(gemm_tc_launch(maps, p, bn, s), "gemm_tc_launch");
+        cuda_check(gemm_tc_launch(maps, p, bn, s, pair), "gemm_tc_launch");
     }
 }
 
