@@ -43,11 +43,11 @@ struct TileCfg {
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
     static constexpr int kStages =
-        std::min<int>(8, (227 * 1024 - 1024 - 256 - kStgBytes) / kStageBytes);
+        std::min<int>(8, (227 * 1024 - 1024 - 1024 - kStgBytes) / kStageBytes);
     static constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;  // TMEM columns per buffer
     static constexpr uint32_t kTmemCols = 2 * kAccStride;
     static constexpr uint32_t kSmemBytes =
-        kStages * kStageBytes + 1024 /*align*/ + 256 /*bars*/ + kStgBytes;
+        kStages * kStageBytes + 1024 /*align*/ + 1024 /*bars*/ + kStgBytes;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -222,7 +222,91 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     }
 }
 
-template <int BN, bool OBF, bool RES, bool ST>
+// TMA-store epilogue (bf16 output, no residual, no column statistics: the Q/K/V
+// projections). A lane converts its accumulator row's 32 columns to bf16 and writes them
+// (64 B) into the warp's staging block in the TMA box layout (32 x 32, 64B swizzle: 16 B
+// chunk j of row r sits at chunk j ^ ((r >> 1) & 3), conflict-free); one lane then stores
+// the block with cp.async.bulk.tensor. Half the smem traffic of the fp32 transpose, and
+// full-line writes without per-lane store instructions. Two staging blocks per warp
+// alternate; a block is rewritten only after its previous store has read it. A partial
+// 16-column chunk (BN = 240) goes out as direct 16-byte row stores.
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t smem_src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(smem_src)
+                 : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* omap,
+                                                  uint32_t tmem_acc, int q, int lane, uint32_t stg,
+                                                  int m0, int n0, int half, uint32_t& nstore) {
+    const int n_lim = min(p.N, n0 + BN);
+    const bool store = !(p.flags & kGemmFlagNoStore);
+#pragma unroll 1
+    for (int c = 32 * half; c < BN; c += 64) {
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(tmem_acc + (uint32_t(q * 32) << 16) + c, r);
+        dev::tmem_wait_ld();
+        const int nb = n0 + c;
+        if (nb >= n_lim || !store) continue;  // warp-uniform
+        float y[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) y[k] = __uint_as_float(r[k]);
+        if (p.bias) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                if (nb + 4 * v < n_lim) {
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + nb) + v);
+                    y[4 * v] += b.x;
+                    y[4 * v + 1] += b.y;
+                    y[4 * v + 2] += b.z;
+                    y[4 * v + 3] += b.w;
+                }
+            }
+        }
+        uint32_t w[16];
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+            w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        if (BN % 32 != 0 && nb + 32 > n0 + BN) {
+            // partial chunk of a 240-wide tile: 16 columns, direct row stores
+            const int64_t gm = int64_t(m0) + lane;
+            if (gm < p.M) {
+                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + gm * p.out_ld + nb;
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+                    if (nb + 8 * v < n_lim)
+                        *reinterpret_cast<uint4*>(dst + 8 * v) =
+                            make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+            }
+            continue;
+        }
+        const uint32_t buf = stg + (nstore & 1) * 2048;
+        if (nstore >= 2) {  // the store that last used this block has finished reading it
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+        }
+        const uint32_t row = buf + lane * 64, sw = (lane >> 1) & 3;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sts128(row + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+        dev::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(omap, buf, nb, m0);
+            dev::bulk_commit();
+        }
+        ++nstore;
+    }
+}
+
+template <int BN, bool OBF, bool RES, bool ST, bool TMAO = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
     using Cfg = TileCfg<BN, ST>;
@@ -327,13 +411,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;            // TMEM lane quadrant this warp may access
         const int half = (warp - 4) >> 2;  // which alternate 32-column chunks it takes
         const uint32_t stg =
-            dev::smem_u32(smem + S * Cfg::kStageBytes + 256) + (warp - 4) * (32 * kStgPitch * 4);
-        uint32_t local = 0;
+            dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
+        uint32_t local = 0, nstore = 0;
         EpiRes<OBF> rr;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const uint32_t acc = local & 1;
             const int m0 = (tile / n_tiles) * kBM + q * 32, n0 = (tile % n_tiles) * BN;
-            {  // the residual does not depend on the accumulator: fetch it while the MMA runs
+            if (!TMAO) {  // the residual does not depend on the accumulator: fetch it early
                 const int n_lim = min(p.N, n0 + BN);
                 const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
                 if (n0 + 32 * half < n_lim)
@@ -341,12 +425,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
-            epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0, n0,
-                                            half, rr);
+            if constexpr (TMAO)
+                epilogue_tile_tma<BN>(p, &maps.out, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
+                                      m0, n0, half, nstore);
+            else
+                epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0,
+                                                n0, half, rr);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (TMAO && lane == 0) bulk_wait_read<0>();  // staging must outlive the stores' reads
     }
 
     dev::tc_fence_before();
@@ -370,11 +459,11 @@ struct PairCfg {
     static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
     static constexpr int kStages =
-        std::min<int>(8, (227 * 1024 - 1024 - 256 - kStgBytes) / kStageBytes);
+        std::min<int>(8, (227 * 1024 - 1024 - 1024 - kStgBytes) / kStageBytes);
     static constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;
     static constexpr uint32_t kTmemCols = 2 * kAccStride;
     static constexpr uint32_t kSmemBytes =
-        kStages * kStageBytes + 1024 /*align*/ + 256 /*bars*/ + kStgBytes;
+        kStages * kStageBytes + 1024 /*align*/ + 1024 /*bars*/ + kStgBytes;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -540,7 +629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int q = warp & 3;
         const int half = (warp - 4) >> 2;
         const uint32_t stg =
-            dev::smem_u32(smem + S * Cfg::kStageBytes + 256) + (warp - 4) * (32 * kStgPitch * 4);
+            dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0;
         EpiRes<OBF> rr;
         for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
@@ -588,12 +677,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 int g_num_sms = 0;
 
-template <int BN, bool OBF, bool RES, bool ST = false>
+template <int BN, bool OBF, bool RES, bool ST = false, bool TMAO = false>
 int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     using Cfg = TileCfg<BN, ST>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES, ST>,
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(Cfg::kSmemBytes));
         if (e != cudaSuccess) return int(e);
@@ -607,7 +696,7 @@ int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     }
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
     const int grid = std::max(1, std::min(tiles, g_num_sms));
-    gemm_tc_kernel<BN, OBF, RES, ST><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
+    gemm_tc_kernel<BN, OBF, RES, ST, TMAO><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
     return int(cudaGetLastError());
 }
 
@@ -620,6 +709,8 @@ int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
         return p.out_bf16 ? launch_cfg<BN, true, true, true>(maps, p, stream)
                           : launch_cfg<BN, false, true, true>(maps, p, stream);
     }
+    if (p.out_bf16 && !res && (p.flags & kGemmFlagTmaOut))
+        return launch_cfg<BN, true, false, false, true>(maps, p, stream);
     if (p.out_bf16) return res ? launch_cfg<BN, true, true>(maps, p, stream)
                                : launch_cfg<BN, true, false>(maps, p, stream);
     return res ? launch_cfg<BN, false, true>(maps, p, stream)
@@ -678,6 +769,19 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
                     gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
+int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems) {
+    auto fn = get_encode_fn();
+    if (!fn) return int(cudaErrorNotSupported);
+    cuuint64_t gdim[2] = {cols, rows};
+    cuuint64_t gstride[1] = {ld_elems * 2};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estride,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 

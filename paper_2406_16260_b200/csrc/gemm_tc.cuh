@@ -47,16 +47,20 @@ struct GemmParams {
 };
 
 constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic
+constexpr int32_t kGemmFlagTmaOut = 1 << 8;  // bf16 output leaves through TMA stores (maps.out)
 
 struct GemmMaps {
     CUtensorMap a[2];
     CUtensorMap b[2];
+    CUtensorMap out;  // [M, N] bf16, box 32 x 32, 64B swizzle (with kGemmFlagTmaOut)
 };
 
 // Host side: encode a 2D bf16 K-major tensor map over [rows, cols] with row stride
 // ld_elems, box = 64 (K) x box_rows, 128B swizzle.
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                    uint64_t ld_elems, uint32_t box_rows);
+// The epilogue's output map: bf16 [rows, cols] (row stride ld_elems), box 32 x 32, 64B swizzle.
+int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems);
 
 // Launches the GEMM on `stream`; picks the N tile. Returns 0 or a cudaError_t.
 // pair: the CTA-pair (cta_group::2) kernel; its B maps must have box rows = block_n / 2.

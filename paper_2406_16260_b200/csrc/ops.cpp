@@ -92,6 +92,13 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         maps.a[1] = maps.a[0];
         maps.b[1] = maps.b[0];
     }
+    // bf16 output without residual / statistics (the Q/K/V projections): TMA-store epilogue
+    const bool tma_out = ep.out_bf16 && !ep.res && !ep.colpart && !split && !pair &&
+                         reinterpret_cast<uintptr_t>(ep.out) % 16 == 0 && ep.out_ld % 8 == 0 &&
+                         getenv("VINF_GEMM_NO_TMA_OUT") == nullptr;
+    if (tma_out)
+        cuda_check(make_tmap_out_bf16(&maps.out, ep.out, uint64_t(M), uint64_t(N), uint64_t(ep.out_ld)),
+                   "tmap out");
     std::vector<GemmSeg> segs;
     for (size_t i = 0; i < a_rows.size(); ++i) {
         const int32_t ar = int32_t(a_rows[i]), br = int32_t(b_rows[i]);
@@ -119,7 +126,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         p.out = ep.out;
         p.out_ld = ep.out_ld;
         p.out_bf16 = ep.out_bf16;
-        p.flags = g_gemm_debug_flags;
+        p.flags = g_gemm_debug_flags | (tma_out ? kGemmFlagTmaOut : 0);
         if (c0 + kGemmMaxSeg >= segs.size()) p.colpart = ep.colpart;  // final output only
         cuda_check(gemm_tc_launch(maps, p, bn, s, pair), "gemm_tc_launch");
     }
