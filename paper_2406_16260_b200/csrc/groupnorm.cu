@@ -281,6 +281,62 @@ __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, ui
 }
 
 // Block = CC * R threads with R = max(1, 256 / CC); returns 0 if C is too wide.
+// bf16 -> bf16 apply (the engine's bf16 mode), shaped like the stub kernel: 16-byte rows
+// in flight as raw words (4 registers each) so four CTAs fit an SM; per-channel
+// (mean, scale, shift) built once per CTA with the same f64 arithmetic as above, so the
+// output bits equal group_apply_kernel<8, true, true, false>'s.
+__global__ void __launch_bounds__(256, 4)
+    group_apply_bf16_kernel(const uint4* __restrict__ x, uint64_t rows, uint32_t C, uint32_t groups,
+                            const double* __restrict__ means, const double* __restrict__ vars,
+                            const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                            uint4* __restrict__ y) {
+    extern __shared__ float tab[];  // [3][C]
+    __shared__ double inv_s[kMaxGroupsApply];
+    const uint32_t gs = C / groups;
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x)
+        inv_s[g] = 1.0 / sqrt(vars[g] + double(eps));  // ops.cpp:152
+    __syncthreads();
+    for (uint32_t ch = threadIdx.x; ch < C; ch += blockDim.x) {
+        const uint32_t g = ch / gs;
+        tab[ch] = float(means[g]);
+        tab[C + ch] = float(double(gamma[ch]) * inv_s[g]);
+        tab[2 * C + ch] = beta[ch];
+    }
+    __syncthreads();
+    constexpr int UNR = 4;
+    const uint32_t CC = C / 8, R = blockDim.x / CC;
+    const uint32_t cc = threadIdx.x % CC, rl = threadIdx.x / CC;
+    if (rl >= R) return;
+    float mu[8], sc[8], bt[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        mu[k] = tab[cc * 8 + k];
+        sc[k] = tab[C + cc * 8 + k];
+        bt[k] = tab[2 * C + cc * 8 + k];
+    }
+    const uint64_t rstride = uint64_t(gridDim.x) * R;
+    for (uint64_t r = uint64_t(blockIdx.x) * R + rl; r < rows; r += UNR * rstride) {
+        uint4 w[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (r + u * rstride < rows) w[u] = __ldg(x + (r + u * rstride) * CC + cc);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (r + u * rstride >= rows) break;
+            const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+            uint32_t o[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float x0 = __uint_as_float(ws[h] << 16), x1 = __uint_as_float(ws[h] & 0xFFFF0000u);
+                const __nv_bfloat162 b2 = __floats2bfloat162_rn(fmaf(x0 - mu[2 * h], sc[2 * h], bt[2 * h]),
+                                                                fmaf(x1 - mu[2 * h + 1], sc[2 * h + 1], bt[2 * h + 1]));
+                o[h] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            y[(r + u * rstride) * CC + cc] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
 inline int block_for(uint32_t C, int vec, int* R) {
     const uint32_t CC = C / vec;
     if (CC == 0 || CC > 1024) return 0;
@@ -427,6 +483,12 @@ int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, u
     if (groups > kMaxGroupsApply) return int(cudaErrorInvalidValue);
     const size_t shm = sizeof(float) * 3 * C;
     if (shm > 48 * 1024) return int(cudaErrorInvalidValue);
+    if (vec == 8 && in_bf16 && out_bf16 && !split) {
+        group_apply_bf16_kernel<<<grid, block, shm, s>>>(static_cast<const uint4*>(x), rows, C, groups,
+                                                         means, vars, gamma, beta, eps,
+                                                         static_cast<uint4*>(y));
+        return int(cudaGetLastError());
+    }
 #define GA(V, IB, OB, SP)                                                                     \
     if (vec == V && in_bf16 == IB && out_bf16 == OB && split == SP) {                         \
         group_apply_kernel<V, IB, OB, SP><<<grid, block, shm, s>>>(x, rows, C, groups, means, \
