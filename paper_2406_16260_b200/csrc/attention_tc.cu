@@ -327,13 +327,17 @@ struct LeanLay {
     static constexpr uint32_t stage = kQBlock * 128 + RP * 128;
     static constexpr uint32_t pb = NS * stage;
     static constexpr uint32_t sp = pb + kQBlock * 128;
-    static constexpr uint32_t ost = sp + kQBlock * SP * 4;
-    static constexpr uint32_t zinv = ost + 2 * kQBlock * 128;
+    // ctx staging (2 x 32 rows x 128 B) reuses the P / S scratch: P lives in registers
+    // for the whole PV phase and S is dead by then
+    static constexpr uint32_t ost = pb;
+    static constexpr uint32_t scratch = kQBlock * 128 + kQBlock * SP * 4;
+    static constexpr uint32_t zinv = pb + (scratch > 2 * kQBlock * 128 ? scratch : 2 * kQBlock * 128);
     static constexpr uint32_t total = zinv + kQBlock * 4;
+    static constexpr int min_blocks = (NTL <= 4 && NS <= 5) ? 4 : 3;  // CTAs per SM the smem allows
 };
 
 template <int NTL, int NS>
-__global__ void __launch_bounds__(kTcThreads, 3)
+__global__ void __launch_bounds__(kTcThreads, LeanLay<NTL, NS>::min_blocks)
     attention_core_lean_kernel(const __nv_bfloat16* __restrict__ qkv, uint32_t HW, uint32_t C,
                                uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt,
                                float scale, float bias, __nv_bfloat16* __restrict__ ctx) {
@@ -597,10 +601,11 @@ int launch_attention_core_tc(const void* qkv, uint64_t qkv_rows, uint32_t HW, ui
         static int ns = -1;
         if (ns < 0) {
             const char* e = getenv("VINF_ATTN_STAGES");
-            ns = e ? atoi(e) : 6;
+            ns = e ? atoi(e) : 5;
         }
 #define LEAN(NTL)                                                                                \
     (ns == 4   ? launch_lean<NTL, 4>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s)    \
+     : ns == 5 ? launch_lean<NTL, 5>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s)    \
      : ns == 8 ? launch_lean<NTL, 8>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s)    \
                : launch_lean<NTL, 6>(qkv, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, s))
         switch (RPmax) {

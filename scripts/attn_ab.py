@@ -50,7 +50,7 @@ if __name__ == "__main__":
         sys.exit(0)
     os.makedirs(OUT, exist_ok=True)
     variants = [("ring", {"VINF_ATTN_VARIANT": "1"})] + [
-        (f"lean{n}", {"VINF_ATTN_VARIANT": "0", "VINF_ATTN_STAGES": str(n)}) for n in (4, 6, 8)]
+        (f"lean{n}", {"VINF_ATTN_VARIANT": "0", "VINF_ATTN_STAGES": str(n)}) for n in (4, 5, 6)]
     for workers, worker in ((1, 0), (4, 1)):
         res = {}
         for v, extra in variants:
