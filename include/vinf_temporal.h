@@ -174,6 +174,10 @@ typedef struct {
     float scale;        /* 0 -> 1/sqrtf(C/heads) */
     uint32_t blocks;
     vinf_dtype dtype;
+    /* Extension (not in the reference, which needs workers | frames, clip_parallel.cpp:56-59):
+     * 1 = uneven clips, worker w owning frames [floor(w*F/N), floor((w+1)*F/N)), e.g. the
+     * paper's 2,300 frames over 8 GPUs. 0 = the reference's even split. */
+    uint32_t uneven;
 } vinf_engine_desc;
 
 typedef struct vinf_layout vinf_layout;
@@ -181,6 +185,8 @@ typedef struct vinf_layout vinf_layout;
 int vinf_layout_create(const vinf_engine_desc* d, vinf_layout** out);
 void vinf_layout_destroy(vinf_layout* l);
 int vinf_layout_workspace_bytes(const vinf_layout* l, uint64_t* bytes);
+/* This worker's clip: first global frame and frame count. */
+int vinf_layout_clip(const vinf_layout* l, uint32_t* start, uint32_t* frames);
 
 /* Named regions of the workspace (for the caller's views / tests). */
 enum {

@@ -65,7 +65,7 @@ class EngineDesc(C.Structure):
                 ("taps", C.c_uint32), ("groups", C.c_uint32), ("heads", C.c_uint32),
                 ("n_local", C.c_uint32), ("n_global", C.c_uint32), ("bias", C.c_float),
                 ("t_star", C.c_double), ("epsilon", C.c_float), ("scale", C.c_float),
-                ("blocks", C.c_uint32), ("dtype", C.c_int)]
+                ("blocks", C.c_uint32), ("dtype", C.c_int), ("uneven", C.c_uint32)]
 
 
 class Xfer(C.Structure):
@@ -113,6 +113,7 @@ _SIGS = {
     "vinf_layout_create": (C.c_int, [C.POINTER(EngineDesc), C.POINTER(_vp)]),
     "vinf_layout_destroy": (None, [_vp]),
     "vinf_layout_workspace_bytes": (C.c_int, [_vp, _u64p]),
+    "vinf_layout_clip": (C.c_int, [_vp, _u32p, _u32p]),
     "vinf_layout_region": (C.c_int, [_vp, C.c_int, _u64p, _u64p, _u64p]),
     "vinf_layout_exchange": (C.c_int, [_vp, C.c_int, C.POINTER(Xfer), C.c_uint32, _u32p]),
     "vinf_layout_reference_traffic": (C.c_int, [_vp, _u64p, _u64p, _u64p]),

@@ -379,6 +379,14 @@ int vinf_layout_region(const vinf_layout* l, int which, uint64_t* offset, uint64
     });
 }
 
+int vinf_layout_clip(const vinf_layout* l, uint32_t* start, uint32_t* frames) {
+    return guarded_call([&] {
+        if (!l) shape_error("null layout");
+        if (start) *start = l->L.start;
+        if (frames) *frames = l->L.f_clip;
+    });
+}
+
 int vinf_layout_exchange(const vinf_layout* l, int stage, vinf_xfer* out, uint32_t cap,
                          uint32_t* count) {
     return guarded_call([&] {

@@ -41,6 +41,11 @@ struct Layout {
 
     std::vector<vinf_xfer> xconv, xattn;
 
+    // First global frame of worker w: w*F/N (even split) or floor(w*F/N) (uneven clips)
+    uint32_t clip_start(uint32_t w) const {
+        return uint32_t(uint64_t(w) * d.frames / d.workers);
+    }
+
    private:
     void build_exchanges();
 };

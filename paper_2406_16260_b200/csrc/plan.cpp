@@ -168,22 +168,30 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     if (!(d.epsilon > 0.0f)) config_error("group norm epsilon must be > 0");
     if (d.channels % 8 != 0)
         shape_error("the clip engine needs channels % 8 == 0 (16-byte TMA rows)");
-    f_clip = make_plan(d.frames, d.workers);
+    if (d.uneven) {
+        if (d.workers == 0 || d.frames < d.workers) config_error("uneven clips need frames >= workers >= 1");
+    } else {
+        make_plan(d.frames, d.workers);  // the reference's even split (clip_parallel.cpp:56-59)
+    }
     if (d.worker >= d.workers) range_error("worker index out of range");
+    f_clip = clip_start(d.worker + 1) - clip_start(d.worker);
+    uint32_t min_clip = f_clip;
+    for (uint32_t w = 0; w < d.workers; ++w)
+        min_clip = std::min(min_clip, clip_start(w + 1) - clip_start(w));
     hw = d.height * d.width;
     hc = (d.taps - 1) / 2;
     ha = d.n_local / 2;
     // pipeline.cpp:131-143
-    if (hc > f_clip)
+    if (hc > min_clip)
         config_error("conv halo exceeds clip: (taps-1)/2 = " + std::to_string(hc) +
-                     " > frames/workers = " + std::to_string(f_clip));
-    if (ha > f_clip)
+                     " > frames/workers = " + std::to_string(min_clip));
+    if (ha > min_clip)
         config_error("attention halo exceeds clip: n_local/2 = " + std::to_string(ha) +
-                     " > frames/workers = " + std::to_string(f_clip));
+                     " > frames/workers = " + std::to_string(min_clip));
     if (d.n_local + 1 + d.n_global > uint32_t(kMaxTokens))
         config_error("n_local + 1 + n_global exceeds " + std::to_string(kMaxTokens));
     gset = build_global_index_set(d.frames, d.n_global);
-    start = d.worker * f_clip;
+    start = clip_start(d.worker);
     f32 = d.dtype == VINF_F32;
     es = f32 ? 4 : 2;
     E = uint64_t(hw) * d.channels;
@@ -195,8 +203,8 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     npost_a = d.worker + 1 < d.workers ? ha : 0;
 
     // Global frames: local (inside this worker's synchronized window) or remote.
-    auto ext_lo = [&](uint32_t w) { return w * f_clip - (w > 0 ? ha : 0); };
-    auto ext_hi = [&](uint32_t w) { return (w + 1) * f_clip + (w + 1 < d.workers ? ha : 0); };
+    auto ext_lo = [&](uint32_t w) { return clip_start(w) - (w > 0 ? ha : 0); };
+    auto ext_hi = [&](uint32_t w) { return clip_start(w + 1) + (w + 1 < d.workers ? ha : 0); };
     g_frame.assign(d.n_global, 0);
     n_remote = 0;
     for (uint32_t j = 0; j < d.n_global; ++j) {
@@ -294,12 +302,13 @@ void Layout::build_exchanges() {
         // Remote global frames: the owner sends each of its members to every worker for
         // which the frame lies outside the synchronized window (T1, clip_parallel.cpp:114-148,
         // minus frames the receiver already holds).
-        auto lo_of = [&](uint32_t w) { return w * f_clip - (w > 0 ? ha : 0); };
-        auto hi_of = [&](uint32_t w) { return (w + 1) * f_clip + (w + 1 < n ? ha : 0); };
+        auto lo_of = [&](uint32_t w) { return clip_start(w) - (w > 0 ? ha : 0); };
+        auto hi_of = [&](uint32_t w) { return clip_start(w + 1) + (w + 1 < n ? ha : 0); };
         std::vector<uint32_t> slot_count(n, 0);
         for (uint32_t j = 0; j < d.n_global; ++j) {
             const uint32_t g = gset[j];
-            const uint32_t owner = g / f_clip;
+            uint32_t owner = 0;
+            while (owner + 1 < n && clip_start(owner + 1) <= g) ++owner;
             for (uint32_t r = 0; r < n; ++r) {
                 if (g >= lo_of(r) && g < hi_of(r)) continue;  // local to r
                 const uint32_t slot = slot_count[r]++;

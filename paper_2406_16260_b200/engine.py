@@ -31,10 +31,10 @@ _ABLATE = {None: _lib.VINF_ABLATE_NONE, "none": _lib.VINF_ABLATE_NONE, "conv": _
 
 def make_desc(frames, workers=1, worker=0, height=32, width=32, channels=320, taps=3, groups=32,
               heads=1, n_local=16, n_global=16, bias=10.0, t_star=800.0, epsilon=1e-5,
-              scale=0.0, blocks=1, dtype=torch.float32) -> EngineDesc:
+              scale=0.0, blocks=1, dtype=torch.float32, uneven=False) -> EngineDesc:
     dt = _lib.VINF_F32 if dtype == torch.float32 else _lib.VINF_BF16
     return EngineDesc(frames, workers, worker, height, width, channels, taps, groups, heads,
-                      n_local, n_global, bias, t_star, epsilon, scale, blocks, dt)
+                      n_local, n_global, bias, t_star, epsilon, scale, blocks, dt, int(uneven))
 
 
 class Layout:
@@ -49,7 +49,9 @@ class Layout:
         n = C.c_uint64()
         _lib.check(self._lib.vinf_layout_workspace_bytes(h, C.byref(n)))
         self.workspace_bytes = n.value
-        self.f_clip = desc.frames // desc.workers
+        st, fc = C.c_uint32(), C.c_uint32()
+        _lib.check(self._lib.vinf_layout_clip(h, C.byref(st), C.byref(fc)))
+        self.start, self.f_clip = st.value, fc.value
         self.dtype = _TORCH_DT[desc.dtype]
 
     def region(self, which: int):

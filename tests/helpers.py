@@ -18,3 +18,10 @@ def normwise(got, want) -> float:
 def to_np(t):
     import torch
     return t.detach().float().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def dev(a, dtype=None):
+    """numpy (or tensor) -> CUDA tensor of the given dtype (fp32 by default)."""
+    import torch
+    t = torch.as_tensor(np.ascontiguousarray(a)) if not isinstance(a, torch.Tensor) else a
+    return t.to("cuda", dtype or torch.float32)
