@@ -191,7 +191,7 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     cuda_check(launch_colpart_to_groups(colpart, uint32_t((rows + 31) / 32), C, L.d.groups,
                                         at<double>(L.off_sums), at<double>(L.off_scratch), s),
                "gn fold");
-    launches += 2;
+    launches += 1;
 }
 
 void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
@@ -200,22 +200,23 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     double* stats = at<double>(L.off_stats);
     const uint32_t G = L.d.groups;
     Span span(this, "gn_apply", s);
-    // mean = sum / n, var = sumsq / n - mean^2 over the whole video (n counts all clips)
-    cuda_check(launch_group_moments(sums, gn_count(), G, stats, s), "gn moments");
+    // mean = sum / n, var = sumsq / n - mean^2 over the whole video (n counts all clips),
+    // formed by the apply kernel itself from the (all-reduced) sums
+    (void)stats;
     auto* u2 = at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E;
     if (f32()) {
         auto* lo = at<__nv_bfloat16>(L.off_u2lo) + uint64_t(L.ha) * L.E;
         cuda_check(launch_group_apply(at(L.off_u1), false, uint64_t(L.f_clip) * L.hw,
-                                      L.d.channels, G, stats, stats + G, B.gamma(), B.beta(),
-                                      L.d.epsilon, at(L.off_u2f), false, u2, lo, s),
+                                      L.d.channels, G, sums, nullptr, B.gamma(), B.beta(),
+                                      L.d.epsilon, at(L.off_u2f), false, u2, lo, s, gn_count()),
                    "gn apply");
     } else {
         cuda_check(launch_group_apply(at(L.off_u1), true, uint64_t(L.f_clip) * L.hw,
-                                      L.d.channels, G, stats, stats + G, B.gamma(), B.beta(),
-                                      L.d.epsilon, u2, true, nullptr, nullptr, s),
+                                      L.d.channels, G, sums, nullptr, B.gamma(), B.beta(),
+                                      L.d.epsilon, u2, true, nullptr, nullptr, s, gn_count()),
                    "gn apply");
     }
-    launches += 2;
+    launches += 1;
 }
 
 void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {

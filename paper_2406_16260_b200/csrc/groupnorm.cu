@@ -194,19 +194,30 @@ __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, ui
                                    const double* __restrict__ vars,
                                    const float* __restrict__ gamma, const float* __restrict__ beta,
                                    float eps, void* __restrict__ y, __nv_bfloat16* __restrict__ hi,
-                                   __nv_bfloat16* __restrict__ lo) {
+                                   __nv_bfloat16* __restrict__ lo, double count) {
     // per-channel (mean, scale, shift) built once per CTA in shared memory: the f64
     // 1/sqrt per group and the f64 gamma product per channel (ops.cpp:152-160) are computed
     // by a few threads instead of every thread redoing them for its 8 channels
     extern __shared__ float tab[];  // [3][C]
-    __shared__ double inv_s[kMaxGroupsApply];
+    __shared__ double inv_s[kMaxGroupsApply], mu_s[kMaxGroupsApply];
     const uint32_t gs = C / groups;
-    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x)
-        inv_s[g] = 1.0 / sqrt(vars[g] + double(eps));  // ops.cpp:152
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
+        double m, v;
+        if (count > 0.0) {  // `means` holds the whole video's (sum, sum of squares)
+            m = means[g] / count;
+            v = means[groups + g] / count - m * m;
+            v = v > 0.0 ? v : 0.0;
+        } else {
+            m = means[g];
+            v = vars[g];
+        }
+        mu_s[g] = m;
+        inv_s[g] = 1.0 / sqrt(v + double(eps));  // ops.cpp:152
+    }
     __syncthreads();
     for (uint32_t ch = threadIdx.x; ch < C; ch += blockDim.x) {
         const uint32_t g = ch / gs;
-        tab[ch] = float(means[g]);
+        tab[ch] = float(mu_s[g]);
         tab[C + ch] = float(double(gamma[ch]) * inv_s[g]);
         tab[2 * C + ch] = beta[ch];
     }
@@ -289,16 +300,27 @@ __global__ void __launch_bounds__(256, 4)
     group_apply_bf16_kernel(const uint4* __restrict__ x, uint64_t rows, uint32_t C, uint32_t groups,
                             const double* __restrict__ means, const double* __restrict__ vars,
                             const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
-                            uint4* __restrict__ y) {
+                            uint4* __restrict__ y, double count) {
     extern __shared__ float tab[];  // [3][C]
-    __shared__ double inv_s[kMaxGroupsApply];
+    __shared__ double inv_s[kMaxGroupsApply], mu_s[kMaxGroupsApply];
     const uint32_t gs = C / groups;
-    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x)
-        inv_s[g] = 1.0 / sqrt(vars[g] + double(eps));  // ops.cpp:152
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
+        double m, v;
+        if (count > 0.0) {  // `means` holds the whole video's (sum, sum of squares)
+            m = means[g] / count;
+            v = means[groups + g] / count - m * m;
+            v = v > 0.0 ? v : 0.0;
+        } else {
+            m = means[g];
+            v = vars[g];
+        }
+        mu_s[g] = m;
+        inv_s[g] = 1.0 / sqrt(v + double(eps));  // ops.cpp:152
+    }
     __syncthreads();
     for (uint32_t ch = threadIdx.x; ch < C; ch += blockDim.x) {
         const uint32_t g = ch / gs;
-        tab[ch] = float(means[g]);
+        tab[ch] = float(mu_s[g]);
         tab[C + ch] = float(double(gamma[ch]) * inv_s[g]);
         tab[2 * C + ch] = beta[ch];
     }
@@ -412,51 +434,69 @@ int launch_group_moment_sums(const void* x, bool bf16, uint64_t rows, uint32_t C
     return int(cudaGetLastError());
 }
 
-// Per-(32-row block, column) partials fp32 [blocks][2][C] -> per-group sums f64 [2][groups],
-// deterministically: (1) each thread owns one of the 2C statistic columns (coalesced) and
-// sums a fixed segment of row blocks into f64 segment partials; (2) one CTA per (statistic,
-// group) folds segments x group columns with a fixed tree.
-constexpr uint32_t kColSegs = 256;
+constexpr uint32_t kColSegs = 256;  // sizes the fold scratch (colpart_scratch_elems)
+
+uint64_t colpart_scratch_elems(uint32_t C) { return uint64_t(kColSegs) * 2 * C; }
+
+// Fold of the conv epilogue's 32-row column partials into per-group (sum, sum of squares)
+// in one launch: CTA (statistic, group, segment) sums its segment of row blocks (fixed
+// per-thread order + fixed tree) into scratch; the last CTA of each (statistic, group)
+// — found with an atomic ticket — adds the segment partials in segment order. The
+// result is therefore independent of CTA scheduling (bitwise reproducible).
+constexpr uint32_t kFoldSegs = 32;
 
 __global__ void __launch_bounds__(128)
-    colpart_segments_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C,
-                            double* __restrict__ seg /* [kColSegs][2C] */) {
-    const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;  // over 2C
-    if (col >= 2 * C) return;
-    const uint32_t per = (blocks + kColSegs - 1) / kColSegs;
-    const uint32_t b0 = blockIdx.y * per, b1 = min(blocks, b0 + per);
+    colpart_fold_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C, uint32_t groups,
+                        double* __restrict__ seg, uint32_t* __restrict__ tickets,
+                        double* __restrict__ sums) {
+    __shared__ double red[128];
+    __shared__ bool last;
+    const uint32_t sg = blockIdx.x / kFoldSegs, sid = blockIdx.x % kFoldSegs;  // sg = which*G + g
+    const uint32_t which = sg / groups, g = sg % groups, gs = C / groups;
+    const uint32_t per = (blocks + kFoldSegs - 1) / kFoldSegs;
+    const uint32_t b0 = min(blocks, sid * per), b1 = min(blocks, b0 + per);
+    const float* base = part + uint64_t(which) * C + uint64_t(g) * gs;
     double a = 0.0;
-#pragma unroll 4
-    for (uint32_t b = b0; b < b1; ++b) a += double(part[uint64_t(b) * 2 * C + col]);
-    seg[uint64_t(blockIdx.y) * 2 * C + col] = a;
-}
-
-__global__ void __launch_bounds__(256)
-    colseg_to_groups_kernel(const double* __restrict__ seg, uint32_t C, uint32_t groups,
-                            double* __restrict__ sums) {
-    __shared__ double red[256];
-    const uint32_t which = blockIdx.x / groups, g = blockIdx.x % groups, gs = C / groups;
-    double a = 0.0;
-    const uint32_t n = kColSegs * gs;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-        a += seg[uint64_t(i / gs) * 2 * C + which * C + g * gs + i % gs];
+    const uint32_t n = (b1 - b0) * gs;
+    for (uint32_t i = threadIdx.x; i < n; i += 128) {
+        const uint32_t b = b0 + i / gs, c = i % gs;
+        a += double(base[uint64_t(b) * 2 * C + c]);
+    }
     red[threadIdx.x] = a;
     __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
+    for (int w = 64; w > 0; w >>= 1) {
         if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) sums[which * groups + g] = red[0];
+    if (threadIdx.x == 0) {
+        seg[uint64_t(sg) * kFoldSegs + sid] = red[0];
+        __threadfence();
+        last = atomicAdd(&tickets[sg], 1u) == kFoldSegs - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x < 32) {  // the segment partials, loaded in parallel, fixed tree
+        static_assert(kFoldSegs == 32, "one partial per lane");
+        __threadfence();
+        double t = reinterpret_cast<const volatile double*>(seg)[uint64_t(sg) * kFoldSegs + threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) {
+            sums[which * groups + g] = t;
+            tickets[sg] = 0;  // ready for the next fold
+        }
+    }
 }
 
-uint64_t colpart_scratch_elems(uint32_t C) { return uint64_t(kColSegs) * 2 * C; }
 
 int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,
                              double* sums, double* scratch, cudaStream_t s) {
     if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
-    dim3 g1((2 * C + 127) / 128, kColSegs);
-    colpart_segments_kernel<<<g1, 128, 0, s>>>(part, blocks, C, scratch);
-    colseg_to_groups_kernel<<<2 * groups, 256, 0, s>>>(scratch, C, groups, sums);
+    // scratch: [2G][kFoldSegs] doubles of segment partials, then 2G uint32 tickets (zero
+    // at rest: the workspace is zeroed at creation and every fold resets its tickets)
+    double* seg = scratch;
+    uint32_t* tickets = reinterpret_cast<uint32_t*>(scratch + uint64_t(2) * groups * kFoldSegs);
+    colpart_fold_kernel<<<2 * groups * kFoldSegs, 128, 0, s>>>(part, blocks, C, groups, seg, tickets,
+                                                              sums);
     return int(cudaGetLastError());
 }
 
@@ -469,7 +509,7 @@ int launch_group_moments(const double* sums, double count, uint32_t groups, doub
 int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
                        const double* means, const double* vars, const float* gamma,
                        const float* beta, float eps, void* y, bool out_bf16, __nv_bfloat16* hi,
-                       __nv_bfloat16* lo, cudaStream_t s) {
+                       __nv_bfloat16* lo, cudaStream_t s, double count) {
     if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
     if (rows == 0) return 0;
     const int vec = (C % 8 == 0) ? 8 : 1;
@@ -486,14 +526,14 @@ int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, u
     if (vec == 8 && in_bf16 && out_bf16 && !split) {
         group_apply_bf16_kernel<<<grid, block, shm, s>>>(static_cast<const uint4*>(x), rows, C, groups,
                                                          means, vars, gamma, beta, eps,
-                                                         static_cast<uint4*>(y));
+                                                         static_cast<uint4*>(y), count);
         return int(cudaGetLastError());
     }
 #define GA(V, IB, OB, SP)                                                                     \
     if (vec == V && in_bf16 == IB && out_bf16 == OB && split == SP) {                         \
         group_apply_kernel<V, IB, OB, SP><<<grid, block, shm, s>>>(x, rows, C, groups, means, \
                                                                  vars, gamma, beta, eps, y,   \
-                                                                 hi, lo);                     \
+                                                                 hi, lo, count);              \
         return int(cudaGetLastError());                                                       \
     }
     GA(8, false, false, false) GA(8, false, false, true) GA(8, true, true, false)

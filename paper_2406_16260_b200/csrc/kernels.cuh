@@ -49,10 +49,12 @@ int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uin
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
                          cudaStream_t s);
 // y = gamma * (x - mean_g) / sqrt(var_g + eps) + beta; optional hi/lo split output.
+// count > 0: means holds the whole video's (sum, sum of squares) and vars is unused;
+// the moments are formed in the kernel (group_moments_kernel's arithmetic).
 int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
                        const double* means, const double* vars, const float* gamma,
                        const float* beta, float eps, void* y, bool out_bf16, __nv_bfloat16* hi,
-                       __nv_bfloat16* lo, cudaStream_t s);
+                       __nv_bfloat16* lo, cudaStream_t s, double count = 0.0);
 
 // ---- attention.cu ----
 constexpr int kMaxTokens = 160;  // n_local + 1 + n_global upper bound

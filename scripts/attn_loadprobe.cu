@@ -6,7 +6,9 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 scripts/attn_loadprobe.cu -o /tmp/probe
 #include <cstdio>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 constexpr int F = 24, HW = 2560, C3 = 1920, NS = 6;
 
@@ -84,6 +86,46 @@ __global__ void __launch_bounds__(256) whole(const uint16_t* q, float* sink) {
     if (acc == 123.f) sink[p] = acc;
 }
 
+
+// D: TMA 3D box loads ({64 ch, 1 position, 24 frames}, SW128) issued by one thread,
+// completion on per-slot mbarriers; one __syncthreads per chunk for slot reuse.
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(256) tma_chunks(const __grid_constant__ CUtensorMap map, float* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NS * 8192);
+    const int tid = threadIdx.x, p = blockIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int i) {
+        if (tid != 0 || i >= 20) return;
+        const int s = i % NS;
+        const int qk = i < 10;
+        const int col = (qk ? i : i - 10) * 64;
+        const uint32_t st = su32(sm + s * 8192);
+        const uint32_t bar = su32(&bars[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(qk ? 6144 : 3072) : "memory");
+        if (qk)
+            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                         ::"r"(st), "l"(&map), "r"(col), "r"(p), "r"(0), "r"(bar) : "memory");
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                     ::"r"(st + 4096), "l"(&map), "r"((qk ? 640 : 1280) + col), "r"(p), "r"(0), "r"(bar) : "memory");
+    };
+    for (int i = 0; i < NS - 1; ++i) issue(i);
+    float acc = 0.f;
+    for (int i = 0; i < 20; ++i) {
+        const uint32_t bar = su32(&bars[i % NS]);
+        const uint32_t par = (i / NS) & 1;
+        asm volatile("{\n.reg .pred P1;\nW: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(bar), "r"(par) : "memory");
+        __syncthreads();
+        issue(i + NS - 1);
+        acc += reinterpret_cast<const float*>(sm + (i % NS) * 8192)[tid];
+    }
+    if (acc == 123.f) sink[p] = acc;
+}
+
 int main() {
     uint16_t* q;
     float* sink;
@@ -100,7 +142,22 @@ int main() {
     cudaFuncSetAttribute(chunks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * 8192);
     cudaFuncSetAttribute(whole, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384);
     const double bytes = double(F) * HW * C3 * 2;
-    for (int v = 0; v < 3; ++v) {
+    CUtensorMap map;
+    {
+        PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &qr);
+        cuuint64_t gdim[3] = {C3, HW, F};
+        cuuint64_t gstr[2] = {C3 * 2ull, uint64_t(HW) * C3 * 2};
+        cuuint32_t box[3] = {64, 1, 24};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)q, gdim, gstr, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) printf("tensor map encode failed %d\n", int(r));
+    }
+    cudaFuncSetAttribute(tma_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * 8192 + 1024);
+    for (int v = 0; v < 4; ++v) {
         float best = 1e9;
         for (int it = 0; it < 10; ++it) {
             cudaMemset(flush, it, 512 << 20);
@@ -108,13 +165,14 @@ int main() {
             if (v == 0) chunks<false><<<HW, 256, NS * 8192>>>(q, sink);
             if (v == 1) chunks<true><<<HW, 256, NS * 8192>>>(q, sink);
             if (v == 2) whole<<<HW, 256, 4 * 16384>>>(q, sink);
+            if (v == 3) tma_chunks<<<HW, 256, NS * 8192 + 1024>>>(map, sink);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms;
             cudaEventElapsedTime(&ms, a, b);
             if (ms < best) best = ms;
         }
-        printf("%s: %.1f us  %.0f GB/s  (%s)\n", v == 0 ? "A frame-major chunks" : v == 1 ? "B position-major chunks" : "C position-major whole",
+        printf("%s: %.1f us  %.0f GB/s  (%s)\n", v == 0 ? "A frame-major chunks" : v == 1 ? "B position-major chunks" : v == 2 ? "C position-major whole" : "D frame-major TMA boxes",
                best * 1000, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
