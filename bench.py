@@ -258,7 +258,9 @@ def run_ours(args):
     barrier()
 
     # ---- timed region: K device-resident steps (value) ---------------------------
-    eng.profile(True)
+    # The engine's normal path (a single worker replays its CUDA graph; workers > 1 run
+    # the staged loop with the exchanges). Per-kernel CUDA events are NOT recorded here:
+    # they serialise the stream and cost ~13% of the step (scripts/graph_vs_profile.py).
     l0 = eng.launches()
     clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local)
     with clocks:
@@ -271,8 +273,6 @@ def run_ours(args):
         t1.record(stream)
         barrier()
     launches = (eng.launches() - l0) // args.steps
-    stats = eng.kernel_stats()
-    eng.profile(False)
     ms = t0.elapsed_time(t1)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -280,6 +280,22 @@ def run_ours(args):
     ms_max = float(ms_t.item())
     ms_per_step = ms_max / args.steps
     value = n * fc * args.steps / (ms_max / 1000.0)
+
+    # ---- per-kernel region: the same K steps with CUDA events around every kernel group
+    # (vinf_engine_profile), for the kernel breakdown and the dominant kernel's roofline
+    eng.profile(True)
+    eng.kernel_stats()
+    barrier()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        step()
+    p1.record(stream)
+    barrier()
+    stats = eng.kernel_stats()
+    eng.profile(False)
+    profiled_ms_per_step = p0.elapsed_time(p1) / args.steps
 
     # ---- e2e: host buffers in, host buffers out, through the public engine API ----
     # Two engines alternate steps; the upload of step j+1 (H2D stream) and the download of
@@ -413,6 +429,9 @@ def run_ours(args):
                 "dtype": args.dtype, "data": "synthetic (tensor_from_seed / build_model seeds 0/1)",
                 "config": workload_config(n, args.dtype),
                 "roofline": roof, "block_roofline": block_roof, "kernels": per_kernel,
+                "kernel_timing": {"region": "second run of the same K steps with CUDA events around "
+                                            "every kernel group (the headline region runs without "
+                                            "them)", "profiled_ms_per_step": profiled_ms_per_step},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": clip_bytes,
                         "d2h_bytes_per_step": clip_bytes, "steps": e_steps,
