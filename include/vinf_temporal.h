@@ -246,7 +246,11 @@ enum {
     VINF_STAGE_STUB = 0,
     VINF_STAGE_CONV = 1,
     VINF_STAGE_GN_APPLY = 2,
-    VINF_STAGE_ATTENTION = 3
+    VINF_STAGE_ATTENTION = 3,
+    /* Optional split of ATTENTION: the own frames' Q/K/V projection, which needs no
+     * exchanged frame, so it can run while the attention exchange is in flight; the
+     * following ATTENTION stage then skips it. */
+    VINF_STAGE_QKV = 4
 };
 int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void* stream);
 /* All blocks, all stages (single worker: no exchanges needed). */

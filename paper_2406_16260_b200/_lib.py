@@ -16,7 +16,7 @@ VINF_OK, VINF_ERR, VINF_ERR_CONFIG, VINF_ERR_TRANSPORT, VINF_ERR_IO, VINF_ERR_IN
 VINF_F32, VINF_BF16 = 0, 1
 VINF_BUF_X, VINF_BUF_Y, VINF_BUF_CONV_IN, VINF_BUF_ATTN_IN, VINF_BUF_GN_SUMS = range(5)
 VINF_XCHG_CONV, VINF_XCHG_ATTN = 0, 1
-VINF_STAGE_STUB, VINF_STAGE_CONV, VINF_STAGE_GN_APPLY, VINF_STAGE_ATTENTION = range(4)
+VINF_STAGE_STUB, VINF_STAGE_CONV, VINF_STAGE_GN_APPLY, VINF_STAGE_ATTENTION, VINF_STAGE_QKV = range(5)
 VINF_ABLATE_NONE, VINF_ABLATE_CONV, VINF_ABLATE_GROUPNORM, VINF_ABLATE_ATTENTION = range(4)
 
 

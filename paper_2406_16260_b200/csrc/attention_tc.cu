@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(kTcThreads, LeanLay<NTL, NS>::min_blocks)
     attention_core_lean_kernel(const __nv_bfloat16* __restrict__ qkv, uint32_t HW, uint32_t C,
                                uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt,
                                float scale, float bias, __nv_bfloat16* __restrict__ ctx) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
     using LL = LeanLay<NTL, NS>;
     constexpr uint32_t RP = LL::RP;
     constexpr int SP = int(LL::SP);
@@ -574,10 +576,9 @@ int launch_lean(const void* qkv, uint32_t HW, uint32_t C, uint32_t heads, uint32
         attr = true;
     }
     dim3 grid(HW, (nq + kQBlock - 1) / kQBlock);
-    attention_core_lean_kernel<NTL, NS><<<grid, kTcThreads, LeanLay<NTL, NS>::total, s>>>(
-        static_cast<const __nv_bfloat16*>(qkv), HW, C, heads, nq, q_frame0, tt, scale, bias,
-        static_cast<__nv_bfloat16*>(ctx));
-    return int(cudaGetLastError());
+    return int(launch_pdl(attention_core_lean_kernel<NTL, NS>, grid, dim3(kTcThreads),
+                          LeanLay<NTL, NS>::total, s, static_cast<const __nv_bfloat16*>(qkv), HW, C,
+                          heads, nq, q_frame0, tt, scale, bias, static_cast<__nv_bfloat16*>(ctx)));
 }
 
 }  // namespace

@@ -11,6 +11,11 @@
 
 namespace vinf {
 
+bool pdl_enabled() {
+    static const bool on = getenv("VINF_NO_PDL") == nullptr;
+    return on;
+}
+
 namespace {
 
 __device__ __forceinline__ float unit_from_state(uint64_t z) {
@@ -59,6 +64,8 @@ __global__ void __launch_bounds__(256)
     stub_bf16_kernel(const uint4* __restrict__ in, uint64_t rows, uint32_t C,
                      const float* __restrict__ a, const float* __restrict__ c,
                      uint4* __restrict__ out) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
     constexpr int UNR = 4;
     const uint32_t CC = C / 8, R = blockDim.x / CC;
     const uint32_t cc = threadIdx.x % CC, rl = threadIdx.x / CC;
@@ -167,6 +174,8 @@ __global__ void cast_kernel(const void* __restrict__ in, int in_bf16, void* __re
 template <bool BF16>
 __global__ void euler_kernel(void* __restrict__ x, const void* __restrict__ eps, uint64_t n,
                              double lambda) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         if (BF16) {
@@ -186,10 +195,8 @@ __global__ void euler_kernel(void* __restrict__ x, const void* __restrict__ eps,
 int launch_euler(void* x, const void* eps, bool bf16, uint64_t n, double lambda, cudaStream_t s) {
     if (n == 0) return 0;
     if (bf16)
-        euler_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(x, eps, n, lambda);
-    else
-        euler_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(x, eps, n, lambda);
-    return int(cudaGetLastError());
+        return int(launch_pdl(euler_kernel<true>, dim3(grid_for(n, 256)), dim3(256), 0, s, x, eps, n, lambda));
+    return int(launch_pdl(euler_kernel<false>, dim3(grid_for(n, 256)), dim3(256), 0, s, x, eps, n, lambda));
 }
 
 int grid_for(uint64_t work_items, int block) {
@@ -220,9 +227,8 @@ int launch_stub(const void* in, bool in_bf16, uint64_t n, uint32_t C, const floa
         uint64_t grid = (rows + R - 1) / R;
         const uint64_t cap = uint64_t(num_sms()) * 4;
         if (grid > cap) grid = cap;
-        stub_bf16_kernel<<<unsigned(grid), CC * R, 0, s>>>(static_cast<const uint4*>(in), rows, C,
-                                                           a, c, static_cast<uint4*>(out));
-        return int(cudaGetLastError());
+        return int(launch_pdl(stub_bf16_kernel, dim3(unsigned(grid)), dim3(CC * R), 0, s,
+                              static_cast<const uint4*>(in), rows, C, a, c, static_cast<uint4*>(out)));
     }
     const uint64_t nv = n / 4;
     const int g = grid_for(nv, 256);

@@ -133,6 +133,9 @@ struct vinf_engine {
     void stage_conv(uint32_t b, cudaStream_t s);
     void stage_gn_apply(uint32_t b, cudaStream_t s);
     void stage_attention(uint32_t b, double t, cudaStream_t s);
+    void stage_qkv(uint32_t b, cudaStream_t s);
+    void project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, bool with_q, cudaStream_t s);
+    int qkv_ready = -1;  // block whose own-frame Q/K/V projection has already run
 };
 
 void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
@@ -219,10 +222,12 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     launches += 1;
 }
 
-void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
+// Q/K/V (with_q) or K/V rows of `nframes` attention-buffer frames from frame0 on.
+void vinf_engine::project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, bool with_q,
+                              cudaStream_t s) {
+    if (!nframes) return;
     const EngineBlock& B = blocks.at(b);
     const uint32_t C = L.d.channels;
-    if (ablate == VINF_ABLATE_ATTENTION) zero_recv_slots(L.xattn, s);
     const uint64_t hw = L.hw;
     Operand A;
     A.hi = at<__nv_bfloat16>(L.off_u2);
@@ -231,19 +236,36 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     A.cols = C;
     A.ld = C;
     const size_t qes = f32() ? 4 : 2;
+    Epilogue ep;
+    ep.out = at(L.off_qkv) + (uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C)) * qes;
+    ep.out_ld = 3 * C;
+    ep.out_bf16 = !f32();
+    Span span(this, with_q ? "qkv_gemm" : "kv_gemm_ctx", s);
+    gemm(A, {int64_t(frame0) * int64_t(hw)}, B.wqkv, {with_q ? 0 : int64_t(C)},
+         int64_t(nframes) * int64_t(hw), with_q ? 3 * C : 2 * C, ep, f32(), s);
+    ++launches;
+}
+
+// The own frames' Q/K/V projection only: it reads just this clip's normalised frames, so
+// a driver may run it while the attention exchange is in flight (on another stream).
+void vinf_engine::stage_qkv(uint32_t b, cudaStream_t s) {
+    project_qkv(b, L.ha, L.f_clip, true, s);
+    qkv_ready = int(b);
+}
+
+void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
+    const EngineBlock& B = blocks.at(b);
+    const uint32_t C = L.d.channels;
+    if (ablate == VINF_ABLATE_ATTENTION) zero_recv_slots(L.xattn, s);
+    const uint64_t hw = L.hw;
     uint8_t* qkv = at(L.off_qkv);
     auto project = [&](uint32_t frame0, uint32_t nframes, bool with_q) {
-        if (!nframes) return;
-        Epilogue ep;
-        ep.out = qkv + (uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C)) * qes;
-        ep.out_ld = 3 * C;
-        ep.out_bf16 = !f32();
-        Span span(this, with_q ? "qkv_gemm" : "kv_gemm_ctx", s);
-        gemm(A, {int64_t(frame0) * int64_t(hw)}, B.wqkv, {with_q ? 0 : int64_t(C)},
-             int64_t(nframes) * int64_t(hw), with_q ? 3 * C : 2 * C, ep, f32(), s);
-        ++launches;
+        project_qkv(b, frame0, nframes, with_q, s);
     };
-    project(L.ha, L.f_clip, true);                           // own frames: Q, K, V
+    // own frames: Q, K, V (unless the QKV stage already ran for this block, overlapping
+    // the attention exchange)
+    if (qkv_ready != int(b)) project(L.ha, L.f_clip, true);
+    qkv_ready = -1;
     project(L.ha - L.npre_a, L.npre_a, false);               // pre halo: K, V
     project(L.ha + L.f_clip, L.npost_a, false);              // post halo: K, V
     const bool abl = ablate == VINF_ABLATE_ATTENTION;
@@ -412,6 +434,7 @@ int vinf_engine_stage(vinf_engine* e, uint32_t block, int stage, double t, void*
             case VINF_STAGE_CONV: e->stage_conv(block, s); break;
             case VINF_STAGE_GN_APPLY: e->stage_gn_apply(block, s); break;
             case VINF_STAGE_ATTENTION: e->stage_attention(block, t, s); break;
+            case VINF_STAGE_QKV: e->stage_qkv(block, s); break;
             default: range_error("unknown stage");
         }
     });

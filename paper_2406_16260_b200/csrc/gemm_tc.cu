@@ -353,6 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     dev::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // the prologue above overlaps the previous kernel's tail (programmatic launch)
+    dev::pdl_wait();
+    dev::pdl_trigger();
 
     if (warp == 0) {
         // ===== TMA producer =====
@@ -696,8 +699,8 @@ int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     }
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
     const int grid = std::max(1, std::min(tiles, g_num_sms));
-    gemm_tc_kernel<BN, OBF, RES, ST, TMAO><<<grid, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
-    return int(cudaGetLastError());
+    return int(launch_pdl(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>, dim3(grid), dim3(kThreads),
+                          Cfg::kSmemBytes, stream, maps, p));
 }
 
 template <int BN>

@@ -195,6 +195,8 @@ __global__ void group_apply_kernel(const void* __restrict__ x, uint64_t rows, ui
                                    const float* __restrict__ gamma, const float* __restrict__ beta,
                                    float eps, void* __restrict__ y, __nv_bfloat16* __restrict__ hi,
                                    __nv_bfloat16* __restrict__ lo, double count) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
     // per-channel (mean, scale, shift) built once per CTA in shared memory: the f64
     // 1/sqrt per group and the f64 gamma product per channel (ops.cpp:152-160) are computed
     // by a few threads instead of every thread redoing them for its 8 channels
@@ -301,6 +303,8 @@ __global__ void __launch_bounds__(256, 4)
                             const double* __restrict__ means, const double* __restrict__ vars,
                             const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
                             uint4* __restrict__ y, double count) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
     extern __shared__ float tab[];  // [3][C]
     __shared__ double inv_s[kMaxGroupsApply], mu_s[kMaxGroupsApply];
     const uint32_t gs = C / groups;
@@ -449,6 +453,8 @@ __global__ void __launch_bounds__(128)
     colpart_fold_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C, uint32_t groups,
                         double* __restrict__ seg, uint32_t* __restrict__ tickets,
                         double* __restrict__ sums) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
     __shared__ double red[128];
     __shared__ bool last;
     const uint32_t sg = blockIdx.x / kFoldSegs, sid = blockIdx.x % kFoldSegs;  // sg = which*G + g
@@ -495,9 +501,8 @@ int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uin
     // at rest: the workspace is zeroed at creation and every fold resets its tickets)
     double* seg = scratch;
     uint32_t* tickets = reinterpret_cast<uint32_t*>(scratch + uint64_t(2) * groups * kFoldSegs);
-    colpart_fold_kernel<<<2 * groups * kFoldSegs, 128, 0, s>>>(part, blocks, C, groups, seg, tickets,
-                                                              sums);
-    return int(cudaGetLastError());
+    return int(launch_pdl(colpart_fold_kernel, dim3(2 * groups * kFoldSegs), dim3(128), 0, s, part, blocks,
+                          C, groups, seg, tickets, sums));
 }
 
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
@@ -524,17 +529,15 @@ int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, u
     const size_t shm = sizeof(float) * 3 * C;
     if (shm > 48 * 1024) return int(cudaErrorInvalidValue);
     if (vec == 8 && in_bf16 && out_bf16 && !split) {
-        group_apply_bf16_kernel<<<grid, block, shm, s>>>(static_cast<const uint4*>(x), rows, C, groups,
-                                                         means, vars, gamma, beta, eps,
-                                                         static_cast<uint4*>(y), count);
-        return int(cudaGetLastError());
+        return int(launch_pdl(group_apply_bf16_kernel, dim3(grid), dim3(block), shm, s,
+                              static_cast<const uint4*>(x), rows, C, groups, means, vars, gamma, beta,
+                              eps, static_cast<uint4*>(y), count));
     }
 #define GA(V, IB, OB, SP)                                                                     \
     if (vec == V && in_bf16 == IB && out_bf16 == OB && split == SP) {                         \
-        group_apply_kernel<V, IB, OB, SP><<<grid, block, shm, s>>>(x, rows, C, groups, means, \
-                                                                 vars, gamma, beta, eps, y,   \
-                                                                 hi, lo, count);              \
-        return int(cudaGetLastError());                                                       \
+        return int(launch_pdl(group_apply_kernel<V, IB, OB, SP>, dim3(grid), dim3(block), shm, s, \
+                              x, rows, C, groups, means, vars, gamma, beta, eps, y, hi, lo,   \
+                              count));                                                        \
     }
     GA(8, false, false, false) GA(8, false, false, true) GA(8, true, true, false)
     GA(8, true, true, true) GA(8, false, true, false) GA(8, true, false, false)

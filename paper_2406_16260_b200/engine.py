@@ -223,9 +223,30 @@ def forward(t: float, engines: list[ClipEngine], group=None, ablate: str | None 
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_GN_APPLY, t)
         if ablate != "attention":
-            group.exchange(engines, _lib.VINF_XCHG_ATTN)
+            # The attention exchange (halo + remote global frames) runs on a side stream
+            # while the compute stream projects the clip's own frames to Q/K/V, which needs
+            # none of the exchanged frames; the halo/remote K/V and the core wait for it.
+            dev = engines[0].device
+            cur = torch.cuda.current_stream(dev)
+            comm = _comm_stream(dev)
+            comm.wait_stream(cur)  # U2 (the normalised clip) is complete before it is sent
+            with torch.cuda.stream(comm):
+                group.exchange(engines, _lib.VINF_XCHG_ATTN)
+            for e in engines:
+                e.stage(b, _lib.VINF_STAGE_QKV, t)
+            cur.wait_stream(comm)
         for e in engines:
             e.stage(b, _lib.VINF_STAGE_ATTENTION, t)
+
+
+_COMM_STREAMS: dict = {}
+
+
+def _comm_stream(device) -> "torch.cuda.Stream":
+    s = _COMM_STREAMS.get(device)
+    if s is None:
+        s = _COMM_STREAMS[device] = torch.cuda.Stream(device)
+    return s
 
 
 def timestep_grid(steps: int) -> list[float]:
