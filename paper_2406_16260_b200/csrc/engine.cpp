@@ -136,6 +136,7 @@ struct vinf_engine {
     void stage_qkv(uint32_t b, cudaStream_t s);
     void project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, bool with_q, cudaStream_t s);
     int qkv_ready = -1;  // block whose own-frame Q/K/V projection has already run
+    bool fused = false;  // Q/K/V projection + attention core in one kernel (attn_fused.cu)
 };
 
 void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
@@ -249,39 +250,44 @@ void vinf_engine::project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, boo
 // The own frames' Q/K/V projection only: it reads just this clip's normalised frames, so
 // a driver may run it while the attention exchange is in flight (on another stream).
 void vinf_engine::stage_qkv(uint32_t b, cudaStream_t s) {
-    project_qkv(b, L.ha, L.f_clip, true, s);
+    if (!fused) project_qkv(b, L.ha, L.f_clip, true, s);  // fused: the attention kernel projects
     qkv_ready = int(b);
 }
 
 void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     const EngineBlock& B = blocks.at(b);
     const uint32_t C = L.d.channels;
-    if (ablate == VINF_ABLATE_ATTENTION) zero_recv_slots(L.xattn, s);
-    const uint64_t hw = L.hw;
-    uint8_t* qkv = at(L.off_qkv);
-    auto project = [&](uint32_t frame0, uint32_t nframes, bool with_q) {
-        project_qkv(b, frame0, nframes, with_q, s);
-    };
-    // own frames: Q, K, V (unless the QKV stage already ran for this block, overlapping
-    // the attention exchange)
-    if (qkv_ready != int(b)) project(L.ha, L.f_clip, true);
-    qkv_ready = -1;
-    project(L.ha - L.npre_a, L.npre_a, false);               // pre halo: K, V
-    project(L.ha + L.f_clip, L.npost_a, false);              // post halo: K, V
     const bool abl = ablate == VINF_ABLATE_ATTENTION;
-    // remote global frames (+ the zero null frame the ablated tables point at): K, V
-    project(2 * L.ha + L.f_clip, L.n_remote + (abl ? 1 : 0), false);
-    const bool bias_global = t > L.d.t_star;                  // ops.cpp:298
+    if (abl) zero_recv_slots(L.xattn, s);
+    const uint64_t hw = L.hw;
+    const bool bias_global = t > L.d.t_star;  // ops.cpp:298
     auto* ctx = at<__nv_bfloat16>(L.off_ctx);
     auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
-    {
-    Span span(this, "attn_core", s);
-    cuda_check(launch_attention_core(qkv, uint64_t(L.af) * hw, !f32(), L.hw, C, L.d.heads, L.f_clip, L.ha,
-                                     tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale, L.d.bias, ctx, !f32(),
-                                     f32() ? ctx : nullptr, ctxlo, s),
-               "attention core");
+    const bool own_done = qkv_ready == int(b);
+    qkv_ready = -1;
+    if (fused && !abl) {
+        // Q/K/V projection and the attention core in one kernel: Q/K/V never reach HBM
+        Span span(this, "qkv_attn_fused", s);
+        cuda_check(launch_qkv_attention_fused(at(L.off_u2), L.af, L.ha, L.hw, C, L.f_clip, B.wqkv.hi,
+                                              tt[bias_global ? 1 : 0], L.scale, L.d.bias, ctx, s),
+                   "fused attention");
+        ++launches;
+    } else {
+        uint8_t* qkv = at(L.off_qkv);
+        // own frames: Q, K, V (unless the QKV stage already ran for this block, overlapping
+        // the attention exchange)
+        if (!own_done) project_qkv(b, L.ha, L.f_clip, true, s);
+        project_qkv(b, L.ha - L.npre_a, L.npre_a, false, s);  // pre halo: K, V
+        project_qkv(b, L.ha + L.f_clip, L.npost_a, false, s);  // post halo: K, V
+        // remote global frames (+ the zero null frame the ablated tables point at): K, V
+        project_qkv(b, 2 * L.ha + L.f_clip, L.n_remote + (abl ? 1 : 0), false, s);
+        Span span(this, "attn_core", s);
+        cuda_check(launch_attention_core(qkv, uint64_t(L.af) * hw, !f32(), L.hw, C, L.d.heads, L.f_clip,
+                                         L.ha, tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale,
+                                         L.d.bias, ctx, !f32(), f32() ? ctx : nullptr, ctxlo, s),
+                   "attention core");
+        ++launches;
     }
-    ++launches;
     Operand O;
     O.hi = ctx;
     O.lo = ctxlo;
@@ -325,6 +331,15 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
             cuda_check(cudaMemcpyAsync(p, blob[b].data(), blob[b].size(), cudaMemcpyHostToDevice, s),
                        "tokens");
             e->tt[b] = L.tok[b].view(p);
+        }
+        // fused projection + attention: every query block's K/V tokens are exactly the
+        // clip's own frames in order (the single-worker layout), bf16, one head
+        e->fused = !L.f32 && fused_attention_supported(L.d.channels, L.d.heads, L.f_clip, L.hw);
+        for (int b = 0; b < 2 && e->fused; ++b) {
+            const HostTokens& T = L.tok[b];
+            e->fused = T.nqb == 1 && T.kv_ok && T.kv_count[0] == L.f_clip;
+            for (uint32_t r = 0; e->fused && r < L.f_clip; ++r)
+                e->fused = T.kv_frames[r] == L.ha + r;
         }
         const uint32_t C = L.d.channels;
         e->blocks.resize(L.d.blocks);

@@ -469,53 +469,6 @@ struct PairCfg {
         kStages * kStageBytes + 1024 /*align*/ + 1024 /*bars*/ + kStgBytes;
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                     : "memory");
-}
-// shared::cluster address of this CTA's shared variable `a` as seen in CTA `rank`
-__device__ __forceinline__ uint32_t peer_addr(uint32_t a, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap, uint32_t bar_leader,
-                                                 int32_t c0, int32_t c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(bar_leader)
-        : "memory");
-}
-__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                               uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// arrive on the barrier at this smem offset in both CTAs once the issued MMAs complete
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(dev::smem_u32(bar)),
-        "h"(uint16_t(3))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
-}
-
 template <int BN, bool OBF, bool RES, bool ST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
@@ -534,7 +487,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = dev::cluster_rank();
     const bool leader = rank == 0;
 
     const int n_tiles = (p.N + BN - 1) / BN;
@@ -569,7 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     dev::tc_fence_before();
-    cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated in both
+    dev::cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated in both
     dev::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
@@ -585,13 +538,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint32_t s = it % S;
                     const uint32_t ph = (it / S) & 1;
                     dev::mbar_wait(&empty[s], ph ^ 1);
-                    const uint32_t bar = peer_addr(dev::smem_u32(&full[s]), 0);
+                    const uint32_t bar = dev::peer_addr(dev::smem_u32(&full[s]), 0);
                     if (leader) dev::mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
                     const GemmSeg& sg = p.seg[k / kb_per_seg];
                     const int kk = (k % kb_per_seg) * kBK;
-                    tma_load_2d_pair(dev::smem_u32(smem_a + s * kABytes), &maps.a[sg.a_map], bar, kk,
+                    dev::tma_load_2d_pair(dev::smem_u32(smem_a + s * kABytes), &maps.a[sg.a_map], bar, kk,
                                      m0 + sg.a_row);
-                    tma_load_2d_pair(dev::smem_u32(smem_b + s * Cfg::kBBytes), &maps.b[sg.b_map], bar,
+                    dev::tma_load_2d_pair(dev::smem_u32(smem_b + s * Cfg::kBBytes), &maps.b[sg.b_map], bar,
                                      kk, n0 + sg.b_row);
                 }
             }
@@ -618,10 +571,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             dev::sw128_kmajor_desc(dev::smem_u32(smem_b + s * Cfg::kBBytes));
 #pragma unroll
                         for (int kk = 0; kk < kBK / 16; ++kk)
-                            umma_bf16_pair(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
+                            dev::umma_bf16_pair(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
                                            (k > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit_pair(&empty[s]);
-                        if (k == k_iters - 1) umma_commit_pair(&tfull[acc]);
+                        dev::umma_commit_pair(&empty[s]);
+                        if (k == k_iters - 1) dev::umma_commit_pair(&tfull[acc]);
                     }
                     __syncwarp();
                 }
@@ -651,12 +604,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                             half, rr);
             dev::tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_remote(peer_addr(dev::smem_u32(&tempty[acc]), 0));
+            if (lane == 0) dev::mbar_arrive_remote(dev::peer_addr(dev::smem_u32(&tempty[acc]), 0));
         }
     }
 
     dev::tc_fence_before();
-    cluster_sync_all();
+    dev::cluster_sync_all();
     dev::tc_fence_after();
     if (warp == 2)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),

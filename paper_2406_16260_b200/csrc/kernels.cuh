@@ -84,6 +84,13 @@ int launch_attention_core_tc(const void* qkv, uint64_t qkv_rows, uint32_t HW, ui
                              cudaStream_t s);
 
 // qkv_rows: rows of the QKV buffer (bounds of the TMA map the bf16 pipeline kernel reads it by)
+// attn_fused.cu: Q/K/V projection + attention core in one kernel for clips whose K/V
+// tokens are all own frames (the single-worker layout), bf16 mode.
+bool fused_attention_supported(uint32_t C, uint32_t heads, uint32_t F, uint32_t HW);
+int launch_qkv_attention_fused(const void* u2, uint32_t af, uint32_t f_own0, uint32_t HW, uint32_t C,
+                               uint32_t F, const void* wqkv, TokenTable tt, float scale, float bias,
+                               void* ctx, cudaStream_t s);
+
 int launch_attention_core(const void* qkv, uint64_t qkv_rows, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
                           uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale, float bias,
                           void* ctx, bool ctx_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,

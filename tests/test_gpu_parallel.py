@@ -282,3 +282,31 @@ def test_engine_matches_reference_run_path(mods, reference):
     en.forward(1000.0, [e])
     got = to_np(x) - to_np(e.y)
     assert normwise(got, x0) <= TOL_F32
+
+
+@pytest.mark.gpu
+def test_fused_projection_attention_bitwise(mods):
+    # the opt-in fused Q/K/V + attention kernel (attn_fused.cu) reproduces the unfused path
+    # bit for bit (same projection accumulation, same S k-order, same softmax)
+    import subprocess, sys, os
+    code = r'''
+import sys, torch, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2406_16260_b200 import engine as en, ops
+d = en.make_desc(24, 1, 0, 4, 8, 128, 3, 8, 1, 16, 16, 10.0, 800.0, 1e-5, 0.0, 1, torch.bfloat16)
+e = en.ClipEngine(en.Layout(d)); e.init_weights(1)
+e.x.copy_(ops.tensor_from_seed((24, 4, 8, 128), 0, dtype=torch.bfloat16, device="cuda"))
+out = []
+for t in (900.0, 700.0):
+    e.forward_single(t); torch.cuda.synchronize(); out.append(e.y.view(torch.int16).cpu().numpy())
+np.save(sys.argv[2], np.stack(out))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for env in ({"VINF_FUSED_ATTN": "1"}, {}):
+        path = f"/tmp/fused_{len(res)}.npy"
+        r = subprocess.run([sys.executable, "-c", code, root, path], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.load(path))
+    assert np.array_equal(res[0], res[1])
