@@ -446,51 +446,55 @@ __global__ void __launch_bounds__(kTcThreads, LeanLay<NTL, NS>::min_blocks)
             }
         }
         __syncthreads();
-        // ---------------- token softmax -> P (in place over S) ----------------
+        // ---------------- softmax over the token lists, per column -> P (in place) ----------
+        // The reference's token list (window, then globals, duplicates kept; ops.cpp:209-241)
+        // in column form: column c carries the window token iff wlo <= c <= whi and
+        // gmult[c] global tokens; p_c = [window] e^(l_w - m) + sum over its global tokens
+        // e^(l_g - m). Each lane owns columns lane and lane + 32: no token-list walk, no
+        // shared-memory atomics.
         for (uint32_t a = warp; a < uint32_t(kQBlock); a += kTcWarps) {
             float* row = sp + a * SP;
+            float pv[2] = {0.f, 0.f};
+            float zi = 0.f;
             if (a < nqh) {
                 const uint32_t qa = a0 + a;
-                const int n = tt.count[qa];
-                const uint8_t* cols = tt.col + size_t(qa) * kMaxTokens;
-                const uint8_t* flg = tt.biased + size_t(qa) * kMaxTokens;
-                float lg[(kMaxTokens + 31) / 32];
-                int cl[(kMaxTokens + 31) / 32];
+                const int lo = tt.wlo[qa], hi = tt.whi[qa];
+                const uint8_t* gm = tt.gmult + size_t(qb) * kKvMax;
+                const float bw = tt.wflag ? bias : 0.f, bg = tt.gflag ? bias : 0.f;
+                float sv[2];
+                bool inw[2];
+                int ng[2];
                 float m = -INFINITY;
-                const int nk = (n + 31) >> 5;
 #pragma unroll
-                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
-                    const int i = lane + 32 * k;
-                    cl[k] = 0;
-                    lg[k] = -INFINITY;
-                    if (k < nk && i < n) {
-                        cl[k] = int(cols[i]);
-                        lg[k] = scale * row[cl[k]] + (flg[i] ? bias : 0.f);
-                    }
-                    m = fmaxf(m, lg[k]);
+                for (int k = 0; k < 2; ++k) {
+                    const int c = lane + 32 * k;
+                    const bool ok = c < int(R);
+                    sv[k] = ok ? scale * row[c] : 0.f;
+                    inw[k] = ok && c >= lo && c <= hi;
+                    ng[k] = ok ? gm[c] : 0;
+                    if (inw[k]) m = fmaxf(m, sv[k] + bw);
+                    if (ng[k]) m = fmaxf(m, sv[k] + bg);
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
                 float z = 0.f;
 #pragma unroll
-                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
-                    lg[k] = (k < nk && lane + 32 * k < n) ? expf(lg[k] - m) : 0.f;
-                    z += lg[k];
+                for (int k = 0; k < 2; ++k) {
+                    float p = inw[k] ? expf(sv[k] + bw - m) : 0.f;
+                    if (ng[k]) {
+                        const float e = expf(sv[k] + bg - m);
+                        for (int t = 0; t < ng[k]; ++t) p += e;
+                    }
+                    pv[k] = p;
+                    z += p;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-                __syncwarp();
-                for (int c = lane; c < SP; c += 32) row[c] = 0.f;
-                __syncwarp();
-                // duplicate tokens: at most two commutative additions per column
-#pragma unroll
-                for (int k = 0; k < (kMaxTokens + 31) / 32; ++k)
-                    if (k < nk && lane + 32 * k < n) atomicAdd(&row[cl[k]], lg[k]);
-                if (lane == 0) zinv[a] = 1.0f / z;
-            } else {
-                for (int c = lane; c < SP; c += 32) row[c] = 0.f;
-                if (lane == 0) zinv[a] = 0.f;
+                zi = 1.0f / z;
             }
+            __syncwarp();
+            for (int c = lane; c < SP; c += 32) row[c] = c < 64 ? pv[c >> 5] : 0.f;
+            if (lane == 0) zinv[a] = zi;
         }
         __syncthreads();
 #pragma unroll

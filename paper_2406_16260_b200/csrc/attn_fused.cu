@@ -312,47 +312,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFuThreads, 1)
                     for (uint32_t rr = uint32_t(w); rr < P * 32; rr += kFuWorkers) {
                         const uint32_t pos = rr >> 5, a_ = rr & 31;
                         float* row = sp + rr * kFuSP;
+                        // per-column token softmax, as in the lean kernel (same bits)
+                        float pv[2] = {0.f, 0.f};
+                        float zi = 0.f;
                         if (a_ < F) {
-                            const int n = tt.count[a_];
-                            const uint8_t* cols = tt.col + size_t(a_) * kMaxTokens;
-                            const uint8_t* flg = tt.biased + size_t(a_) * kMaxTokens;
-                            float lg[(kMaxTokens + 31) / 32];
-                            int cl[(kMaxTokens + 31) / 32];
+                            const int lo = tt.wlo[a_], hi = tt.whi[a_];
+                            const float bw = tt.wflag ? bias : 0.f, bg = tt.gflag ? bias : 0.f;
+                            float sv[2];
+                            bool inw[2];
+                            int ng[2];
                             float m = -INFINITY;
-                            const int nk = (n + 31) >> 5;
 #pragma unroll
-                            for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
-                                const int i = lane + 32 * k;
-                                cl[k] = 0;
-                                lg[k] = -INFINITY;
-                                if (k < nk && i < n) {
-                                    cl[k] = int(cols[i]);
-                                    lg[k] = scale * row[cl[k]] + (flg[i] ? bias : 0.f);
-                                }
-                                m = fmaxf(m, lg[k]);
+                            for (int k = 0; k < 2; ++k) {
+                                const int c = lane + 32 * k;
+                                const bool ok = c < int(F);
+                                sv[k] = ok ? scale * row[c] : 0.f;
+                                inw[k] = ok && c >= lo && c <= hi;
+                                ng[k] = ok ? tt.gmult[c] : 0;
+                                if (inw[k]) m = fmaxf(m, sv[k] + bw);
+                                if (ng[k]) m = fmaxf(m, sv[k] + bg);
                             }
 #pragma unroll
                             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
                             float z = 0.f;
 #pragma unroll
-                            for (int k = 0; k < (kMaxTokens + 31) / 32; ++k) {
-                                lg[k] = (k < nk && lane + 32 * k < n) ? expf(lg[k] - m) : 0.f;
-                                z += lg[k];
+                            for (int k = 0; k < 2; ++k) {
+                                float p = inw[k] ? expf(sv[k] + bw - m) : 0.f;
+                                if (ng[k]) {
+                                    const float e = expf(sv[k] + bg - m);
+                                    for (int t = 0; t < ng[k]; ++t) p += e;
+                                }
+                                pv[k] = p;
+                                z += p;
                             }
 #pragma unroll
                             for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-                            __syncwarp();
-                            if (lane < kFuSP) row[lane] = 0.f;
-                            __syncwarp();
-                            // duplicate tokens: at most two commutative additions per column
-#pragma unroll
-                            for (int k = 0; k < (kMaxTokens + 31) / 32; ++k)
-                                if (k < nk && lane + 32 * k < n) atomicAdd(&row[cl[k]], lg[k]);
-                            if (lane == 0) zinv_s[pos][a_] = 1.0f / z;
-                        } else {
-                            if (lane < kFuSP) row[lane] = 0.f;
-                            if (lane == 0) zinv_s[pos][a_] = 0.f;
+                            zi = 1.0f / z;
                         }
+                        __syncwarp();
+                        if (lane < kFuSP) row[lane] = pv[0];
+                        if (lane == 0) zinv_s[pos][a_] = zi;
                     }
                     dev::named_bar(1, kFuWorkers * 32);
                     if (active) {

@@ -51,6 +51,13 @@ struct HostTokens {
     std::vector<uint8_t> col;
     std::vector<uint16_t> kv_frames;
     std::vector<uint16_t> kv_count;
+    // Per-column form of the token lists (what the tensor-core cores use): query a's
+    // window tokens are the contiguous columns [wlo[a], whi[a]] of its block's K/V list,
+    // its global tokens put gmult[block][c] copies on column c; window / global tokens get
+    // the bias iff wflag / gflag (uniform per table, checked).
+    std::vector<uint16_t> nwin;
+    std::vector<uint8_t> wlo, whi, gmult;
+    int wflag = 0, gflag = 0;
     uint32_t nq = 0, nqb = 0;
     bool kv_ok = true;
     void resize(uint32_t n) {
@@ -62,13 +69,20 @@ struct HostTokens {
         col.assign(size_t(n) * kMaxTokens, 0);
         kv_frames.assign(size_t(nqb) * kKvMax, 0);
         kv_count.assign(nqb, 0);
+        nwin.assign(n, 0);
+        wlo.assign(n, 0);
+        whi.assign(n, 0);
+        gmult.assign(size_t(nqb) * kKvMax, 0);
     }
-    void push(uint32_t a, uint32_t row, bool b) {
+    // Window tokens first, then (global = true) the sampled global tokens.
+    void push(uint32_t a, uint32_t row, bool b, bool global = false) {
         const uint16_t k = count[a];
         if (k >= kMaxTokens) config_error("too many tokens per query (n_local + 1 + n_global)");
+        if (!global && nwin[a] != k) config_error("window tokens must precede global tokens");
         rows[size_t(a) * kMaxTokens + k] = uint16_t(row);
         biased[size_t(a) * kMaxTokens + k] = b ? 1 : 0;
         count[a] = k + 1;
+        if (!global) nwin[a] = k + 1;
     }
     // Builds the per-block K/V lists; call after all push()es.
     void finalize();

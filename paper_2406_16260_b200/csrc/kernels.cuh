@@ -68,6 +68,10 @@ struct TokenTable {
     const uint8_t* col;         // [nq][kMaxTokens] token -> column of its block's K/V list
     const uint16_t* kv_frames;  // [nqb][kKvMax] K/V frame row of each column
     const uint16_t* kv_count;   // [nqb]
+    const uint8_t* wlo;         // [nq] first window column of the query's block list
+    const uint8_t* whi;         // [nq] last window column (inclusive)
+    const uint8_t* gmult;       // [nqb][kKvMax] global tokens on each column
+    int wflag, gflag;           // window / global tokens carry +bias
     int kv_ok;                  // every block's K/V list fits kKvMax
     int max_kv;                 // largest K/V list over the blocks
 };

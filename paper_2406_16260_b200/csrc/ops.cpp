@@ -321,7 +321,7 @@ void dual_scope(const vinf_tensor* v, double t, const vinf_attention_params* p,
     tok.resize(F);
     for (uint32_t a = 0; a < F; ++a) {
         for (uint32_t g : build_local_window(a, F, cfg->n_local)) tok.push(a, g, !bias_global);
-        for (uint32_t g : gset) tok.push(a, g, bias_global);
+        for (uint32_t g : gset) tok.push(a, g, bias_global, true);
     }
     attention_generic(v->data, v->dtype, F, v->h * v->w, v->c, 0, F, tok, p, cfg->bias, out, s);
 }
@@ -427,7 +427,7 @@ void attention_parallel(uint32_t frames, uint32_t workers, uint32_t worker, cons
                                std::to_string(worker));
             tok.push(a, g - ext_start, !bias_global);
         }
-        for (uint32_t j = 0; j < cfg->n_global; ++j) tok.push(a, ext_f + j, bias_global);
+        for (uint32_t j = 0; j < cfg->n_global; ++j) tok.push(a, ext_f + j, bias_global, true);
     }
     const size_t fb = size_t(v->h) * v->w * v->c * elem_size(v->dtype);
     TmpBuf ext(size_t(ext_f + ng) * fb, s);

@@ -88,6 +88,7 @@ void predict_groupnorm_traffic(uint32_t frames, uint32_t workers, uint32_t group
 
 void HostTokens::finalize() {
     kv_ok = true;
+    wflag = gflag = -1;
     for (uint32_t qb = 0; qb < nqb; ++qb) {
         std::vector<uint16_t> uniq;
         const uint32_t a1 = std::min<uint32_t>(nq, (qb + 1) * kQBlock);
@@ -108,12 +109,40 @@ void HostTokens::finalize() {
                 col[size_t(a) * kMaxTokens + i] =
                     uint8_t(std::lower_bound(uniq.begin(), uniq.end(), row) - uniq.begin());
             }
+        // per-column form: the window is a contiguous frame range, hence a contiguous
+        // column range of the sorted list; the global tokens are counted per column
+        for (uint32_t a = qb * kQBlock; a < a1; ++a) {
+            const uint8_t* c = &col[size_t(a) * kMaxTokens];
+            const uint8_t* f = &biased[size_t(a) * kMaxTokens];
+            const uint32_t nw = nwin[a], n = count[a];
+            if (nw == 0) config_error("every query needs at least one window token");
+            wlo[a] = c[0];
+            whi[a] = c[nw - 1];
+            if (uint32_t(whi[a] - wlo[a] + 1) != nw) config_error("window tokens must be contiguous frames");
+            for (uint32_t i = 0; i < n; ++i) {
+                const bool is_w = i < nw;
+                int& flag = is_w ? wflag : gflag;
+                if (flag == -1) flag = f[i];
+                if (flag != f[i]) config_error("bias flags must be uniform per token kind");
+                if (is_w && i > 0 && c[i] != c[i - 1] + 1) config_error("window tokens must be ascending");
+            }
+            if (a == qb * kQBlock) {
+                for (uint32_t i = nw; i < n; ++i) ++gmult[size_t(qb) * kKvMax + c[i]];
+            } else {  // every query of a block has the same global tokens
+                std::vector<uint8_t> gm(kKvMax, 0);
+                for (uint32_t i = nw; i < n; ++i) ++gm[c[i]];
+                if (!std::equal(gm.begin(), gm.end(), gmult.begin() + size_t(qb) * kKvMax))
+                    config_error("queries of one block must share their global tokens");
+            }
+        }
     }
+    if (wflag < 0) wflag = 0;
+    if (gflag < 0) gflag = 0;
 }
 
 size_t HostTokens::blob_bytes() const {
     return rows.size() * 2 + biased.size() + col.size() + count.size() * 2 +
-           kv_frames.size() * 2 + kv_count.size() * 2 + 64;
+           kv_frames.size() * 2 + kv_count.size() * 2 + wlo.size() + whi.size() + gmult.size() + 64;
 }
 
 void HostTokens::pack(uint8_t* dst) const {
@@ -128,6 +157,9 @@ void HostTokens::pack(uint8_t* dst) const {
     put(kv_count.data(), kv_count.size() * 2);
     put(biased.data(), biased.size());
     put(col.data(), col.size());
+    put(wlo.data(), wlo.size());
+    put(whi.data(), whi.size());
+    put(gmult.data(), gmult.size());
 }
 
 TokenTable HostTokens::view(const uint8_t* base) const {
@@ -144,6 +176,14 @@ TokenTable HostTokens::view(const uint8_t* base) const {
     t.biased = base + o;
     o += biased.size();
     t.col = base + o;
+    o += col.size();
+    t.wlo = base + o;
+    o += wlo.size();
+    t.whi = base + o;
+    o += whi.size();
+    t.gmult = base + o;
+    t.wflag = wflag;
+    t.gflag = gflag;
     t.kv_ok = kv_ok ? 1 : 0;
     t.max_kv = 0;
     for (uint16_t c : kv_count) t.max_kv = std::max<int>(t.max_kv, c);
@@ -228,7 +268,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
             for (uint32_t g : build_local_window(start + a, d.frames, d.n_local))
                 tok[b].push(a, ha + g - start, (b & 1) == 0);
             for (uint32_t j = 0; j < d.n_global; ++j)
-                tok[b].push(a, b >= 2 ? null_frame : g_frame[j], (b & 1) == 1);
+                tok[b].push(a, b >= 2 ? null_frame : g_frame[j], (b & 1) == 1, true);
         }
         tok[b].finalize();
     }

@@ -220,8 +220,10 @@ def test_engine_clip_parallel_equals_single(mods, oracle, n, dtype):
     en.forward(900.0, engines)
     got = torch.cat([e.y for e in engines])
     torch.cuda.synchronize()
-    # identical arithmetic except the GN statistics' summation grouping
-    bound = 1e-5 if dtype == torch.float32 else 2e-3
+    # identical arithmetic except the summation grouping of the GN statistics and of the
+    # softmax normaliser (columns follow each worker's K/V list); in bf16 that can move an
+    # output by one unit in the last place (2^-8 relative)
+    bound = 1e-5 if dtype == torch.float32 else 2.0 ** -8
     assert normwise(to_np(got), to_np(single.y)) <= bound
     if dtype == torch.float32:
         bp = oracle.build_block(64, 3, weight_seed=1)
