@@ -471,7 +471,7 @@ int launch_qkv_attention_fused(const void* u2, uint32_t af, uint32_t f_own0, uin
         if (e != cudaSuccess) return int(e);
         attr = L.total;
     }
-    static const uint32_t stagger = getenv("VINF_FUSED_STAGGER") ? 1u : 0u;
+    const uint32_t stagger = 0;  // 1 rotates the channel-chunk order per CTA (measured: no gain)
     return int(launch_pdl(qkv_attention_fused_kernel, dim3(HW / P), dim3(kFuThreads), L.total, s, maps, HW, C,
                           F, P, f_own0, tt, scale, bias, static_cast<__nv_bfloat16*>(ctx), stagger));
 }

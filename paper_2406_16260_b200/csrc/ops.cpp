@@ -147,18 +147,11 @@ void check_tensor(const vinf_tensor* t, const char* what) {
 
 uint64_t numel(const vinf_tensor* t) { return uint64_t(t->f) * t->h * t->w * t->c; }
 
-static bool tmp_sync() {
-    static int v = -1;
-    if (v < 0) v = getenv("VINF_TMP_SYNC") ? 1 : 0;
-    return v == 1;
-}
 TmpBuf::TmpBuf(size_t bytes, cudaStream_t s) : s_(s) {
-    if (bytes && tmp_sync()) cuda_check(cudaMalloc(&p, bytes + 4096), "cudaMalloc");
-    else if (bytes) cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    if (bytes) cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
 }
 TmpBuf::~TmpBuf() {
-    if (p && tmp_sync()) { cudaStreamSynchronize(s_); cudaFree(p); }
-    else if (p) cudaFreeAsync(p, s_);
+    if (p) cudaFreeAsync(p, s_);
 }
 
 // Operand view of a [rows, C] activation; fp32 inputs are split into hi/lo planes.
