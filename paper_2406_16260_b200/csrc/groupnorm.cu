@@ -462,11 +462,25 @@ __global__ void __launch_bounds__(128)
     const uint32_t per = (blocks + kFoldSegs - 1) / kFoldSegs;
     const uint32_t b0 = min(blocks, sid * per), b1 = min(blocks, b0 + per);
     const float* base = part + uint64_t(which) * C + uint64_t(g) * gs;
+    // thread = (row lane, group column): rows b0 + rl, b0 + rl + nrl, ... of one column;
+    // a warp reads whole runs of the group's columns, loads independent (no divisions)
     double a = 0.0;
-    const uint32_t n = (b1 - b0) * gs;
-    for (uint32_t i = threadIdx.x; i < n; i += 128) {
-        const uint32_t b = b0 + i / gs, c = i % gs;
-        a += double(base[uint64_t(b) * 2 * C + c]);
+    const uint32_t nrl = gs <= 128 ? 128 / gs : 1;
+    const uint32_t rl = threadIdx.x / gs, c = threadIdx.x % gs;
+    if (rl < nrl && c < gs) {
+        double a1 = 0.0;
+        uint32_t b = b0 + rl;
+        for (; b + nrl < b1; b += 2 * nrl) {
+            a += double(base[uint64_t(b) * 2 * C + c]);
+            a1 += double(base[uint64_t(b + nrl) * 2 * C + c]);
+        }
+        if (b < b1) a += double(base[uint64_t(b) * 2 * C + c]);
+        a += a1;
+    }
+    if (gs > 128) {  // wide groups: every thread strides the columns as well
+        a = 0.0;
+        for (uint32_t cc = threadIdx.x; cc < gs; cc += 128)
+            for (uint32_t b = b0; b < b1; ++b) a += double(base[uint64_t(b) * 2 * C + cc]);
     }
     red[threadIdx.x] = a;
     __syncthreads();
