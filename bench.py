@@ -206,6 +206,7 @@ def kernel_work(f_clip: int, dtype_bytes: int):
         "stub": (f_clip * E * (s + s), "hbm"),
         "gn_stats": (f_clip * E * s, "hbm"),
         "gn_apply": (f_clip * E * (s + s), "hbm"),
+        "gn_fold": (3 * C * C * (s + s) + 3 * C * 4, "hbm"),  # W read, W' + b' written
         "attn_core": (f_clip * E * s * 4, "hbm"),  # Q, K, V once + ctx write
     }
 

@@ -137,6 +137,28 @@ struct vinf_engine {
     void project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, bool with_q, cudaStream_t s);
     int qkv_ready = -1;  // block whose own-frame Q/K/V projection has already run
     bool fused = false;  // Q/K/V projection + attention core in one kernel (attn_fused.cu)
+    // bf16 mode: GroupNorm folded into the projections. The conv writes the raw GN input
+    // straight into the attention buffer (so the exchanges ship raw frames), GN_APPLY
+    // becomes one tiny kernel forming W' = W diag(s) and b' = W t, and the O GEMM adds the
+    // residual as u * s + t. Needs the same (s, t) on every worker for every frame, and
+    // zero receive/null frames to stay zero after projection, so not under GroupNorm or
+    // attention ablation. VINF_NO_GN_FOLD=1 keeps the separate apply kernel.
+    bool fold_env = [] {
+        const char* v = getenv("VINF_NO_GN_FOLD");
+        return !v || !*v || *v == '0';
+    }();
+    bool fold() const {
+        return !f32() && fold_env && (ablate == VINF_ABLATE_NONE || ablate == VINF_ABLATE_CONV);
+    }
+    bool use_fused() const { return fused && !fold(); }
+    DevMat wfold_view() const {  // the folded Q/K/V weights (workspace), hi plane only
+        DevMat m;
+        m.rows = 3 * L.d.channels;
+        m.K = L.d.channels;
+        m.hi = at<__nv_bfloat16>(L.off_wfold);
+        return m;
+    }
+    float* gn_aff() const { return at<float>(L.off_gnaff); }  // [s; t; b'(3C)]
 };
 
 void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
@@ -177,7 +199,7 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     ep.res = f32() ? at(L.off_u0f) : static_cast<void*>(at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E);
     ep.res_ld = C;
     ep.res_bf16 = !f32();
-    ep.out = at(L.off_u1);
+    ep.out = fold() ? static_cast<void*>(at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E) : at(L.off_u1);
     ep.out_ld = C;
     ep.out_bf16 = !f32();
     // GroupNorm statistics of u1 fused into the GEMM epilogue: per-column (sum, sum of
@@ -203,12 +225,18 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     double* sums = at<double>(L.off_sums);
     double* stats = at<double>(L.off_stats);
     const uint32_t G = L.d.groups;
-    Span span(this, "gn_apply", s);
+    Span span(this, fold() ? "gn_fold" : "gn_apply", s);
     // mean = sum / n, var = sumsq / n - mean^2 over the whole video (n counts all clips),
     // formed by the apply kernel itself from the (all-reduced) sums
     (void)stats;
     auto* u2 = at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E;
-    if (f32()) {
+    if (fold()) {
+        const uint32_t C = L.d.channels;
+        float* aff = gn_aff();
+        cuda_check(launch_group_fold(sums, gn_count(), C, G, B.gamma(), B.beta(), L.d.epsilon, B.wqkv.hi,
+                                     3 * C, wfold_view().hi, aff + 2 * C, aff, s),
+                   "gn fold");
+    } else if (f32()) {
         auto* lo = at<__nv_bfloat16>(L.off_u2lo) + uint64_t(L.ha) * L.E;
         cuda_check(launch_group_apply(at(L.off_u1), false, uint64_t(L.f_clip) * L.hw,
                                       L.d.channels, G, sums, nullptr, B.gamma(), B.beta(),
@@ -238,11 +266,13 @@ void vinf_engine::project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, boo
     A.ld = C;
     const size_t qes = f32() ? 4 : 2;
     Epilogue ep;
+    const bool fo = fold();
+    if (fo) ep.bias = gn_aff() + 2 * C + (with_q ? 0 : C);
     ep.out = at(L.off_qkv) + (uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C)) * qes;
     ep.out_ld = 3 * C;
     ep.out_bf16 = !f32();
     Span span(this, with_q ? "qkv_gemm" : "kv_gemm_ctx", s);
-    gemm(A, {int64_t(frame0) * int64_t(hw)}, B.wqkv, {with_q ? 0 : int64_t(C)},
+    gemm(A, {int64_t(frame0) * int64_t(hw)}, fo ? wfold_view() : B.wqkv, {with_q ? 0 : int64_t(C)},
          int64_t(nframes) * int64_t(hw), with_q ? 3 * C : 2 * C, ep, f32(), s);
     ++launches;
 }
@@ -250,7 +280,7 @@ void vinf_engine::project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, boo
 // The own frames' Q/K/V projection only: it reads just this clip's normalised frames, so
 // a driver may run it while the attention exchange is in flight (on another stream).
 void vinf_engine::stage_qkv(uint32_t b, cudaStream_t s) {
-    if (!fused) project_qkv(b, L.ha, L.f_clip, true, s);  // fused: the attention kernel projects
+    if (!use_fused()) project_qkv(b, L.ha, L.f_clip, true, s);  // fused: the attention kernel projects
     qkv_ready = int(b);
 }
 
@@ -265,7 +295,7 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
     const bool own_done = qkv_ready == int(b);
     qkv_ready = -1;
-    if (fused && !abl) {
+    if (use_fused() && !abl) {
         // Q/K/V projection and the attention core in one kernel: Q/K/V never reach HBM
         Span span(this, "qkv_attn_fused", s);
         cuda_check(launch_qkv_attention_fused(at(L.off_u2), L.af, L.ha, L.hw, C, L.f_clip, B.wqkv.hi,
@@ -298,6 +328,10 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     ep.res = f32() ? at(L.off_u2f) : static_cast<void*>(at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E);
     ep.res_ld = C;
     ep.res_bf16 = !f32();
+    if (fold()) {  // the buffer holds the raw GN input: residual = GN(u) = u * s + t
+        ep.res_scale = gn_aff();
+        ep.bias = gn_aff() + C;
+    }
     ep.out = y_of(b);
     ep.out_ld = C;
     ep.out_bf16 = !f32();

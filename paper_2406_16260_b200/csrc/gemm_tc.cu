@@ -123,6 +123,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     // rr already holds this warp's first chunk (loaded before the accumulator was ready)
 #pragma unroll 1
     for (int c = 32 * half; c < BN; c += 64) {
+        float rs[8];  // residual scale of this lane's 8 columns (GroupNorm folding)
+        if (RES && p.res_scale) {
+            const int nc = min(n0 + c + tc, n_lim - 8);
+            const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.res_scale + nc));
+            const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.res_scale + nc) + 1);
+            rs[0] = s0.x; rs[1] = s0.y; rs[2] = s0.z; rs[3] = s0.w;
+            rs[4] = s1.x; rs[5] = s1.y; rs[6] = s1.z; rs[7] = s1.w;
+        }
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_acc + (uint32_t(q * 32) << 16) + c, r);
         dev::tmem_wait_ld();
@@ -141,12 +149,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
             if (RES) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
+                    float r;
                     if (OBF) {
                         const uint32_t w = rr.w[i][k >> 1];
-                        cur[i][k] += __uint_as_float((k & 1) ? (w & 0xFFFF0000u) : (w << 16));
+                        r = __uint_as_float((k & 1) ? (w & 0xFFFF0000u) : (w << 16));
                     } else {
-                        cur[i][k] += __uint_as_float(rr.w[i][k % EpiRes<OBF>::W]);
+                        r = __uint_as_float(rr.w[i][k % EpiRes<OBF>::W]);
                     }
+                    cur[i][k] = p.res_scale ? fmaf(r, rs[k], cur[i][k]) : cur[i][k] + r;
                 }
             }
         }

@@ -33,6 +33,7 @@ struct GemmParams {
     GemmSeg seg[kGemmMaxSeg];
     const float* bias;  // [N] fp32 or null
     const void* res;    // residual [M, ld] or null
+    const float* res_scale;  // optional per-column scale of the residual (16-byte aligned)
     int64_t res_ld;
     int32_t res_bf16;
     void* out;

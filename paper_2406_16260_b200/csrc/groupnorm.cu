@@ -519,6 +519,99 @@ int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uin
                           C, groups, seg, tickets, sums));
 }
 
+// GroupNorm folded into the following projection (bf16 mode): with per-channel
+// s_c = gamma_c / sqrt(var_g + eps) and t_c = beta_c - mu_g s_c (the same f64 moments as
+// group_apply_bf16_kernel), GN(y) W^T = y (W diag(s))^T + W t. One warp per output row n
+// of W [N][C] (16-byte loads): W'[n][:] = bf16(W[n][:] * s) and bias[n] = sum_k W[n][k] t_k
+// (fixed-order lane sums + butterfly: deterministic). CTA 0 also stores s and t for the
+// O GEMM (residual scale s, bias t).
+__global__ void __launch_bounds__(256)
+    group_fold_kernel(const double* __restrict__ sums, double count, uint32_t C, uint32_t groups,
+                      const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                      const __nv_bfloat16* __restrict__ w, uint32_t N, __nv_bfloat16* __restrict__ wf,
+                      float* __restrict__ bias, float* __restrict__ st) {
+    extern __shared__ __align__(16) float tab[];  // [2][C]: s, t
+    constexpr int kMaxV = 4;  // 16-byte pieces of a row per lane: C <= 1024
+    const uint32_t lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    const uint32_t n = blockIdx.x * warps + (threadIdx.x >> 5);
+    const bool vec = C % 8 == 0 && C <= 32 * 8 * kMaxV;
+    // weights do not depend on the preceding kernels: fetch this warp's row and this
+    // thread's (gamma, beta) before the dependency wait
+    uint4 wr[kMaxV];
+#pragma unroll
+    for (int i = 0; i < kMaxV; ++i) {
+        const uint32_t v = lane + 32 * i;
+        wr[i] = (vec && n < N && v < C / 8) ? __ldg(reinterpret_cast<const uint4*>(w + uint64_t(n) * C) + v)
+                                             : make_uint4(0u, 0u, 0u, 0u);
+    }
+    dev::pdl_wait();
+    dev::pdl_trigger();
+    const uint32_t gs = C / groups;
+    for (uint32_t ch = threadIdx.x; ch < C; ch += blockDim.x) {
+        const uint32_t g = ch / gs;
+        const double m = sums[g] / count;
+        double var = sums[groups + g] / count - m * m;
+        var = var > 0.0 ? var : 0.0;
+        const float sc = float(double(gamma[ch]) / sqrt(var + double(eps)));
+        const float t = beta[ch] - float(m) * sc;
+        tab[ch] = sc;
+        tab[C + ch] = t;
+        if (blockIdx.x == 0 && st) {
+            st[ch] = sc;
+            st[C + ch] = t;
+        }
+    }
+    __syncthreads();
+    if (n >= N) return;
+    float acc = 0.f;
+    if (vec) {
+        uint4* orow = reinterpret_cast<uint4*>(wf + uint64_t(n) * C);
+#pragma unroll
+        for (int i = 0; i < kMaxV; ++i) {
+            const uint32_t v = lane + 32 * i;
+            if (v >= C / 8) break;
+            const uint32_t in[4] = {wr[i].x, wr[i].y, wr[i].z, wr[i].w};
+            const float4 s0 = *reinterpret_cast<const float4*>(tab + v * 8);
+            const float4 s1 = *reinterpret_cast<const float4*>(tab + v * 8 + 4);
+            const float4 t0 = *reinterpret_cast<const float4*>(tab + C + v * 8);
+            const float4 t1 = *reinterpret_cast<const float4*>(tab + C + v * 8 + 4);
+            const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+            uint32_t out[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float w0 = __uint_as_float(in[h] << 16), w1 = __uint_as_float(in[h] & 0xFFFF0000u);
+                const __nv_bfloat162 b2 = __floats2bfloat162_rn(w0 * sv[2 * h], w1 * sv[2 * h + 1]);
+                out[h] = *reinterpret_cast<const uint32_t*>(&b2);
+                acc = fmaf(w0, tv[2 * h], acc);
+                acc = fmaf(w1, tv[2 * h + 1], acc);
+            }
+            orow[v] = make_uint4(out[0], out[1], out[2], out[3]);
+        }
+    } else {
+        for (uint32_t k = lane; k < C; k += 32) {
+            const float wk = __bfloat162float(w[uint64_t(n) * C + k]);
+            wf[uint64_t(n) * C + k] = __float2bfloat16_rn(wk * tab[k]);
+            acc = fmaf(wk, tab[C + k], acc);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) bias[n] = acc;
+}
+
+int launch_group_fold(const double* sums, double count, uint32_t C, uint32_t groups, const float* gamma,
+                      const float* beta, float eps, const __nv_bfloat16* w, uint32_t N,
+                      __nv_bfloat16* wf, float* bias, float* st, cudaStream_t s) {
+    if (groups == 0 || C % groups != 0 || groups > kMaxGroupsApply || count <= 0.0)
+        return int(cudaErrorInvalidValue);
+    const size_t shm = sizeof(float) * 2 * C;
+    if (shm > 48 * 1024) return int(cudaErrorInvalidValue);
+    const uint32_t grid = (N + 7) / 8;  // one warp per row, 8 per CTA (s, t built per CTA)
+    return int(launch_pdl(group_fold_kernel, dim3(grid), dim3(256), shm, s, sums, count, C, groups,
+                          gamma, beta, eps, w, N, wf, bias, st));
+}
+
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
                          cudaStream_t s) {
     group_moments_kernel<<<(groups + 127) / 128, 128, 0, s>>>(sums, count, groups, stats);

@@ -122,6 +122,7 @@ struct Operand {
 struct Epilogue {
     const float* bias = nullptr;
     const void* res = nullptr;
+    const float* res_scale = nullptr;  // residual * scale per column (or identity)
     int64_t res_ld = 0;
     bool res_bf16 = false;
     void* out = nullptr;

@@ -51,6 +51,11 @@ int launch_group_moments(const double* sums, double count, uint32_t groups, doub
 // y = gamma * (x - mean_g) / sqrt(var_g + eps) + beta; optional hi/lo split output.
 // count > 0: means holds the whole video's (sum, sum of squares) and vars is unused;
 // the moments are formed in the kernel (group_moments_kernel's arithmetic).
+// bf16 mode: GroupNorm folded into the next projection W [N][C] (groupnorm.cu):
+// wf = bf16(W diag(s)), bias = W t, st = [s; t] (f32, 2C) for the residual affine.
+int launch_group_fold(const double* sums, double count, uint32_t C, uint32_t groups, const float* gamma,
+                      const float* beta, float eps, const __nv_bfloat16* w, uint32_t N,
+                      __nv_bfloat16* wf, float* bias, float* st, cudaStream_t s);
 int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
                        const double* means, const double* vars, const float* gamma,
                        const float* beta, float eps, void* y, bool out_bf16, __nv_bfloat16* hi,

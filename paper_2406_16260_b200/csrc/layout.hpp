@@ -37,6 +37,9 @@ struct Layout {
     uint64_t off_x = 0, off_y = 0, off_tmp = 0, off_u0 = 0, off_u0lo = 0, off_u0f = 0, off_u1 = 0;
     uint64_t off_u2 = 0, off_u2lo = 0, off_u2f = 0, off_qkv = 0, off_ctx = 0, off_ctxlo = 0;
     uint64_t off_sums = 0, off_stats = 0, off_scratch = 0, off_colstats = 0, off_tok[4] = {0, 0, 0, 0};
+    // bf16 mode: GroupNorm folded into the projections (engine.cpp stage_gn_apply):
+    // W' = W diag(s) [3C][C] bf16, b' = W t [3C] f32, s and t [C] f32
+    uint64_t off_wfold = 0, off_gnaff = 0;
     uint64_t scratch_elems = 0, total = 0;
 
     std::vector<vinf_xfer> xconv, xattn;

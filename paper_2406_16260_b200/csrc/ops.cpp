@@ -121,6 +121,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         const bool first = c0 == 0;
         p.bias = first ? ep.bias : nullptr;
         p.res = first ? ep.res : ep.out;
+        p.res_scale = first ? ep.res_scale : nullptr;
         p.res_ld = first ? ep.res_ld : ep.out_ld;
         p.res_bf16 = first ? ep.res_bf16 : ep.out_bf16;
         p.out = ep.out;

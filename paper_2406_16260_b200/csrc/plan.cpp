@@ -295,6 +295,10 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     off_ctx = take(clip * 2);
     off_ctxlo = f32 ? take(clip * 2) : 0;
     off_sums = take(sizeof(double) * 2 * d.groups);
+    if (!f32) {
+        off_wfold = take(uint64_t(3) * d.channels * d.channels * 2);
+        off_gnaff = take(sizeof(float) * 5 * d.channels);
+    }
     off_stats = take(sizeof(double) * 2 * d.groups);
     scratch_elems = std::max<uint64_t>(uint64_t(kScratchBlocks) * d.groups,
                                        uint64_t(256) * 2 * d.channels);  // colpart segments

@@ -12,5 +12,5 @@ CMD="python bench.py --steps 3 --warmup 2 --no-cpu-baseline"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 300 $CMD > gpurun_out/plain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_tc|attention_core|group_apply|stub|colpart|colseg" -s 8 -c 8 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_tc|attention_core|group_apply|group_fold|stub|colpart|colseg" -s 8 -c 9 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 ls -la gpurun_out
