@@ -109,10 +109,56 @@ __device__ __forceinline__ void epi_load_res(const GemmParams& p, EpiRes<OBF>& r
     }
 }
 
+// Per-lane column statistics accumulated over a CTA's tiles (kGemmFlagColCta): chunk j of
+// this warp (columns 32*half + 64*j + tc .. +7), its 4 rows per tile.
+template <int BN>
+constexpr int epi_chunks() { return ((BN + 31) / 32 + 1) / 2; }
+template <int BN, bool ST>
+struct EpiStats {
+    float s[ST ? epi_chunks<BN>() : 1][8], q[ST ? epi_chunks<BN>() : 1][8];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int j = 0; j < (ST ? epi_chunks<BN>() : 1); ++j)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s[j][k] = q[j][k] = 0.f;
+    }
+};
+
+// Writes a CTA's accumulated statistics: butterfly over the lanes holding the same
+// columns (l ^ 4, 8, 16), then lanes tr == 0 store their 8 columns' (sum, sum of squares).
+template <int BN, bool ST>
+__device__ __forceinline__ void epi_flush_stats(const GemmParams& p, EpiStats<BN, ST>& acc, int lane,
+                                                int row, int n0, int half) {
+    if (!ST) return;
+    const int tr = lane >> 2, tc = (lane & 3) * 8;
+    const int n_lim = min(p.N, n0 + BN);
+#pragma unroll
+    for (int j = 0; j < epi_chunks<BN>(); ++j) {
+        const int c = 32 * half + 64 * j;
+        if (c >= BN) break;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#pragma unroll
+            for (int o = 4; o <= 16; o <<= 1) {
+                acc.s[j][k] += __shfl_xor_sync(0xffffffffu, acc.s[j][k], o);
+                acc.q[j][k] += __shfl_xor_sync(0xffffffffu, acc.q[j][k], o);
+            }
+        }
+        const int n = n0 + c + tc;
+        if (tr == 0 && n < n_lim) {
+            float* part = p.colpart + int64_t(row) * 2 * p.N + n;
+            *reinterpret_cast<float4*>(part) = make_float4(acc.s[j][0], acc.s[j][1], acc.s[j][2], acc.s[j][3]);
+            *reinterpret_cast<float4*>(part + 4) = make_float4(acc.s[j][4], acc.s[j][5], acc.s[j][6], acc.s[j][7]);
+            *reinterpret_cast<float4*>(part + p.N) = make_float4(acc.q[j][0], acc.q[j][1], acc.q[j][2], acc.q[j][3]);
+            *reinterpret_cast<float4*>(part + p.N + 4) = make_float4(acc.q[j][4], acc.q[j][5], acc.q[j][6], acc.q[j][7]);
+        }
+    }
+}
+
 template <int BN, bool OBF, bool RES, bool ST>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int q, int lane,
                                               uint32_t stg, int m0, int n0, int half,
-                                              EpiRes<OBF>& rr) {
+                                              EpiRes<OBF>& rr, EpiStats<BN, ST && OBF>& acc) {
     using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
     const int tr = lane >> 2;        // transposed: rows tr + 8i
     const int tc = (lane & 3) * 8;   // transposed: first of 8 columns
@@ -120,9 +166,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
     const bool store = !(p.flags & kGemmFlagNoStore);
     T* out = static_cast<T*>(p.out);
-    // rr already holds this warp's first chunk (loaded before the accumulator was ready)
-#pragma unroll 1
-    for (int c = 32 * half; c < BN; c += 64) {
+    constexpr bool kCta = ST && OBF;  // fp32 outputs keep the per-32-row form (registers)
+    const bool per_cta = kCta && (p.flags & kGemmFlagColCta);
+    // rr already holds this warp's first chunk (loaded before the accumulator was ready).
+    // Unrolled over the warp's chunks (static indices into the statistics registers).
+#pragma unroll
+    for (int jc = 0; jc < epi_chunks<BN>(); ++jc) {
+        const int c = 32 * half + 64 * jc;
+        if (c >= BN) break;
         float rs[8];  // residual scale of this lane's 8 columns (GroupNorm folding)
         if (RES && p.res_scale) {
             const int nc = min(n0 + c + tc, n_lim - 8);
@@ -210,7 +261,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
                 }
             }
         }
-        if (ST) {
+        if (kCta && per_cta) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                acc.s[kCta ? jc : 0][k] += cs[k];
+                acc.q[kCta ? jc : 0][k] += cq[k];
+            }
+        } else if (ST) {
             // lanes l ^ {4, 8, 16} hold the same 8 columns for the block's other rows
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -427,6 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0, nstore = 0;
         EpiRes<OBF> rr;
+        EpiStats<BN, ST && OBF> sacc;
+        sacc.zero();
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const uint32_t acc = local & 1;
             const int m0 = (tile / n_tiles) * kBM + q * 32, n0 = (tile % n_tiles) * BN;
@@ -443,11 +502,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       m0, n0, half, nstore);
             else
                 epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0,
-                                                n0, half, rr);
+                                                n0, half, rr, sacc);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (ST && OBF && (p.flags & kGemmFlagColCta))  // this CTA's one N tile, quadrant q's rows
+            epi_flush_stats<BN, ST && OBF>(p, sacc, lane, int(blockIdx.x / n_tiles) * 4 + q,
+                                    int(blockIdx.x % n_tiles) * BN, half);
         if (TMAO && lane == 0) bulk_wait_read<0>();  // staging must outlive the stores' reads
     }
 
@@ -598,6 +660,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0;
         EpiRes<OBF> rr;
+        EpiStats<BN, ST && OBF> sacc;  // unused: the pair kernel writes per-32-row partials
+        sacc.zero();
         for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
             const uint32_t acc = local & 1;
             const int m0 = (tile / n_tiles) * 2 * kBM + int(rank) * kBM + q * 32;
@@ -611,7 +675,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
             epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0, n0,
-                                            half, rr);
+                                            half, rr, sacc);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) dev::mbar_arrive_remote(dev::peer_addr(dev::smem_u32(&tempty[acc]), 0));
@@ -642,6 +706,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 int g_num_sms = 0;
+int num_sms_cached() {
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
 
 template <int BN, bool OBF, bool RES, bool ST = false, bool TMAO = false>
 int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
@@ -654,12 +727,7 @@ int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
         if (e != cudaSuccess) return int(e);
         attr_set = true;
     }
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
+    num_sms_cached();
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
     const int grid = std::max(1, std::min(tiles, g_num_sms));
     return int(launch_pdl(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>, dim3(grid), dim3(kThreads),
@@ -694,12 +762,7 @@ int launch_pair_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stre
         if (e != cudaSuccess) return int(e);
         attr_set = true;
     }
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
+    num_sms_cached();
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + 2 * kBM - 1) / (2 * kBM));
     const int clusters = std::max(1, std::min(tiles, g_num_sms / 2));
     gemm_tc2_kernel<BN, OBF, RES, ST><<<2 * clusters, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
@@ -749,6 +812,16 @@ int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t col
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
+int gemm_colpart_rows(int M, int N, int block_n, bool pair, bool out_bf16, bool* per_cta) {
+    const int n_tiles = (N + block_n - 1) / block_n;
+    const int tiles = n_tiles * ((M + kBM - 1) / kBM);
+    const int grid = std::max(1, std::min(tiles, num_sms_cached()));  // = launch_cfg's grid
+    static const bool off = getenv("VINF_GEMM_NO_COLCTA") != nullptr;  // A/B switch
+    const bool cta = !off && !pair && out_bf16 && grid % n_tiles == 0;
+    if (per_cta) *per_cta = cta;
+    return cta ? grid / n_tiles * 4 : (M + 31) / 32;
 }
 
 int gemm_pick_block_n(int N) {

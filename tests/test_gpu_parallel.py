@@ -305,10 +305,43 @@ np.save(sys.argv[2], np.stack(out))
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
-    for env in ({"VINF_FUSED_ATTN": "1"}, {}):
+    # (the fused kernel reads normalised frames: GroupNorm folding off in both runs)
+    for env in ({"VINF_FUSED_ATTN": "1", "VINF_NO_GN_FOLD": "1"}, {"VINF_NO_GN_FOLD": "1"}):
         path = f"/tmp/fused_{len(res)}.npy"
         r = subprocess.run([sys.executable, "-c", code, root, path], env=dict(os.environ, **env),
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(np.load(path))
     assert np.array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("n", [1, 3])
+def test_gn_fold_matches_apply_path(mods, oracle, n, monkeypatch):
+    # bf16 mode folds GroupNorm into W_qkv (W diag(s), bias W t) and the O GEMM residual;
+    # VINF_NO_GN_FOLD=1 keeps the explicit apply kernel. Both are bf16 evaluations of the
+    # same block: they agree to bf16 rounding, and each meets the oracle tolerance.
+    _, _, en, _ = mods
+    F = 24
+    kw = dict(BLOCK, frames=F)
+    x = dev(oracle.tensor_from_seed((F, 4, 8, 64), 11), torch.bfloat16)
+    outs = {}
+    for fold in (True, False):
+        if fold:
+            monkeypatch.delenv("VINF_NO_GN_FOLD", raising=False)
+        else:
+            monkeypatch.setenv("VINF_NO_GN_FOLD", "1")
+        engines = []
+        for w in range(n):
+            e = _engine(mods, torch.bfloat16, workers=n, worker=w, **kw)
+            e.init_weights(3)
+            e.x.copy_(x[w * F // n:(w + 1) * F // n])
+            engines.append(e)
+        for t in (900.0, 700.0):
+            en.forward(t, engines)
+            outs[(fold, t)] = torch.cat([e.y for e in engines]).clone()
+    bp = oracle.build_block(64, 3, weight_seed=3)
+    for t in (900.0, 700.0):
+        want = oracle.block_forward(to_np(x), bp, t, 8)
+        a, b = to_np(outs[(True, t)]), to_np(outs[(False, t)])
+        assert normwise(a, b) <= 1e-2, normwise(a, b)
+        assert normwise(a, want) <= TOL_BF16 and normwise(b, want) <= TOL_BF16
