@@ -208,14 +208,13 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     const uint64_t rows = uint64_t(L.f_clip) * L.hw;
     float* colpart = at<float>(L.off_colstats);
     ep.colpart = colpart;
-    uint32_t prow = 0;
     {
         Span span(this, "conv_gemm", s);
-        prow = gemm(A, ar, B.conv, br, int64_t(rows), C, ep, f32(), s);
+        gemm(A, ar, B.conv, br, int64_t(rows), C, ep, f32(), s);
     }
     ++launches;
     Span span(this, "gn_stats", s);
-    cuda_check(launch_colpart_to_groups(colpart, prow, C, L.d.groups,
+    cuda_check(launch_colpart_to_groups(colpart, uint32_t((rows + 31) / 32), C, L.d.groups,
                                         at<double>(L.off_sums), at<double>(L.off_scratch), s),
                "gn fold");
     launches += 1;

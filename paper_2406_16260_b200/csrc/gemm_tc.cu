@@ -109,56 +109,34 @@ __device__ __forceinline__ void epi_load_res(const GemmParams& p, EpiRes<OBF>& r
     }
 }
 
-// Per-lane column statistics accumulated over a CTA's tiles (kGemmFlagColCta): chunk j of
-// this warp (columns 32*half + 64*j + tc .. +7), its 4 rows per tile.
-template <int BN>
-constexpr int epi_chunks() { return ((BN + 31) / 32 + 1) / 2; }
-template <int BN, bool ST>
-struct EpiStats {
-    float s[ST ? epi_chunks<BN>() : 1][8], q[ST ? epi_chunks<BN>() : 1][8];
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int j = 0; j < (ST ? epi_chunks<BN>() : 1); ++j)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) s[j][k] = q[j][k] = 0.f;
-    }
+// Per-column epilogue vectors of a lane's 8 columns in one chunk: bias, and the residual
+// scale (GemmParams::res_scale, GroupNorm folding). Fetched one chunk ahead, like the
+// residual, so their load latency is not exposed.
+struct EpiCol {
+    float b[8], s[8];
 };
-
-// Writes a CTA's accumulated statistics: butterfly over the lanes holding the same
-// columns (l ^ 4, 8, 16), then lanes tr == 0 store their 8 columns' (sum, sum of squares).
-template <int BN, bool ST>
-__device__ __forceinline__ void epi_flush_stats(const GemmParams& p, EpiStats<BN, ST>& acc, int lane,
-                                                int row, int n0, int half) {
-    if (!ST) return;
-    const int tr = lane >> 2, tc = (lane & 3) * 8;
-    const int n_lim = min(p.N, n0 + BN);
-#pragma unroll
-    for (int j = 0; j < epi_chunks<BN>(); ++j) {
-        const int c = 32 * half + 64 * j;
-        if (c >= BN) break;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-#pragma unroll
-            for (int o = 4; o <= 16; o <<= 1) {
-                acc.s[j][k] += __shfl_xor_sync(0xffffffffu, acc.s[j][k], o);
-                acc.q[j][k] += __shfl_xor_sync(0xffffffffu, acc.q[j][k], o);
-            }
-        }
-        const int n = n0 + c + tc;
-        if (tr == 0 && n < n_lim) {
-            float* part = p.colpart + int64_t(row) * 2 * p.N + n;
-            *reinterpret_cast<float4*>(part) = make_float4(acc.s[j][0], acc.s[j][1], acc.s[j][2], acc.s[j][3]);
-            *reinterpret_cast<float4*>(part + 4) = make_float4(acc.s[j][4], acc.s[j][5], acc.s[j][6], acc.s[j][7]);
-            *reinterpret_cast<float4*>(part + p.N) = make_float4(acc.q[j][0], acc.q[j][1], acc.q[j][2], acc.q[j][3]);
-            *reinterpret_cast<float4*>(part + p.N + 4) = make_float4(acc.q[j][4], acc.q[j][5], acc.q[j][6], acc.q[j][7]);
-        }
+template <bool RES>
+__device__ __forceinline__ void epi_load_col(const GemmParams& p, EpiCol& col, int lane, int n0, int c,
+                                             int n_lim) {
+    const int n = n0 + c + (lane & 3) * 8;
+    const bool okb = p.bias && n < n_lim;
+    const float4 b0 = okb ? __ldg(reinterpret_cast<const float4*>(p.bias + n)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b1 = okb ? __ldg(reinterpret_cast<const float4*>(p.bias + n) + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    col.b[0] = b0.x; col.b[1] = b0.y; col.b[2] = b0.z; col.b[3] = b0.w;
+    col.b[4] = b1.x; col.b[5] = b1.y; col.b[6] = b1.z; col.b[7] = b1.w;
+    if (RES && p.res_scale) {
+        const int nc = min(n, n_lim - 8);
+        const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.res_scale + nc));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.res_scale + nc) + 1);
+        col.s[0] = s0.x; col.s[1] = s0.y; col.s[2] = s0.z; col.s[3] = s0.w;
+        col.s[4] = s1.x; col.s[5] = s1.y; col.s[6] = s1.z; col.s[7] = s1.w;
     }
 }
 
 template <int BN, bool OBF, bool RES, bool ST>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int q, int lane,
                                               uint32_t stg, int m0, int n0, int half,
-                                              EpiRes<OBF>& rr, EpiStats<BN, ST && OBF>& acc) {
+                                              EpiRes<OBF>& rr, EpiCol& col) {
     using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
     const int tr = lane >> 2;        // transposed: rows tr + 8i
     const int tc = (lane & 3) * 8;   // transposed: first of 8 columns
@@ -166,22 +144,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
     const bool store = !(p.flags & kGemmFlagNoStore);
     T* out = static_cast<T*>(p.out);
-    constexpr bool kCta = ST && OBF;  // fp32 outputs keep the per-32-row form (registers)
-    const bool per_cta = kCta && (p.flags & kGemmFlagColCta);
-    // rr already holds this warp's first chunk (loaded before the accumulator was ready).
-    // Unrolled over the warp's chunks (static indices into the statistics registers).
-#pragma unroll
-    for (int jc = 0; jc < epi_chunks<BN>(); ++jc) {
-        const int c = 32 * half + 64 * jc;
-        if (c >= BN) break;
-        float rs[8];  // residual scale of this lane's 8 columns (GroupNorm folding)
-        if (RES && p.res_scale) {
-            const int nc = min(n0 + c + tc, n_lim - 8);
-            const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.res_scale + nc));
-            const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.res_scale + nc) + 1);
-            rs[0] = s0.x; rs[1] = s0.y; rs[2] = s0.z; rs[3] = s0.w;
-            rs[4] = s1.x; rs[5] = s1.y; rs[6] = s1.z; rs[7] = s1.w;
-        }
+    // rr and col already hold this warp's first chunk (loaded before the accumulator was ready)
+#pragma unroll 1
+    for (int c = 32 * half; c < BN; c += 64) {
+        const EpiCol cc = col;
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_acc + (uint32_t(q * 32) << 16) + c, r);
         dev::tmem_wait_ld();
@@ -207,22 +173,18 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
                     } else {
                         r = __uint_as_float(rr.w[i][k % EpiRes<OBF>::W]);
                     }
-                    cur[i][k] = p.res_scale ? fmaf(r, rs[k], cur[i][k]) : cur[i][k] + r;
+                    cur[i][k] = p.res_scale ? fmaf(r, cc.s[k], cur[i][k]) : cur[i][k] + r;
                 }
             }
         }
         __syncwarp();
-        if (c + 64 < BN && n0 + c + 64 < n_lim)
-            epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, c + 64, full, n_lim);  // next chunk
+        if (c + 64 < BN && n0 + c + 64 < n_lim) {  // next chunk
+            epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, c + 64, full, n_lim);
+            epi_load_col<RES>(p, col, lane, n0, c + 64, n_lim);
+        }
         if (!store) continue;
         const int n = n0 + c + tc;
-        float b8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (p.bias && n < n_lim) {
-            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + n));
-            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + n) + 1);
-            b8[0] = b0.x; b8[1] = b0.y; b8[2] = b0.z; b8[3] = b0.w;
-            b8[4] = b1.x; b8[5] = b1.y; b8[6] = b1.z; b8[7] = b1.w;
-        }
+        const float* b8 = cc.b;
         float cs[8], cq[8];  // column stats of the stored values
 #pragma unroll
         for (int k = 0; k < 8; ++k) cs[k] = cq[k] = 0.f;
@@ -261,13 +223,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
                 }
             }
         }
-        if (kCta && per_cta) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                acc.s[kCta ? jc : 0][k] += cs[k];
-                acc.q[kCta ? jc : 0][k] += cq[k];
-            }
-        } else if (ST) {
+        if (ST) {
             // lanes l ^ {4, 8, 16} hold the same 8 columns for the block's other rows
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -484,16 +440,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0, nstore = 0;
         EpiRes<OBF> rr;
-        EpiStats<BN, ST && OBF> sacc;
-        sacc.zero();
+        EpiCol col;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const uint32_t acc = local & 1;
             const int m0 = (tile / n_tiles) * kBM + q * 32, n0 = (tile % n_tiles) * BN;
             if (!TMAO) {  // the residual does not depend on the accumulator: fetch it early
                 const int n_lim = min(p.N, n0 + BN);
                 const bool full = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
-                if (n0 + 32 * half < n_lim)
+                if (n0 + 32 * half < n_lim) {
                     epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, 32 * half, full, n_lim);
+                    epi_load_col<RES>(p, col, lane, n0, 32 * half, n_lim);
+                }
             }
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
@@ -502,14 +459,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       m0, n0, half, nstore);
             else
                 epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0,
-                                                n0, half, rr, sacc);
+                                                n0, half, rr, col);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (ST && OBF && (p.flags & kGemmFlagColCta))  // this CTA's one N tile, quadrant q's rows
-            epi_flush_stats<BN, ST && OBF>(p, sacc, lane, int(blockIdx.x / n_tiles) * 4 + q,
-                                    int(blockIdx.x % n_tiles) * BN, half);
         if (TMAO && lane == 0) bulk_wait_read<0>();  // staging must outlive the stores' reads
     }
 
@@ -660,8 +614,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
         uint32_t local = 0;
         EpiRes<OBF> rr;
-        EpiStats<BN, ST && OBF> sacc;  // unused: the pair kernel writes per-32-row partials
-        sacc.zero();
+        EpiCol col;
         for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
             const uint32_t acc = local & 1;
             const int m0 = (tile / n_tiles) * 2 * kBM + int(rank) * kBM + q * 32;
@@ -669,13 +622,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             {
                 const int n_lim = min(p.N, n0 + BN);
                 const bool full_t = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
-                if (n0 + 32 * half < n_lim)
+                if (n0 + 32 * half < n_lim) {
                     epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, 32 * half, full_t, n_lim);
+                    epi_load_col<RES>(p, col, lane, n0, 32 * half, n_lim);
+                }
             }
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
             epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0, n0,
-                                            half, rr, sacc);
+                                            half, rr, col);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) dev::mbar_arrive_remote(dev::peer_addr(dev::smem_u32(&tempty[acc]), 0));
@@ -706,15 +661,6 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 int g_num_sms = 0;
-int num_sms_cached() {
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
 
 template <int BN, bool OBF, bool RES, bool ST = false, bool TMAO = false>
 int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
@@ -727,7 +673,12 @@ int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
         if (e != cudaSuccess) return int(e);
         attr_set = true;
     }
-    num_sms_cached();
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
     const int grid = std::max(1, std::min(tiles, g_num_sms));
     return int(launch_pdl(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>, dim3(grid), dim3(kThreads),
@@ -762,7 +713,12 @@ int launch_pair_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stre
         if (e != cudaSuccess) return int(e);
         attr_set = true;
     }
-    num_sms_cached();
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
     const int tiles = ((p.N + BN - 1) / BN) * ((p.M + 2 * kBM - 1) / (2 * kBM));
     const int clusters = std::max(1, std::min(tiles, g_num_sms / 2));
     gemm_tc2_kernel<BN, OBF, RES, ST><<<2 * clusters, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
@@ -812,16 +768,6 @@ int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t col
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
-}
-
-int gemm_colpart_rows(int M, int N, int block_n, bool pair, bool out_bf16, bool* per_cta) {
-    const int n_tiles = (N + block_n - 1) / block_n;
-    const int tiles = n_tiles * ((M + kBM - 1) / kBM);
-    const int grid = std::max(1, std::min(tiles, num_sms_cached()));  // = launch_cfg's grid
-    static const bool off = getenv("VINF_GEMM_NO_COLCTA") != nullptr;  // A/B switch
-    const bool cta = !off && !pair && out_bf16 && grid % n_tiles == 0;
-    if (per_cta) *per_cta = cta;
-    return cta ? grid / n_tiles * 4 : (M + 31) / 32;
 }
 
 int gemm_pick_block_n(int N) {

@@ -44,16 +44,11 @@ struct GemmParams {
     // conv epilogue), one partial per 32-row block, each written exactly once (no atomics,
     // deterministic): colpart[(rb*2 + 0)*N + n] = sum over the block's rows of out[m,n],
     // colpart[(rb*2 + 1)*N + n] = sum of squares. fp32 [ceil(M/32)][2][N].
-    // With kGemmFlagColCta (persistent grid a multiple of the N-tile count, so each CTA
-    // keeps one N tile): each epilogue warp accumulates its columns over ALL of its CTA's
-    // tiles in registers and writes once at the end: rb = (cta / n_tiles) * 4 + quadrant,
-    // grid / n_tiles * 4 rows in all (gemm_colpart_rows), ~13x fewer than ceil(M/32).
     float* colpart;
 };
 
 constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic
 constexpr int32_t kGemmFlagTmaOut = 1 << 8;  // bf16 output leaves through TMA stores (maps.out)
-constexpr int32_t kGemmFlagColCta = 1 << 9;  // colpart rows per (CTA slot, quadrant), see above
 
 struct GemmMaps {
     CUtensorMap a[2];
@@ -74,10 +69,6 @@ int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaS
                    bool pair = false);
 // Whether a GEMM of this shape uses the CTA-pair kernel (VINF_GEMM_PAIR=0/1 overrides).
 bool gemm_use_pair(int M, int N, int block_n);
-
-// Rows of colpart the launch writes; *per_cta: whether it uses the kGemmFlagColCta form
-// (single-CTA kernel, bf16 output, grid a multiple of the N-tile count).
-int gemm_colpart_rows(int M, int N, int block_n, bool pair, bool out_bf16, bool* per_cta);
 
 // Largest supported N tile for a given N (used to build B tensor maps).
 int gemm_pick_block_n(int N);

@@ -128,16 +128,14 @@ struct Epilogue {
     void* out = nullptr;
     int64_t out_ld = 0;
     bool out_bf16 = false;
-    float* colpart = nullptr;  // fused per-column (sum, sum of squares) partials (see gemm())
+    float* colpart = nullptr;  // fused per-(32-row block, column) (sum, sum of squares)
 };
 
 // out[m, n] = sum_s A[m + a_rows[s]] . B[n + b_rows[s]] (+ bias, + res); M x N, K = A.cols.
 // Split mode (A.lo && B.lo) expands each segment into hi*hi + hi*lo + lo*hi.
-// Returns the rows of ep.colpart written (0 without statistics): per 32-row block, or per
-// (CTA slot, TMEM quadrant) when the persistent grid keeps one N tile per CTA.
-uint32_t gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
-              const std::vector<int64_t>& b_rows, int64_t M, int64_t N, const Epilogue& ep, bool split,
-              cudaStream_t s);
+void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
+          const std::vector<int64_t>& b_rows, int64_t M, int64_t N, const Epilogue& ep, bool split,
+          cudaStream_t s);
 
 }  // namespace vinf
 

@@ -71,17 +71,15 @@ void DevMat::release() {
 
 int g_gemm_debug_flags = 0;
 
-uint32_t gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
-              const std::vector<int64_t>& b_rows, int64_t M, int64_t N, const Epilogue& ep, bool split,
-              cudaStream_t s) {
+void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
+          const std::vector<int64_t>& b_rows, int64_t M, int64_t N, const Epilogue& ep, bool split,
+          cudaStream_t s) {
     if (A.cols != B.K) shape_error("gemm: K mismatch");
     if (a_rows.size() != b_rows.size() || a_rows.empty()) shape_error("gemm: segment mismatch");
-    if (M <= 0 || N <= 0) return 0;
+    if (M <= 0 || N <= 0) return;
     if (split && (!A.lo || !B.lo)) shape_error("gemm: split mode needs lo planes");
     const int bn = gemm_pick_block_n(int(N));
     const bool pair = gemm_use_pair(int(M), int(N), bn);
-    bool per_cta = false;
-    const uint32_t colpart_rows = uint32_t(gemm_colpart_rows(int(M), int(N), bn, pair, ep.out_bf16, &per_cta));
     const uint32_t b_box = uint32_t(pair ? bn / 2 : bn);  // the pair kernel loads half of B per CTA
     GemmMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -130,13 +128,9 @@ uint32_t gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat
         p.out_ld = ep.out_ld;
         p.out_bf16 = ep.out_bf16;
         p.flags = g_gemm_debug_flags | (tma_out ? kGemmFlagTmaOut : 0);
-        if (c0 + kGemmMaxSeg >= segs.size()) {  // final output only
-            p.colpart = ep.colpart;
-            if (ep.colpart && per_cta) p.flags |= kGemmFlagColCta;  // (bf16 outputs only)
-        }
+        if (c0 + kGemmMaxSeg >= segs.size()) p.colpart = ep.colpart;  // final output only
         cuda_check(gemm_tc_launch(maps, p, bn, s, pair), "gemm_tc_launch");
     }
-    return ep.colpart ? colpart_rows : 0;
 }
 
 // ---- activation operands ------------------------------------------------------
