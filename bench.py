@@ -204,7 +204,7 @@ def kernel_work(f_clip: int, dtype_bytes: int):
         "o_gemm": (2.0 * M * C * C, "tensor"),
         "kv_gemm_ctx": (None, "tensor"),
         "stub": (f_clip * E * (s + s), "hbm"),
-        "gn_stats": (f_clip * E * s, "hbm"),
+        "gn_stats": (((M + 31) // 32) * 2 * C * 4, "hbm"),  # the conv epilogue's 32-row partials
         "gn_apply": (f_clip * E * (s + s), "hbm"),
         "gn_fold": (3 * C * C * (s + s) + 3 * C * 4, "hbm"),  # W read, W' + b' written
         "attn_core": (f_clip * E * s * 4, "hbm"),  # Q, K, V once + ctx write
