@@ -531,7 +531,8 @@ __global__ void __launch_bounds__(256)
                       const __nv_bfloat16* __restrict__ w, uint32_t N, __nv_bfloat16* __restrict__ wf,
                       float* __restrict__ bias, float* __restrict__ st) {
     extern __shared__ __align__(16) float tab[];  // [2][C]: s, t
-    constexpr int kMaxV = 4;  // 16-byte pieces of a row per lane: C <= 1024
+    constexpr int kMaxV = 5;   // 16-byte pieces of a row per lane: C <= 1280
+    constexpr int kMaxCh = 8;  // channels per thread for (s, t): C <= 8 * blockDim
     const uint32_t lane = threadIdx.x & 31, warps = blockDim.x >> 5;
     const uint32_t n = blockIdx.x * warps + (threadIdx.x >> 5);
     const bool vec = C % 8 == 0 && C <= 32 * 8 * kMaxV;
@@ -544,16 +545,29 @@ __global__ void __launch_bounds__(256)
         wr[i] = (vec && n < N && v < C / 8) ? __ldg(reinterpret_cast<const uint4*>(w + uint64_t(n) * C) + v)
                                              : make_uint4(0u, 0u, 0u, 0u);
     }
+    float gm[kMaxCh], bt[kMaxCh];
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+        const uint32_t ch = threadIdx.x + blockDim.x * i;
+        gm[i] = ch < C ? __ldg(gamma + ch) : 0.f;
+        bt[i] = ch < C ? __ldg(beta + ch) : 0.f;
+    }
     dev::pdl_wait();
     dev::pdl_trigger();
+    // mean and variance in f64 from the (all-reduced) sums; the scale in f32 (it is
+    // rounded into bf16 weights)
     const uint32_t gs = C / groups;
-    for (uint32_t ch = threadIdx.x; ch < C; ch += blockDim.x) {
+    const double ic = 1.0 / count;
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+        const uint32_t ch = threadIdx.x + blockDim.x * i;
+        if (ch >= C) break;
         const uint32_t g = ch / gs;
-        const double m = sums[g] / count;
-        double var = sums[groups + g] / count - m * m;
+        const double m = sums[g] * ic;
+        double var = fma(-m, m, sums[groups + g] * ic);
         var = var > 0.0 ? var : 0.0;
-        const float sc = float(double(gamma[ch]) / sqrt(var + double(eps)));
-        const float t = beta[ch] - float(m) * sc;
+        const float sc = gm[i] * rsqrtf(float(var + double(eps)));
+        const float t = bt[i] - float(m) * sc;
         tab[ch] = sc;
         tab[C + ch] = t;
         if (blockIdx.x == 0 && st) {
@@ -606,7 +620,7 @@ int launch_group_fold(const double* sums, double count, uint32_t C, uint32_t gro
     if (groups == 0 || C % groups != 0 || groups > kMaxGroupsApply || count <= 0.0)
         return int(cudaErrorInvalidValue);
     const size_t shm = sizeof(float) * 2 * C;
-    if (shm > 48 * 1024) return int(cudaErrorInvalidValue);
+    if (shm > 48 * 1024 || C > 8 * 256) return int(cudaErrorInvalidValue);
     const uint32_t grid = (N + 7) / 8;  // one warp per row, 8 per CTA (s, t built per CTA)
     return int(launch_pdl(group_fold_kernel, dim3(grid), dim3(256), shm, s, sums, count, C, groups,
                           gamma, beta, eps, w, N, wf, bias, st));
