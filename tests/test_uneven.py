@@ -52,23 +52,27 @@ def test_even_split_still_required_without_flag(lib):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("F,N,blocks", [(19, 4, 1), (16, 3, 2)])
-def test_uneven_engines_match_single_worker(lib, F, N, blocks):
+@pytest.mark.parametrize("F,N,blocks,dtype", [(19, 4, 1, torch.float32), (16, 3, 2, torch.float32),
+                                              (19, 4, 2, torch.bfloat16)])
+def test_uneven_engines_match_single_worker(lib, F, N, blocks, dtype):
+    # bf16 runs the GroupNorm-folded projections: raw frames cross the uneven clip edges
     from paper_2406_16260_b200 import engine as en, ops
     kw = dict(height=4, width=4, channels=32, groups=4, n_local=4, n_global=5, blocks=blocks,
-              dtype=torch.float32)
+              dtype=dtype)
     x = ops.tensor_from_seed((F, 4, 4, 32), 0)
     one = en.ClipEngine(en.Layout(en.make_desc(F, 1, 0, **kw)))
     one.init_weights(1)
-    one.x.copy_(dev(x))
+    one.x.copy_(dev(x, dtype))
     en.denoise(2, [one])
     engines = []
     for w in range(N):
         e = en.ClipEngine(en.Layout(en.make_desc(F, N, w, uneven=True, **kw)))
         e.init_weights(1)
-        e.x.copy_(dev(x[e.layout.start:e.layout.start + e.layout.f_clip]))
+        e.x.copy_(dev(x[e.layout.start:e.layout.start + e.layout.f_clip], dtype))
         engines.append(e)
     en.denoise(2, engines)
     got = np.concatenate([to_np(e.x) for e in engines])
     want = to_np(one.x)
-    assert normwise(got, want) <= 1e-5, normwise(got, want)
+    # fp32: summation grouping only; bf16: plus one rounding step per block (2^-8 each)
+    bound = 1e-5 if dtype == torch.float32 else 2.0 ** -7
+    assert normwise(got, want) <= bound, normwise(got, want)
