@@ -349,7 +349,10 @@ __global__ void __launch_bounds__(kTcThreads, LeanLay<NTL, NS>::min_blocks)
     static_assert(NTL % 2 == 0 && NTL <= 8, "K/V rows padded to a multiple of 16, at most 64");
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t p = blockIdx.x, qb = blockIdx.y;
+    // query blocks of one position are adjacent in launch order: their shared K/V rows
+    // (the sampled globals, the overlapping window bands) are re-read from L2, not HBM
+    const uint32_t nqb = (nq + kQBlock - 1) / kQBlock;
+    const uint32_t p = blockIdx.x / nqb, qb = blockIdx.x - p * nqb;
     const uint32_t a0 = qb * kQBlock;
     const uint32_t nqh = min(uint32_t(kQBlock), nq - a0);
     const uint32_t R = tt.kv_count[qb];
@@ -579,7 +582,7 @@ int launch_lean(const void* qkv, uint32_t HW, uint32_t C, uint32_t heads, uint32
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(LeanLay<NTL, NS>::total));
         attr = true;
     }
-    dim3 grid(HW, (nq + kQBlock - 1) / kQBlock);
+    dim3 grid(HW * ((nq + kQBlock - 1) / kQBlock));
     return int(launch_pdl(attention_core_lean_kernel<NTL, NS>, grid, dim3(kTcThreads),
                           LeanLay<NTL, NS>::total, s, static_cast<const __nv_bfloat16*>(qkv), HW, C,
                           heads, nq, q_frame0, tt, scale, bias, static_cast<__nv_bfloat16*>(ctx)));

@@ -38,16 +38,24 @@ constexpr uint32_t kABytes = kBM * kBK * 2;
 constexpr int kStgPitch = 36;  // floats per staged row (32 + 4 pad: conflict-free 16 B access)
 constexpr uint32_t kStgBytes = kEpiWarps * 32 * kStgPitch * 4;  // a 32x32 fp32 block per epilogue warp
 
-template <int BN, bool ST = false>
+constexpr int kResSlots = 3;  // TMA residual ring depth per epilogue warp (32 x 32 bf16 boxes)
+
+// RT: residual in through TMA and output out through TMA (bf16, no statistics): the
+// epilogue needs no transpose block, only two 2 KB store-staging blocks and a residual ring
+// per warp.
+template <int BN, bool ST = false, bool RT = false>
 struct TileCfg {
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+    static constexpr uint32_t kStgWarp = RT ? 4096 : 32 * kStgPitch * 4;  // staging per epilogue warp
+    static constexpr uint32_t kStg = kEpiWarps * kStgWarp;
+    static constexpr uint32_t kRes = RT ? kEpiWarps * kResSlots * 2048 : 0;
     static constexpr int kStages =
-        std::min<int>(8, (227 * 1024 - 1024 - 1024 - kStgBytes) / kStageBytes);
+        std::min<int>(8, (227 * 1024 - 1024 - 1024 - kStg - kRes) / kStageBytes);
     static constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;  // TMEM columns per buffer
     static constexpr uint32_t kTmemCols = 2 * kAccStride;
     static constexpr uint32_t kSmemBytes =
-        kStages * kStageBytes + 1024 /*align*/ + 1024 /*bars*/ + kStgBytes;
+        kStages * kStageBytes + 1024 /*align*/ + 1024 /*bars*/ + kStg + kRes;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -329,10 +337,137 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
     }
 }
 
+// Residual through TMA (RT flavour: bf16 output + bf16 residual, e.g. the O projection,
+// whose epilogue moves two bytes of HBM traffic for every byte of A). Each epilogue warp
+// streams the 32 x 32 residual boxes of its own (tile, chunk) sequence through a private
+// kResSlots-deep ring (64B swizzle, the store staging's layout, so a lane reads its
+// accumulator row's 32 values conflict-free without a transpose). Loads run kResSlots boxes
+// ahead, across tile boundaries, and hold no registers.
+struct ResRing {
+    uint32_t base;   // smem address of slot 0 of this warp's ring
+    uint64_t* bar;   // kResSlots mbarriers
+    uint32_t ncons;  // boxes consumed
+    uint32_t nload;  // boxes issued
+    int lt, lc;      // next box to issue: tile, chunk column
+};
+
+template <int BN>
+__device__ __forceinline__ void res_seek(const GemmParams& p, ResRing& rg, int n_tiles, int num_tiles,
+                                         int half) {
+    // move (lt, lc) to the first box at or after it that lies inside the matrix
+    while (rg.lt < num_tiles) {
+        const int n0 = (rg.lt % n_tiles) * BN;
+        if (rg.lc < BN && n0 + rg.lc < min(p.N, n0 + BN)) return;
+        rg.lt += gridDim.x;
+        rg.lc = 32 * half;
+    }
+}
+
+template <int BN>
+__device__ __forceinline__ void res_issue(const GemmParams& p, const CUtensorMap* rmap, ResRing& rg,
+                                          int n_tiles, int num_tiles, int q, int half) {
+    // lane 0 only
+    if (rg.lt >= num_tiles) return;
+    const uint32_t slot = rg.nload % kResSlots;
+    const int m0 = (rg.lt / n_tiles) * kBM + q * 32, n0 = (rg.lt % n_tiles) * BN;
+    dev::mbar_arrive_expect_tx(&rg.bar[slot], 2048);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(rg.base + slot * 2048),
+        "l"(reinterpret_cast<uint64_t>(rmap)), "r"(n0 + rg.lc), "r"(m0), "r"(dev::smem_u32(&rg.bar[slot]))
+        : "memory");
+    ++rg.nload;
+    rg.lc += 64;
+    res_seek<BN>(p, rg, n_tiles, num_tiles, half);
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_tma_res(const GemmParams& p, const CUtensorMap* omap,
+                                                      const CUtensorMap* rmap, uint32_t tmem_acc, int q,
+                                                      int lane, uint32_t stg, int m0, int n0, int half,
+                                                      uint32_t& nstore, ResRing& rg, int n_tiles,
+                                                      int num_tiles) {
+    static_assert(BN % 32 == 0, "whole 32-column chunks");
+    const int n_lim = min(p.N, n0 + BN);
+    const bool store = !(p.flags & kGemmFlagNoStore);
+    const uint32_t sw = (lane >> 1) & 3;
+#pragma unroll 1
+    for (int c = 32 * half; c < BN; c += 64) {
+        const int nb = n0 + c;
+        if (nb >= n_lim) break;  // warp-uniform; the ring holds only in-range boxes
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(tmem_acc + (uint32_t(q * 32) << 16) + c, r);
+        // this chunk's residual box
+        const uint32_t slot = rg.ncons % kResSlots;
+        dev::mbar_wait(&rg.bar[slot], (rg.ncons / kResSlots) & 1);
+        uint32_t rw[16];
+        {
+            const uint32_t row = rg.base + slot * 2048 + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float4 v = lds128(row + ((j ^ sw) << 4));
+                rw[4 * j] = __float_as_uint(v.x);
+                rw[4 * j + 1] = __float_as_uint(v.y);
+                rw[4 * j + 2] = __float_as_uint(v.z);
+                rw[4 * j + 3] = __float_as_uint(v.w);
+            }
+        }
+        ++rg.ncons;
+        __syncwarp();
+        if (lane == 0) {  // the slot is read: refill it with the box kResSlots ahead
+            dev::fence_proxy_async_smem();
+            res_issue<BN>(p, rmap, rg, n_tiles, num_tiles, q, half);
+        }
+        dev::tmem_wait_ld();
+        float y[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            float4 b = make_float4(0.f, 0.f, 0.f, 0.f), sc = b;
+            const bool okv = nb + 4 * v < n_lim;  // N % 8 == 0: a float4 is wholly in or out
+            if (p.bias && okv) b = __ldg(reinterpret_cast<const float4*>(p.bias + nb) + v);
+            if (p.res_scale && okv) sc = __ldg(reinterpret_cast<const float4*>(p.res_scale + nb) + v);
+            const float bb[4] = {b.x, b.y, b.z, b.w}, ss[4] = {sc.x, sc.y, sc.z, sc.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = 4 * v + e;
+                const uint32_t w = rw[k >> 1];
+                const float rv = __uint_as_float((k & 1) ? (w & 0xFFFF0000u) : (w << 16));
+                const float a = __uint_as_float(r[k]);
+                // the transposed epilogue's arithmetic: (acc + res*scale) + bias
+                const float cur = p.res_scale ? fmaf(rv, ss[e], a) : a + rv;
+                y[k] = cur + bb[e];
+            }
+        }
+        if (!store) continue;
+        uint32_t w[16];
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+            w[h] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        const uint32_t buf = stg + (nstore & 1) * 2048;
+        if (nstore >= 2) {
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+        }
+        const uint32_t row = buf + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sts128(row + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+        dev::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(omap, buf, nb, m0);
+            dev::bulk_commit();
+        }
+        ++nstore;
+    }
+}
+
 template <int BN, bool OBF, bool RES, bool ST, bool TMAO = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
-    using Cfg = TileCfg<BN, ST>;
+    constexpr bool RT = TMAO && RES;  // residual through TMA (the RT flavour)
+    using Cfg = TileCfg<BN, ST, RT>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -344,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + S;   // [2]
     uint64_t* tempty = tfull + 2;  // [2]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rbar = full + 32;    // RT: [kEpiWarps][kResSlots] residual ring barriers
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -369,6 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             dev::mbar_init(&tfull[i], 1);
             dev::mbar_init(&tempty[i], kEpiWarps);
         }
+        if (RT)
+            for (int i = 0; i < kEpiWarps * kResSlots; ++i) dev::mbar_init(&rbar[i], 1);
         dev::fence_barrier_init();
     }
     if (warp == 2) dev::tmem_alloc(tmem_holder, Cfg::kTmemCols);
@@ -437,10 +575,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;            // TMEM lane quadrant this warp may access
         const int half = (warp - 4) >> 2;  // which alternate 32-column chunks it takes
         const uint32_t stg =
-            dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
+            dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * Cfg::kStgWarp;
         uint32_t local = 0, nstore = 0;
         EpiRes<OBF> rr;
         EpiCol col;
+        ResRing rg;
+        if (RT) {
+            rg.base = dev::smem_u32(smem + S * Cfg::kStageBytes + 1024 + Cfg::kStg) +
+                      (warp - 4) * (kResSlots * 2048);
+            rg.bar = rbar + (warp - 4) * kResSlots;
+            rg.ncons = rg.nload = 0;
+            rg.lt = blockIdx.x;
+            rg.lc = 32 * half;
+            res_seek<BN>(p, rg, n_tiles, num_tiles, half);
+            if (lane == 0) {
+                dev::tma_prefetch_desc(&maps.res);
+                for (int i = 0; i < kResSlots; ++i) res_issue<BN>(p, &maps.res, rg, n_tiles, num_tiles, q, half);
+            }
+        }
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
             const uint32_t acc = local & 1;
             const int m0 = (tile / n_tiles) * kBM + q * 32, n0 = (tile % n_tiles) * BN;
@@ -454,7 +606,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
-            if constexpr (TMAO)
+            if constexpr (RT)
+                epilogue_tile_tma_res<BN>(p, &maps.out, &maps.res, tmem_base + acc * Cfg::kAccStride, q,
+                                          lane, stg, m0, n0, half, nstore, rg, n_tiles, num_tiles);
+            else if constexpr (TMAO)
                 epilogue_tile_tma<BN>(p, &maps.out, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
                                       m0, n0, half, nstore);
             else
@@ -664,7 +819,7 @@ int g_num_sms = 0;
 
 template <int BN, bool OBF, bool RES, bool ST = false, bool TMAO = false>
 int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
-    using Cfg = TileCfg<BN, ST>;
+    using Cfg = TileCfg<BN, ST, TMAO && RES>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>,
@@ -696,6 +851,10 @@ int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
     }
     if (p.out_bf16 && !res && (p.flags & kGemmFlagTmaOut))
         return launch_cfg<BN, true, false, false, true>(maps, p, stream);
+    if constexpr (BN % 32 == 0) {
+        if (p.out_bf16 && res && (p.flags & kGemmFlagTmaRes))
+            return launch_cfg<BN, true, true, false, true>(maps, p, stream);
+    }
     if (p.out_bf16) return res ? launch_cfg<BN, true, true>(maps, p, stream)
                                : launch_cfg<BN, true, false>(maps, p, stream);
     return res ? launch_cfg<BN, false, true>(maps, p, stream)

@@ -49,11 +49,14 @@ struct GemmParams {
 
 constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic
 constexpr int32_t kGemmFlagTmaOut = 1 << 8;  // bf16 output leaves through TMA stores (maps.out)
+// bf16 output + bf16 residual both through TMA (maps.out, maps.res); block_n % 32 == 0
+constexpr int32_t kGemmFlagTmaRes = 1 << 9;
 
 struct GemmMaps {
     CUtensorMap a[2];
     CUtensorMap b[2];
-    CUtensorMap out;  // [M, N] bf16, box 32 x 32, 64B swizzle (with kGemmFlagTmaOut)
+    CUtensorMap out;  // [M, N] bf16, box 32 x 32, 64B swizzle (with kGemmFlagTmaOut / TmaRes)
+    CUtensorMap res;  // [M, N] bf16 residual, same box and swizzle (with kGemmFlagTmaRes)
 };
 
 // Host side: encode a 2D bf16 K-major tensor map over [rows, cols] with row stride

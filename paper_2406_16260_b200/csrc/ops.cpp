@@ -96,9 +96,20 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
     const bool tma_out = ep.out_bf16 && !ep.res && !ep.colpart && !split && !pair &&
                          reinterpret_cast<uintptr_t>(ep.out) % 16 == 0 && ep.out_ld % 8 == 0 &&
                          getenv("VINF_GEMM_NO_TMA_OUT") == nullptr;
-    if (tma_out)
+    // bf16 output with a bf16 residual and no statistics (the O projection): residual in and
+    // output out through TMA (the RT epilogue)
+    static const bool no_tma_res = getenv("VINF_GEMM_NO_TMA_RES") != nullptr;
+    const bool tma_res = ep.out_bf16 && ep.res && ep.res_bf16 && !ep.colpart && !split && !pair &&
+                         bn % 32 == 0 && reinterpret_cast<uintptr_t>(ep.out) % 16 == 0 &&
+                         ep.out_ld % 8 == 0 && reinterpret_cast<uintptr_t>(ep.res) % 16 == 0 &&
+                         ep.res_ld % 8 == 0 && !no_tma_res;
+    if (tma_out || tma_res)
         cuda_check(make_tmap_out_bf16(&maps.out, ep.out, uint64_t(M), uint64_t(N), uint64_t(ep.out_ld)),
                    "tmap out");
+    if (tma_res)
+        cuda_check(make_tmap_out_bf16(&maps.res, const_cast<void*>(ep.res), uint64_t(M), uint64_t(N),
+                                      uint64_t(ep.res_ld)),
+                   "tmap residual");
     std::vector<GemmSeg> segs;
     for (size_t i = 0; i < a_rows.size(); ++i) {
         const int32_t ar = int32_t(a_rows[i]), br = int32_t(b_rows[i]);
@@ -127,7 +138,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         p.out = ep.out;
         p.out_ld = ep.out_ld;
         p.out_bf16 = ep.out_bf16;
-        p.flags = g_gemm_debug_flags | (tma_out ? kGemmFlagTmaOut : 0);
+        p.flags = g_gemm_debug_flags | (tma_out ? kGemmFlagTmaOut : 0) | (tma_res ? kGemmFlagTmaRes : 0);
         if (c0 + kGemmMaxSeg >= segs.size()) p.colpart = ep.colpart;  // final output only
         cuda_check(gemm_tc_launch(maps, p, bn, s, pair), "gemm_tc_launch");
     }
