@@ -214,7 +214,7 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     }
     ++launches;
     Span span(this, "gn_stats", s);
-    cuda_check(launch_colpart_to_groups(colpart, uint32_t((rows + 31) / 32), C, L.d.groups,
+    cuda_check(launch_colpart_to_groups(colpart, uint32_t(gemm_colpart_rows(int64_t(rows), int(C))), C, L.d.groups,
                                         at<double>(L.off_sums), at<double>(L.off_scratch), s),
                "gn fold");
     launches += 1;

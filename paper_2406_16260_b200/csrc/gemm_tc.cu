@@ -141,10 +141,19 @@ __device__ __forceinline__ void epi_load_col(const GemmParams& p, EpiCol& col, i
     }
 }
 
+// Column statistics accumulated per (CTA, epilogue warp) over all of the CTA's tiles, used
+// when every CTA keeps one column tile (gridDim.x % n_tiles == 0): after the butterfly, lane
+// l keeps column (l & 3) * 8 + (l >> 2) of each of its chunks (<= 4 per tile), in a fixed
+// order, so the partial rows drop from M / 32 to 4 per CTA (the fold reads 13x less at the
+// block's shapes) and stay deterministic.
+struct CtaStats {
+    float s[4], q[4];
+};
+
 template <int BN, bool OBF, bool RES, bool ST>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int q, int lane,
                                               uint32_t stg, int m0, int n0, int half,
-                                              EpiRes<OBF>& rr, EpiCol& col) {
+                                              EpiRes<OBF>& rr, EpiCol& col, CtaStats* cst = nullptr) {
     using T = typename std::conditional<OBF, __nv_bfloat16, float>::type;
     const int tr = lane >> 2;        // transposed: rows tr + 8i
     const int tc = (lane & 3) * 8;   // transposed: first of 8 columns
@@ -242,7 +251,23 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
                 cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 8);
                 cq[k] += __shfl_xor_sync(0xffffffffu, cq[k], 16);
             }
-            if (tr == 0 && n < n_lim && m0 < p.M) {  // this warp owns (row block, 8 columns)
+            if (cst) {
+                const int kk = lane >> 2;
+                float ss = cs[0], sq = cq[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k)
+                    if (kk == k) {
+                        ss = cs[k];
+                        sq = cq[k];
+                    }
+                const int jc = (c - 32 * half) >> 6;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j == jc) {
+                        cst->s[j] += ss;
+                        cst->q[j] += sq;
+                    }
+            } else if (tr == 0 && n < n_lim && m0 < p.M) {  // this warp owns (row block, 8 columns)
                 float* part = p.colpart + int64_t(m0 >> 5) * 2 * p.N + n;
                 *reinterpret_cast<float4*>(part) = make_float4(cs[0], cs[1], cs[2], cs[3]);
                 *reinterpret_cast<float4*>(part + 4) = make_float4(cs[4], cs[5], cs[6], cs[7]);
@@ -580,6 +605,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         EpiRes<OBF> rr;
         EpiCol col;
         ResRing rg;
+        // ST: per-CTA column statistics when this CTA's column tile never changes
+        const bool cta_stats = ST && (gridDim.x % n_tiles) == 0;
+        CtaStats cst;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cst.s[j] = cst.q[j] = 0.f;
         if (RT) {
             rg.base = dev::smem_u32(smem + S * Cfg::kStageBytes + 1024 + Cfg::kStg) +
                       (warp - 4) * (kResSlots * 2048);
@@ -614,12 +644,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       m0, n0, half, nstore);
             else
                 epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0,
-                                                n0, half, rr, col);
+                                                n0, half, rr, col, cta_stats ? &cst : nullptr);
             dev::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         if (TMAO && lane == 0) bulk_wait_read<0>();  // staging must outlive the stores' reads
+        if (cta_stats && !(p.flags & kGemmFlagNoStore)) {
+            // partial row (CTA group, quadrant): the n_tiles CTAs of a group cover every column once
+            const int n0 = (blockIdx.x % n_tiles) * BN, n_lim = min(p.N, n0 + BN);
+            float* part = p.colpart + (int64_t(blockIdx.x / n_tiles) * 4 + q) * 2 * p.N;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = n0 + 32 * half + 64 * j + (lane & 3) * 8 + (lane >> 2);
+                if (32 * half + 64 * j < BN && n < n_lim) {
+                    part[n] = cst.s[j];
+                    part[p.N + n] = cst.q[j];
+                }
+            }
+        }
     }
 
     dev::tc_fence_before();
@@ -927,6 +970,21 @@ int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t col
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
+int gemm_colpart_rows(int64_t M, int N) {
+    const int bn = gemm_pick_block_n(N);
+    const int64_t rb = (M + 31) / 32;
+    if (gemm_use_pair(int(M), N, bn)) return int(rb);
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    const int64_t n_tiles = (N + bn - 1) / bn, tiles = n_tiles * ((M + kBM - 1) / kBM);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, g_num_sms));
+    return int(grid % n_tiles == 0 ? grid / n_tiles * 4 : rb);
 }
 
 int gemm_pick_block_n(int N) {

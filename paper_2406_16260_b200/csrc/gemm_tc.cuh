@@ -41,9 +41,11 @@ struct GemmParams {
     int32_t out_bf16;
     int32_t flags;  // kGemmFlag* (diagnostics)
     // Optional per-column statistics of the stored output (GroupNorm fused into the
-    // conv epilogue), one partial per 32-row block, each written exactly once (no atomics,
-    // deterministic): colpart[(rb*2 + 0)*N + n] = sum over the block's rows of out[m,n],
-    // colpart[(rb*2 + 1)*N + n] = sum of squares. fp32 [ceil(M/32)][2][N].
+    // conv epilogue), partial rows each written exactly once (no atomics, deterministic):
+    // colpart[(r*2 + 0)*N + n] = sum over the rows of partial r of out[m,n],
+    // colpart[(r*2 + 1)*N + n] = sum of squares; fp32 [gemm_colpart_rows(M, N)][2][N].
+    // Partial r is one (CTA group, TMEM quadrant) when every CTA keeps one column tile
+    // (4 * gridDim / n_tiles rows), else one 32-row block (ceil(M / 32) rows).
     float* colpart;
 };
 
@@ -75,5 +77,9 @@ bool gemm_use_pair(int M, int N, int block_n);
 
 // Largest supported N tile for a given N (used to build B tensor maps).
 int gemm_pick_block_n(int N);
+
+// Partial rows the fused column statistics of an M x N GEMM occupy (see GemmParams::colpart);
+// never more than 4 * ceil(M / 128), the size to allocate.
+int gemm_colpart_rows(int64_t M, int N);
 
 }  // namespace vinf

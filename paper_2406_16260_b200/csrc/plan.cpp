@@ -303,7 +303,8 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     scratch_elems = std::max<uint64_t>(uint64_t(kScratchBlocks) * d.groups,
                                        uint64_t(256) * 2 * d.channels);  // colpart segments
     off_scratch = take(sizeof(double) * scratch_elems);
-    off_colstats = take(sizeof(float) * 2 * d.channels * ((uint64_t(f_clip) * hw + 31) / 32));
+    // column-statistic partial rows: 4 per 128-row tile bounds both layouts (gemm_colpart_rows)
+    off_colstats = take(sizeof(float) * 2 * d.channels * 4 * ((uint64_t(f_clip) * hw + 127) / 128));
     for (int b = 0; b < 4; ++b) off_tok[b] = take(tok[b].blob_bytes());
     total = off;
 
