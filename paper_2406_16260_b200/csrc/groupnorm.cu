@@ -507,10 +507,47 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// Few partial rows (the conv GEMM's per-CTA statistics: 4 rows per CTA group): one CTA per
+// (statistic, group) reads the group's whole column block, each thread a fixed strided set of
+// (row, column) entries in f64, then a fixed tree. No tickets, one dependent step.
+constexpr uint32_t kDirectThreads = 256;
+constexpr uint32_t kDirectMaxEntries = 16384;  // rows x group width handled by one CTA
+
+__global__ void __launch_bounds__(kDirectThreads)
+    colpart_fold_direct_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C,
+                               uint32_t groups, double* __restrict__ sums) {
+    dev::pdl_wait();
+    dev::pdl_trigger();
+    __shared__ double red[kDirectThreads];
+    const uint32_t which = blockIdx.x / groups, g = blockIdx.x % groups, gs = C / groups;
+    const float* base = part + uint64_t(which) * C + uint64_t(g) * gs;
+    const uint32_t n = blocks * gs;
+    double a0 = 0.0, a1 = 0.0;
+    uint32_t i = threadIdx.x;
+    for (; i + kDirectThreads < n; i += 2 * kDirectThreads) {
+        const uint32_t r0 = i / gs, r1 = (i + kDirectThreads) / gs;
+        a0 += double(base[uint64_t(r0) * 2 * C + (i - r0 * gs)]);
+        a1 += double(base[uint64_t(r1) * 2 * C + (i + kDirectThreads - r1 * gs)]);
+    }
+    if (i < n) {
+        const uint32_t r0 = i / gs;
+        a0 += double(base[uint64_t(r0) * 2 * C + (i - r0 * gs)]);
+    }
+    red[threadIdx.x] = a0 + a1;
+    __syncthreads();
+    for (uint32_t w = kDirectThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[which * groups + g] = red[0];
+}
 
 int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,
                              double* sums, double* scratch, cudaStream_t s) {
     if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
+    if (uint64_t(blocks) * (C / groups) <= kDirectMaxEntries)
+        return int(launch_pdl(colpart_fold_direct_kernel, dim3(2 * groups), dim3(kDirectThreads), 0, s,
+                              part, blocks, C, groups, sums));
     // scratch: [2G][kFoldSegs] doubles of segment partials, then 2G uint32 tickets (zero
     // at rest: the workspace is zeroed at creation and every fold resets its tickets)
     double* seg = scratch;
