@@ -877,8 +877,12 @@ int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
     }
-    const int tiles = ((p.N + BN - 1) / BN) * ((p.M + kBM - 1) / kBM);
-    const int grid = std::max(1, std::min(tiles, g_num_sms));
+    const int n_tiles = (p.N + BN - 1) / BN;
+    const int tiles = n_tiles * ((p.M + kBM - 1) / kBM);
+    int grid = std::max(1, std::min(tiles, g_num_sms));
+    // column statistics: a grid that is a multiple of the column tiles keeps every CTA on
+    // one column tile (per-CTA statistics, gemm_colpart_rows)
+    if (ST && grid > n_tiles) grid -= grid % n_tiles;
     return int(launch_pdl(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>, dim3(grid), dim3(kThreads),
                           Cfg::kSmemBytes, stream, maps, p));
 }
@@ -972,6 +976,11 @@ int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t col
     return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 int gemm_colpart_rows(int64_t M, int N) {
     const int bn = gemm_pick_block_n(N);
     const int64_t rb = (M + 31) / 32;
@@ -983,12 +992,25 @@ int gemm_colpart_rows(int64_t M, int N) {
         if (g_num_sms <= 0) g_num_sms = 148;
     }
     const int64_t n_tiles = (N + bn - 1) / bn, tiles = n_tiles * ((M + kBM - 1) / kBM);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, g_num_sms));
+    int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, g_num_sms));
+    if (grid > n_tiles) grid -= grid % n_tiles;  // as launch_cfg does for the statistics kernels
     return int(grid % n_tiles == 0 ? grid / n_tiles * 4 : rb);
 }
 
 int gemm_pick_block_n(int N) {
-    static const int cands[] = {256, 240, 192, 160, 128, 64};
+    // Wide tiles feed the tensor pipe best (more MMA work per operand byte and per
+    // instruction: at M = 61440, K = 640 the main loop runs at ~1550 TFLOP/s with N = 240
+    // against ~1200 with N = 160), so take the widest tile that pads N by less than 1/16;
+    // otherwise the least padding. (N = 640: 224; N = 1920: 240; N = 1280: 256; N = 320: 160.)
+    static const int cands[] = {256, 240, 224, 192, 160, 128, 64};
+    static const int forced = env_int("VINF_GEMM_BN", 0);  // diagnostics
+    for (int bn : cands)
+        if (bn == forced) return bn;
+    for (int bn : cands) {
+        if (bn < 192) break;
+        const long padded = long((N + bn - 1) / bn) * bn;
+        if (16 * (padded - N) < padded) return bn;
+    }
     int best = 64;
     long best_waste = -1;
     for (int bn : cands) {
@@ -1025,6 +1047,7 @@ int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaS
         switch (block_n) {
             case 256: return launch_pair<256>(maps, p, stream);
             case 240: return launch_pair<240>(maps, p, stream);
+            case 224: return launch_pair<224>(maps, p, stream);
             case 192: return launch_pair<192>(maps, p, stream);
             case 160: return launch_pair<160>(maps, p, stream);
             case 128: return launch_pair<128>(maps, p, stream);
@@ -1035,6 +1058,7 @@ int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaS
     switch (block_n) {
         case 256: return launch<256>(maps, p, stream);
         case 240: return launch<240>(maps, p, stream);
+        case 224: return launch<224>(maps, p, stream);
         case 192: return launch<192>(maps, p, stream);
         case 160: return launch<160>(maps, p, stream);
         case 128: return launch<128>(maps, p, stream);
