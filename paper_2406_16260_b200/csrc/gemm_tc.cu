@@ -374,23 +374,26 @@ struct ResRing {
     uint32_t ncons;  // boxes consumed
     uint32_t nload;  // boxes issued
     int lt, lc;      // next box to issue: tile, chunk column
+    uint32_t lloc;   // lt's index among this CTA's tiles (its parity swaps the warp's chunks)
+    int h0;          // the warp's chunk parity on its even tiles
 };
 
 template <int BN>
-__device__ __forceinline__ void res_seek(const GemmParams& p, ResRing& rg, int n_tiles, int num_tiles,
-                                         int half) {
-    // move (lt, lc) to the first box at or after it that lies inside the matrix
+__device__ __forceinline__ void res_seek(const GemmParams& p, ResRing& rg, int n_tiles, int num_tiles) {
+    // move (lt, lc) to the first box at or after it that lies inside the matrix (chunk parity
+    // h0 on the warp's even tiles, swapped on odd ones, as the epilogue takes them)
     while (rg.lt < num_tiles) {
         const int n0 = (rg.lt % n_tiles) * BN;
         if (rg.lc < BN && n0 + rg.lc < min(p.N, n0 + BN)) return;
         rg.lt += gridDim.x;
-        rg.lc = 32 * half;
+        ++rg.lloc;
+        rg.lc = 32 * (rg.h0 ^ int(rg.lloc & 1));
     }
 }
 
 template <int BN>
 __device__ __forceinline__ void res_issue(const GemmParams& p, const CUtensorMap* rmap, ResRing& rg,
-                                          int n_tiles, int num_tiles, int q, int half) {
+                                          int n_tiles, int num_tiles, int q) {
     // lane 0 only
     if (rg.lt >= num_tiles) return;
     const uint32_t slot = rg.nload % kResSlots;
@@ -403,7 +406,7 @@ __device__ __forceinline__ void res_issue(const GemmParams& p, const CUtensorMap
         : "memory");
     ++rg.nload;
     rg.lc += 64;
-    res_seek<BN>(p, rg, n_tiles, num_tiles, half);
+    res_seek<BN>(p, rg, n_tiles, num_tiles);
 }
 
 template <int BN>
@@ -441,7 +444,7 @@ __device__ __forceinline__ void epilogue_tile_tma_res(const GemmParams& p, const
         __syncwarp();
         if (lane == 0) {  // the slot is read: refill it with the box kResSlots ahead
             dev::fence_proxy_async_smem();
-            res_issue<BN>(p, rmap, rg, n_tiles, num_tiles, q, half);
+            res_issue<BN>(p, rmap, rg, n_tiles, num_tiles, q);
         }
         dev::tmem_wait_ld();
         float y[32];
@@ -616,11 +619,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             rg.bar = rbar + (warp - 4) * kResSlots;
             rg.ncons = rg.nload = 0;
             rg.lt = blockIdx.x;
+            rg.lloc = 0;
+            rg.h0 = half;
             rg.lc = 32 * half;
-            res_seek<BN>(p, rg, n_tiles, num_tiles, half);
+            res_seek<BN>(p, rg, n_tiles, num_tiles);
             if (lane == 0) {
                 dev::tma_prefetch_desc(&maps.res);
-                for (int i = 0; i < kResSlots; ++i) res_issue<BN>(p, &maps.res, rg, n_tiles, num_tiles, q, half);
+                for (int i = 0; i < kResSlots; ++i) res_issue<BN>(p, &maps.res, rg, n_tiles, num_tiles, q);
             }
         }
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -636,12 +641,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
             dev::tc_fence_after();
+            // TMA epilogues: the two warps of a quadrant swap chunk parity every tile, so an odd
+            // chunk count (BN = 160: 3 + 2, 224: 4 + 3) balances over two tiles (the accumulator
+            // is double-buffered: the lighter warp runs ahead into the next tile)
+            const int hsw = half ^ int(local & 1);
             if constexpr (RT)
                 epilogue_tile_tma_res<BN>(p, &maps.out, &maps.res, tmem_base + acc * Cfg::kAccStride, q,
-                                          lane, stg, m0, n0, half, nstore, rg, n_tiles, num_tiles);
+                                          lane, stg, m0, n0, hsw, nstore, rg, n_tiles, num_tiles);
             else if constexpr (TMAO)
                 epilogue_tile_tma<BN>(p, &maps.out, tmem_base + acc * Cfg::kAccStride, q, lane, stg,
-                                      m0, n0, half, nstore);
+                                      m0, n0, hsw, nstore);
             else
                 epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0,
                                                 n0, half, rr, col, cta_stats ? &cst : nullptr);

@@ -126,6 +126,43 @@ __global__ void __launch_bounds__(256) tma_chunks(const __grid_constant__ CUtens
     if (acc == 123.f) sink[p] = acc;
 }
 
+// E: frame-major whole rows (3840 B per (frame, position)) by cp.async.bulk, one thread
+// issuing; persistent CTAs with two position buffers (the next position loads while the
+// current one is consumed).
+__global__ void __launch_bounds__(256) rows_bulk(const uint16_t* q, float* sink) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    constexpr uint32_t kRow = C3 * 2, kPitch = kRow + 16, kBuf = F * kPitch;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * kBuf);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int p, int b) {
+        const uint32_t bar = su32(&bars[b]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(F * kRow) : "memory");
+        for (int f = 0; f < F; ++f) {
+            const uint16_t* src = q + (uint64_t(f) * HW + p) * C3;
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su32(sm + b * kBuf + f * kPitch)), "l"(src), "r"(kRow), "r"(bar) : "memory");
+        }
+    };
+    float acc = 0.f;
+    int it = 0;
+    if (tid == 0 && blockIdx.x < HW) issue(blockIdx.x, 0);
+    for (int p = blockIdx.x; p < HW; p += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (tid == 0 && p + int(gridDim.x) < HW) issue(p + gridDim.x, b ^ 1);
+        const uint32_t bar = su32(&bars[b]);
+        const uint32_t par = (it >> 1) & 1;
+        asm volatile("{\n.reg .pred P1;\nW: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(bar), "r"(par) : "memory");
+        acc += reinterpret_cast<const float*>(sm + b * kBuf)[tid];
+        __syncthreads();
+    }
+    if (acc == 123.f) sink[0] = acc;
+}
+
 int main() {
     uint16_t* q;
     float* sink;
@@ -157,7 +194,11 @@ int main() {
         if (r != CUDA_SUCCESS) printf("tensor map encode failed %d\n", int(r));
     }
     cudaFuncSetAttribute(tma_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * 8192 + 1024);
-    for (int v = 0; v < 4; ++v) {
+    const int rows_smem = 2 * F * (C3 * 2 + 16) + 64;
+    cudaFuncSetAttribute(rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, rows_smem);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    for (int v = 0; v < 5; ++v) {
         float best = 1e9;
         for (int it = 0; it < 10; ++it) {
             cudaMemset(flush, it, 512 << 20);
@@ -166,13 +207,14 @@ int main() {
             if (v == 1) chunks<true><<<HW, 256, NS * 8192>>>(q, sink);
             if (v == 2) whole<<<HW, 256, 4 * 16384>>>(q, sink);
             if (v == 3) tma_chunks<<<HW, 256, NS * 8192 + 1024>>>(map, sink);
+            if (v == 4) rows_bulk<<<nsm, 256, rows_smem>>>(q, sink);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms;
             cudaEventElapsedTime(&ms, a, b);
             if (ms < best) best = ms;
         }
-        printf("%s: %.1f us  %.0f GB/s  (%s)\n", v == 0 ? "A frame-major chunks" : v == 1 ? "B position-major chunks" : v == 2 ? "C position-major whole" : "D frame-major TMA boxes",
+        printf("%s: %.1f us  %.0f GB/s  (%s)\n", v == 0 ? "A frame-major chunks" : v == 1 ? "B position-major chunks" : v == 2 ? "C position-major whole" : v == 3 ? "D frame-major TMA boxes" : "E frame-major whole rows, bulk, 2 buffers/SM",
                best * 1000, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
