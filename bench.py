@@ -543,7 +543,26 @@ def run_vc2(args):
     return 0
 
 
+def _stdout_for_result_only() -> None:
+    """The driver reads ONE JSON line from stdout. Libraries may print there too (NCCL
+    prints its version line to stdout when NCCL_DEBUG=WARN/VERSION), so route the process's
+    fd 1 to stderr and keep a private handle on the real stdout for the result line."""
+    global print
+    real = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    builtin_print = print
+
+    def _print(*a, **k):
+        if "file" not in k:
+            k["file"] = real
+        builtin_print(*a, **k)
+
+    print = _print  # noqa: A001
+
+
 def main():
+    _stdout_for_result_only()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)

@@ -4,13 +4,14 @@ import json
 import sys
 
 GROUPS = {
-    "gemm_tc_kernel<160, 1, 1, 1, 0>": "conv_gemm",
-    "colpart_fold_kernel": "gn_stats",
+    # (bf16 out, residual, statistics, TMA epilogue) flavours of gemm_tc_kernel<BN, ...>
+    ", 1, 1, 1, 0>": "conv_gemm",
+    "colpart_fold": "gn_stats",
     "group_fold_kernel": "gn_fold",
     "group_apply_bf16_kernel": "gn_apply",
-    "gemm_tc_kernel<240, 1, 0, 0, 1>": "qkv_gemm",
+    ", 1, 0, 0, 1>": "qkv_gemm",
     "attention_core_lean_kernel": "attn_core",
-    "gemm_tc_kernel<160, 1, 1, 0, 0>": "o_gemm",
+    ", 1, 1, 0, 1>": "o_gemm",
     "stub_bf16_kernel": "stub",
 }
 summary, source = sys.argv[1], sys.argv[2]
