@@ -167,6 +167,31 @@ def test_engine_production_channels(mods, oracle, C):
         assert torch.equal(e.y, y1)
 
 
+@pytest.mark.parametrize("H,W,C,groups", [(40, 41, 64, 8), (12, 23, 640, 32)])
+def test_engine_many_tiles_per_cta(mods, oracle, H, W, C, groups):
+    # enough rows that persistent GEMM CTAs run several tiles (the TMA residual ring crosses
+    # tile boundaries, the quadrant warps swap chunk parity on odd tiles, the conv's column
+    # statistics accumulate per CTA), with a partial last row tile and, at C = 640, a
+    # partial last column tile (N tile 224); bf16 engine vs the CPU oracle, and repeatable
+    _, _, en, _ = mods
+    F = 24
+    kw = dict(frames=F, height=H, width=W, channels=C, groups=groups, n_local=16, n_global=16)
+    x = oracle.tensor_from_seed((F, H, W, C), 4)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    e = _engine(mods, torch.bfloat16, **kw)
+    e.init_weights(1)
+    xd = dev(x, torch.bfloat16)
+    e.x.copy_(xd)
+    en.forward(700.0, [e])
+    y1 = e.y.clone()
+    want = oracle.block_forward(to_np(xd), bp, 700.0, groups)
+    assert normwise(to_np(y1), want) <= TOL_BF16, normwise(to_np(y1), want)
+    e.x.copy_(xd)
+    en.forward(700.0, [e])
+    torch.cuda.synchronize()
+    assert torch.equal(e.y, y1)
+
+
 def test_engine_set_block_equals_init_weights(mods, oracle):
     _, _, en, _ = mods
     bp = oracle.build_block(64, 3, weight_seed=5)
