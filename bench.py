@@ -48,6 +48,27 @@ def parse():
     return ap.parse_args()
 
 
+def kernel_floor_us(frames: int, h: int, w: int, c: int, es: int, hbm_gbs: float, tf: float) -> dict:
+    """Roofline floor of one block step, kernel by kernel (bf16 GroupNorm-folded pipeline):
+    each kernel takes at least max(its tensor work / peak, its algorithmic HBM bytes / peak),
+    with T = frames*H*W*C*s the bytes of one clip-sized tensor:
+      stub  reads + writes the clip                    2 T              (HBM)
+      conv  2*H*W*3C^2 flop per frame; A, residual, out 3 T
+      QKV   2*H*W*3C^2 flop per frame; in, Q/K/V out   4 T
+      attn  Q/K/V in, ctx out                          4 T              (HBM)
+      O     2*H*W*C^2 flop per frame; ctx, residual, out 3 T
+    GroupNorm statistics and folding are not counted (latency-bound, a few us per step)."""
+    t = frames * h * w * c * es
+    m = frames * h * w
+    parts = {"stub": (0.0, 2 * t), "conv_gemm": (6.0 * m * c * c, 3 * t),
+             "qkv_gemm": (6.0 * m * c * c, 4 * t), "attn_core": (0.0, 4 * t),
+             "o_gemm": (2.0 * m * c * c, 3 * t)}
+    out = {}
+    for k, (fl, by) in parts.items():
+        out[k] = max(fl / (tf * 1e12), by / (hbm_gbs * 1e9)) * 1e6
+    return out
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -400,9 +421,14 @@ def run_ours(args):
             pass
     # whole-block roofline: all tensor work of the step at the sustained tensor peak
     flops_step = sum(work[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm"))
+    floor = kernel_floor_us(fc, H, W, C, es, hbm, tf_sus)
     block_roof = {"flops_per_step": flops_step,
                   "achieved_tflops": flops_step / (ms_per_step / 1000.0) / 1e12,
-                  "frac_of_sustained": flops_step / (ms_per_step / 1000.0) / 1e12 / tf_sus}
+                  "frac_of_sustained": flops_step / (ms_per_step / 1000.0) / 1e12 / tf_sus,
+                  # per-kernel floor: each kernel at max(tensor time, HBM time) (kernel_floor_us)
+                  "kernel_floor_us": sum(floor.values()),
+                  "frac_of_kernel_floor": sum(floor.values()) / (ms_per_step * 1000.0),
+                  "kernel_floor_parts_us": floor}
     for k, v in per_kernel.items():
         w_, bound = work.get(k, (None, None))
         if w_:
@@ -517,10 +543,13 @@ def run_vc2(args):
                 for li in range(len(engines))]
     hbm, tf_burst, tf_sus, src = peaks()
     flops = [14.0 * fc * h * w * c * c for (c, h, w) in VC2_LEVELS]  # conv 6MC^2 + qkv 6MC^2 + o 2MC^2
+    es = 2 if args.dtype == "bf16" else 4
+    floors = [sum(kernel_floor_us(fc, h, w, c, es, hbm, tf_sus).values()) for (c, h, w) in VC2_LEVELS]
     levels = [{"channels": c, "height": h, "width": w, "ms": m,
                "achieved_tflops": fl / (m / 1000.0) / 1e12,
-               "frac_of_sustained": fl / (m / 1000.0) / 1e12 / tf_sus}
-              for (c, h, w), m, fl in zip(VC2_LEVELS, level_ms, flops)]
+               "frac_of_sustained": fl / (m / 1000.0) / 1e12 / tf_sus,
+               "kernel_floor_ms": fu / 1000.0, "frac_of_kernel_floor": fu / 1000.0 / m}
+              for (c, h, w), m, fl, fu in zip(VC2_LEVELS, level_ms, flops, floors)]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -534,7 +563,9 @@ def run_vc2(args):
                            "clips": "uneven (floor(w*F/N) split)" if F % n else "even"},
                 "block_roofline": {"flops_per_step": sum(flops),
                                    "achieved_tflops": sum(flops) / (ms / args.steps / 1000.0) / 1e12,
-                                   "frac_of_sustained": sum(flops) / (ms / args.steps / 1000.0) / 1e12 / tf_sus},
+                                   "frac_of_sustained": sum(flops) / (ms / args.steps / 1000.0) / 1e12 / tf_sus,
+                                   "kernel_floor_ms": sum(floors) / 1000.0,
+                                   "frac_of_kernel_floor": sum(floors) / 1000.0 / (ms / args.steps)},
                 "levels": levels, "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
