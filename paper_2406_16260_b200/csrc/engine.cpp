@@ -308,9 +308,16 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
         // the attention exchange)
         if (!own_done) project_qkv(b, L.ha, L.f_clip, true, s);
         project_qkv(b, L.ha - L.npre_a, L.npre_a, false, s);  // pre halo: K, V
-        project_qkv(b, L.ha + L.f_clip, L.npost_a, false, s);  // post halo: K, V
-        // remote global frames (+ the zero null frame the ablated tables point at): K, V
-        project_qkv(b, 2 * L.ha + L.f_clip, L.n_remote + (abl ? 1 : 0), false, s);
+        // post halo, then the remote global frames (+ the zero null frame the ablated tables
+        // point at): K, V; one launch when the post halo fills its slots (the two ranges are
+        // then adjacent in the attention buffer)
+        const uint32_t nrem = L.n_remote + (abl ? 1 : 0);
+        if (L.npost_a == L.ha) {
+            project_qkv(b, L.ha + L.f_clip, L.npost_a + nrem, false, s);
+        } else {
+            project_qkv(b, L.ha + L.f_clip, L.npost_a, false, s);
+            project_qkv(b, 2 * L.ha + L.f_clip, nrem, false, s);
+        }
         Span span(this, "attn_core", s);
         cuda_check(launch_attention_core(qkv, uint64_t(L.af) * hw, !f32(), L.hw, C, L.d.heads, L.f_clip,
                                          L.ha, tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale,
