@@ -345,7 +345,12 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
             continue;
         }
         const uint32_t buf = stg + (nstore & 1) * 2048;
-        if (nstore >= 2) {  // the store that last used this block has finished reading it
+        if (p.flags & kGemmFlagDiagNoSts) {  // diagnostics: no staging, no store
+            if (w[0] == 0x7fc17fc1u && w[15] == 0x7fc17fc1u) static_cast<uint32_t*>(p.out)[lane] = w[7];
+            continue;
+        }
+        const bool tma = !(p.flags & kGemmFlagDiagNoTma);
+        if (nstore >= 2 && tma) {  // the store that last used this block has finished reading it
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
         }
@@ -354,8 +359,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         for (int j = 0; j < 4; ++j) sts128(row + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
         dev::fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-            tma_store_2d(omap, buf, nb, m0);
+        if (lane == 0 && tma) {
+            // diagnostics: kGemmFlagDiagL2Out folds the rows onto 1024 (output stays in L2)
+            tma_store_2d(omap, buf, nb, (p.flags & kGemmFlagDiagL2Out) ? (m0 & 1023) : m0);
             dev::bulk_commit();
         }
         ++nstore;

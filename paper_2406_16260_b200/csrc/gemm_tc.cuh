@@ -50,6 +50,9 @@ struct GemmParams {
 };
 
 constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic
+constexpr int32_t kGemmFlagDiagNoTma = 16;  // diagnostics (TMA-store epilogue): stage, do not store
+constexpr int32_t kGemmFlagDiagNoSts = 32;  // diagnostics (TMA-store epilogue): convert only
+constexpr int32_t kGemmFlagDiagL2Out = 64;  // diagnostics (TMA-store epilogue): rows folded mod 1024
 constexpr int32_t kGemmFlagTmaOut = 1 << 8;  // bf16 output leaves through TMA stores (maps.out)
 // bf16 output + bf16 residual both through TMA (maps.out, maps.res); block_n % 32 == 0
 constexpr int32_t kGemmFlagTmaRes = 1 << 9;

@@ -46,3 +46,25 @@ mb = n * 2 / 1e6
 for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
     ms = timed(fn)
     print(f"{name}: {ms:.3f} ms/step  {mb / ms:.1f} GB/s per direction  -> {24 / ms * 1000:.0f} frames/s if PCIe-bound")
+
+# the same bidirectional transfer split into k chunks on k streams per direction
+for k in (2, 4):
+    ups = [torch.cuda.Stream() for _ in range(k)]
+    downs = [torch.cuda.Stream() for _ in range(k)]
+    c = n // k
+
+    def both_k():
+        cur = torch.cuda.current_stream()
+        for i in range(k):
+            ups[i].wait_stream(cur)
+            downs[i].wait_stream(cur)
+            with torch.cuda.stream(ups[i]):
+                d_a[i * c:(i + 1) * c].copy_(h_in[i * c:(i + 1) * c], non_blocking=True)
+            with torch.cuda.stream(downs[i]):
+                h_out[i * c:(i + 1) * c].copy_(d_b[i * c:(i + 1) * c], non_blocking=True)
+        for i in range(k):
+            cur.wait_stream(ups[i])
+            cur.wait_stream(downs[i])
+
+    ms = timed(both_k)
+    print(f"both x{k} streams: {ms:.3f} ms/step  {mb / ms:.1f} GB/s per direction  -> {24 / ms * 1000:.0f} frames/s")
