@@ -47,7 +47,8 @@ template <int BN, bool ST = false, bool RT = false>
 struct TileCfg {
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr uint32_t kStgWarp = RT ? 4096 : 32 * kStgPitch * 4;  // staging per epilogue warp
+    // staging per epilogue warp (RT stages its output boxes in the residual ring)
+    static constexpr uint32_t kStgWarp = RT ? 0 : 32 * kStgPitch * 4;
     static constexpr uint32_t kStg = kEpiWarps * kStgWarp;
     static constexpr uint32_t kRes = RT ? kEpiWarps * kResSlots * 2048 : 0;
     static constexpr int kStages =
@@ -382,6 +383,7 @@ struct ResRing {
     int lt, lc;      // next box to issue: tile, chunk column
     uint32_t lloc;   // lt's index among this CTA's tiles (its parity swaps the warp's chunks)
     int h0;          // the warp's chunk parity on its even tiles
+    bool pend;       // the slot consumed last holds an output box still being stored
 };
 
 template <int BN>
@@ -448,7 +450,7 @@ __device__ __forceinline__ void epilogue_tile_tma_res(const GemmParams& p, const
         }
         ++rg.ncons;
         __syncwarp();
-        if (lane == 0) {  // the slot is read: refill it with the box kResSlots ahead
+        if (!store && lane == 0) {  // the slot is read: refill it with the box kResSlots ahead
             dev::fence_proxy_async_smem();
             res_issue<BN>(p, rmap, rg, n_tiles, num_tiles, q);
         }
@@ -479,20 +481,24 @@ __device__ __forceinline__ void epilogue_tile_tma_res(const GemmParams& p, const
             const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
             w[h] = *reinterpret_cast<const uint32_t*>(&b2);
         }
-        const uint32_t buf = stg + (nstore & 1) * 2048;
-        if (nstore >= 2) {
-            if (lane == 0) bulk_wait_read<1>();
-            __syncwarp();
-        }
-        const uint32_t row = buf + lane * 64;
+        // the output box is staged in the residual slot just read (same 64B-swizzled box
+        // layout; every lane's reads are done at the __syncwarp above): no separate staging,
+        // which leaves the operand ring a fourth stage. The slot is refilled one chunk later,
+        // once this store has read it.
+        const uint32_t row = rg.base + slot * 2048 + lane * 64;
 #pragma unroll
         for (int j = 0; j < 4; ++j) sts128(row + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
         dev::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            tma_store_2d(omap, buf, nb, m0);
+            tma_store_2d(omap, rg.base + slot * 2048, nb, m0);
             dev::bulk_commit();
+            if (rg.pend) {  // the previous chunk's slot: its store has read it once <= 1 is pending
+                bulk_wait_read<1>();
+                res_issue<BN>(p, rmap, rg, n_tiles, num_tiles, q);
+            }
         }
+        rg.pend = true;
         ++nstore;
     }
 }
@@ -628,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             rg.lloc = 0;
             rg.h0 = half;
             rg.lc = 32 * half;
+            rg.pend = false;
             res_seek<BN>(p, rg, n_tiles, num_tiles);
             if (lane == 0) {
                 dev::tma_prefetch_desc(&maps.res);
