@@ -43,12 +43,13 @@ constexpr int kResSlots = 3;  // TMA residual ring depth per epilogue warp (32 x
 // RT: residual in through TMA and output out through TMA (bf16, no statistics): the
 // epilogue needs no transpose block, only two 2 KB store-staging blocks and a residual ring
 // per warp.
-template <int BN, bool ST = false, bool RT = false>
+template <int BN, bool ST = false, bool RT = false, bool TMAO = false>
 struct TileCfg {
     static constexpr uint32_t kBBytes = BN * kBK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    // staging per epilogue warp (RT stages its output boxes in the residual ring)
-    static constexpr uint32_t kStgWarp = RT ? 0 : 32 * kStgPitch * 4;
+    // staging per epilogue warp: RT stages its output boxes in the residual ring, the other
+    // TMA-store epilogue uses two 2 KB boxes, the transposed epilogue a 32 x kStgPitch fp32 block
+    static constexpr uint32_t kStgWarp = RT ? 0 : TMAO ? 4096 : 32 * kStgPitch * 4;
     static constexpr uint32_t kStg = kEpiWarps * kStgWarp;
     static constexpr uint32_t kRes = RT ? kEpiWarps * kResSlots * 2048 : 0;
     static constexpr int kStages =
@@ -507,7 +508,7 @@ template <int BN, bool OBF, bool RES, bool ST, bool TMAO = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
     constexpr bool RT = TMAO && RES;  // residual through TMA (the RT flavour)
-    using Cfg = TileCfg<BN, ST, RT>;
+    using Cfg = TileCfg<BN, ST, RT, TMAO>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -884,7 +885,7 @@ int g_num_sms = 0;
 
 template <int BN, bool OBF, bool RES, bool ST = false, bool TMAO = false>
 int launch_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
-    using Cfg = TileCfg<BN, ST, TMAO && RES>;
+    using Cfg = TileCfg<BN, ST, TMAO && RES, TMAO>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, OBF, RES, ST, TMAO>,
