@@ -110,7 +110,14 @@ def run_reference(args):
     frames = FRAMES_PER_GPU * args.gpus
     workers = ref_workers(frames)
     side = args.cpu_sample_hw
-    for _ in range(args.warmup):
+    # keep the whole --steps K --warmup W run within a few minutes: when one sample of the
+    # crop would push the run past ~180 s, halve the crop side (a quarter of the positions;
+    # frames/s is scaled by the positions sampled, so the value stays comparable)
+    _, probe_wall = cpu_reference_sample(frames, side, workers)
+    while side > 2 and probe_wall * (args.steps + args.warmup) > 180.0:
+        side //= 2
+        probe_wall /= 4.0
+    for _ in range(max(0, args.warmup - 1)):
         cpu_reference_sample(frames, side, workers)
     vals, walls = [], []
     for _ in range(args.steps):
