@@ -13,6 +13,127 @@
 #define ORC_ECONFIG 1
 #define ORC_ERANGE 2
 
+/* ---- speed without changing a bit --------------------------------------------------
+ * The checker must finish the BASELINE configurations (up to 24 x 40x64 x C=640 and
+ * C=1280 levels) in seconds on the GPU box's host, and stay bitwise equal to the
+ * reference. Two devices do that:
+ *   1. positions (and frames) are independent in every reduction the reference does
+ *      per output, so they are split over pthreads (ORC_THREADS, default: all cores);
+ *      each output is still computed by exactly one thread in the reference's order;
+ *   2. the f64-accumulated dot products (ops.cpp:90-99, :200-207) are vectorised ACROSS
+ *      outputs, never along the reduction: each output's accumulator sees the same
+ *      sequence of additions as the reference's scalar loop. f32 x f32 products are exact
+ *      in f64, so a fused or separate multiply-add rounds identically.
+ * The GroupNorm statistics (one running sum per group over the whole tensor,
+ * ops.cpp:112-142) are order-dependent and stay serial. */
+#include <pthread.h>
+#include <unistd.h>
+
+typedef double orc_v4d __attribute__((vector_size(32)));
+typedef float orc_v4f __attribute__((vector_size(16), aligned(4)));
+
+static int orc_threads(void) {
+    const char* e = getenv("ORC_THREADS");
+    long n = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    if (n < 1) n = 1;
+    if (n > 256) n = 256;
+    return (int)n;
+}
+
+typedef void (*orc_range_fn)(void* ctx, size_t lo, size_t hi);
+typedef struct { orc_range_fn fn; void* ctx; size_t lo, hi; } orc_job;
+static void* orc_job_run(void* p) {
+    orc_job* j = (orc_job*)p;
+    j->fn(j->ctx, j->lo, j->hi);
+    return NULL;
+}
+/* fn(ctx, lo, hi) over [0, n) in contiguous ranges, one per thread */
+static void orc_parallel(size_t n, orc_range_fn fn, void* ctx) {
+    int nt = orc_threads();
+    if ((size_t)nt > n) nt = (int)(n ? n : 1);
+    if (nt <= 1) { fn(ctx, 0, n); return; }
+    pthread_t th[256];
+    orc_job jobs[256];
+    for (int t = 0; t < nt; ++t) {
+        jobs[t].fn = fn; jobs[t].ctx = ctx;
+        jobs[t].lo = n * (size_t)t / (size_t)nt;
+        jobs[t].hi = n * (size_t)(t + 1) / (size_t)nt;
+    }
+    for (int t = 1; t < nt; ++t) pthread_create(&th[t], NULL, orc_job_run, &jobs[t]);
+    orc_job_run(&jobs[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
+/* Row micro-kernel. For nr <= 4 rows r and every output o < N:
+ *   acc = init ? (double)init[o] : 0.0;
+ *   for s in [0, nseg): for i in [0, K): acc += (double)wT[s][i*N + o] * (double)x[s][r][i];
+ *   y[r][o] = (float)acc;
+ * wT[s] is the TRANSPOSED weight matrix ([K][N]), so a step over i reads N contiguous
+ * weights; x[s][r] points at row r's K inputs of segment s. */
+#define ORC_MAXSEG 16
+static void orc_rows(uint32_t nr, uint32_t nseg, const float* const* wT,
+                     const float* const (*x)[4], uint32_t K, uint32_t N, const float* init,
+                     float* const* y) {
+    uint32_t o0 = 0;
+    for (; o0 + 8 <= N; o0 += 8) {
+        orc_v4d a[4][2];
+        for (uint32_t r = 0; r < 4; ++r)
+            for (int h = 0; h < 2; ++h)
+                for (int k = 0; k < 4; ++k) a[r][h][k] = init ? (double)init[o0 + 4 * h + k] : 0.0;
+        for (uint32_t s = 0; s < nseg; ++s) {
+            const float* w = wT[s] + o0;
+            const float* x0 = x[s][0];
+            const float* x1 = x[s][nr > 1 ? 1 : 0];
+            const float* x2 = x[s][nr > 2 ? 2 : 0];
+            const float* x3 = x[s][nr > 3 ? 3 : 0];
+            for (uint32_t i = 0; i < K; ++i, w += N) {
+                const orc_v4d w0 = __builtin_convertvector(*(const orc_v4f*)w, orc_v4d);
+                const orc_v4d w1 = __builtin_convertvector(*(const orc_v4f*)(w + 4), orc_v4d);
+                const double v0 = (double)x0[i], v1 = (double)x1[i], v2 = (double)x2[i],
+                             v3 = (double)x3[i];
+                a[0][0] += w0 * v0; a[0][1] += w1 * v0;
+                a[1][0] += w0 * v1; a[1][1] += w1 * v1;
+                a[2][0] += w0 * v2; a[2][1] += w1 * v2;
+                a[3][0] += w0 * v3; a[3][1] += w1 * v3;
+            }
+        }
+        for (uint32_t r = 0; r < nr; ++r)
+            for (int h = 0; h < 2; ++h)
+                for (int k = 0; k < 4; ++k) y[r][o0 + 4 * h + k] = (float)a[r][h][k];
+    }
+    for (; o0 < N; ++o0) /* N % 8 tail (the reference's own tests use C = 3, 4) */
+        for (uint32_t r = 0; r < nr; ++r) {
+            double acc = init ? (double)init[o0] : 0.0;
+            for (uint32_t s = 0; s < nseg; ++s)
+                for (uint32_t i = 0; i < K; ++i)
+                    acc += (double)wT[s][(size_t)i * N + o0] * (double)x[s][r][i];
+            y[r][o0] = (float)acc;
+        }
+}
+
+/* [rows][cols] -> [cols][rows] */
+static float* orc_transpose(const float* w, uint32_t rows, uint32_t cols) {
+    float* t = (float*)malloc(sizeof(float) * (size_t)rows * cols);
+    for (uint32_t r = 0; r < rows; ++r)
+        for (uint32_t c = 0; c < cols; ++c) t[(size_t)c * rows + r] = w[(size_t)r * cols + c];
+    return t;
+}
+
+/* y_r = W x_r for nr rows through the micro-kernel (WT = W transposed, [dim][dim]) */
+static void orc_project_rows(const float* WT, const float* const* xs, uint32_t nr, uint32_t dim,
+                             float* const* ys) {
+    for (uint32_t r0 = 0; r0 < nr; r0 += 4) {
+        const uint32_t n = nr - r0 < 4 ? nr - r0 : 4;
+        const float* xr[1][4];
+        float* yr[4];
+        for (uint32_t r = 0; r < 4; ++r) {
+            xr[0][r] = xs[r0 + (r < n ? r : 0)];
+            yr[r] = ys[r0 + (r < n ? r : 0)];
+        }
+        orc_rows(n, 1, &WT, (const float* const(*)[4])xr, dim, dim, NULL, yr);
+    }
+}
+
 /* ---- rng.hpp ------------------------------------------------------------ */
 
 uint64_t orc_splitmix_next(uint64_t* state) { /* rng.hpp:14-19 */
@@ -71,40 +192,71 @@ int orc_build_block(uint32_t C, uint32_t taps, uint64_t weight_seed, uint32_t b,
 
 /* ---- ops.cpp:42-55 ------------------------------------------------------- */
 
-void orc_spatial_affine_tanh(const float* v, size_t n, uint32_t C, const float* a, const float* c,
-                             float* out) {
-    for (size_t i = 0; i < n; ++i) {
-        const uint32_t ch = (uint32_t)(i % C);
-        out[i] = tanhf(a[ch] * v[i] + c[ch]);
+typedef struct { const float* v; uint32_t C; const float *a, *c; float* out; } orc_stub_job;
+static void orc_stub_range(void* p, size_t lo, size_t hi) {
+    const orc_stub_job* J = (const orc_stub_job*)p;
+    for (size_t i = lo; i < hi; ++i) {
+        const uint32_t ch = (uint32_t)(i % J->C);
+        J->out[i] = tanhf(J->a[ch] * J->v[i] + J->c[ch]);
     }
 }
 
+void orc_spatial_affine_tanh(const float* v, size_t n, uint32_t C, const float* a, const float* c,
+                             float* out) {
+    orc_stub_job J = {v, C, a, c, out};
+    orc_parallel(n, orc_stub_range, &J);
+}
+
 /* ---- ops.cpp:73-104 ------------------------------------------------------ */
+
+typedef struct {
+    const float* ext; uint32_t ext_f, C, taps, out_start;
+    size_t npos, fe;
+    const float* const* wT; /* [taps] transposed [C][C] tap matrices */
+    const float* bias; float* out;
+} orc_conv_job;
+
+/* unit u = (output frame f, block of 4 positions) */
+static void orc_conv_range(void* p, size_t lo, size_t hi) {
+    const orc_conv_job* J = (const orc_conv_job*)p;
+    const size_t nb = (J->npos + 3) / 4;
+    const int halo = (int)((J->taps - 1) / 2);
+    for (size_t u = lo; u < hi; ++u) {
+        const uint32_t f = (uint32_t)(u / nb);
+        const size_t p0 = (u % nb) * 4;
+        const uint32_t nr = (uint32_t)(J->npos - p0 < 4 ? J->npos - p0 : 4);
+        const float* wT[ORC_MAXSEG];
+        const float* xs[ORC_MAXSEG][4];
+        float* ys[4];
+        uint32_t ns = 0;
+        for (int j = -halo; j <= halo; ++j) { /* ops.cpp:91-99: taps in order, edges skipped */
+            const int64_t sf = (int64_t)J->out_start + f + j;
+            if (sf < 0 || sf >= (int64_t)J->ext_f) continue; /* video edge: zeros */
+            wT[ns] = J->wT[j + halo];
+            for (uint32_t r = 0; r < 4; ++r)
+                xs[ns][r] = J->ext + (size_t)sf * J->fe + (p0 + (r < nr ? r : 0)) * J->C;
+            ++ns;
+        }
+        for (uint32_t r = 0; r < 4; ++r)
+            ys[r] = J->out + (size_t)f * J->fe + (p0 + (r < nr ? r : 0)) * J->C;
+        orc_rows(nr, ns, wT, (const float* const(*)[4])xs, J->C, J->C, J->bias, ys);
+    }
+}
 
 int orc_conv_over_extended(const float* ext, uint32_t ext_f, uint32_t H, uint32_t W, uint32_t C,
                            uint32_t out_start, uint32_t out_len, uint32_t taps, const float* wts,
                            const float* bias, float* out) {
     if (taps == 0 || taps % 2 == 0) return ORC_ECONFIG;
     if (out_len == 0 || out_start > ext_f || out_len > ext_f - out_start) return ORC_ERANGE;
-    const int halo = (int)((taps - 1) / 2);
-    const size_t npos = (size_t)H * W;
-    const size_t fe = npos * C;
-    for (uint32_t f = 0; f < out_len; ++f) {
-        for (size_t pos = 0; pos < npos; ++pos) {
-            float* o = out + (size_t)f * fe + pos * C;
-            for (uint32_t oc = 0; oc < C; ++oc) {
-                double acc = (double)bias[oc];
-                for (int j = -halo; j <= halo; ++j) {
-                    const int64_t sf = (int64_t)out_start + f + j;
-                    if (sf < 0 || sf >= (int64_t)ext_f) continue; /* video edge: zeros */
-                    const float* in = ext + (size_t)sf * fe + pos * C;
-                    const float* wr = wts + ((size_t)(j + halo) * C + oc) * C;
-                    for (uint32_t ic = 0; ic < C; ++ic) acc += (double)wr[ic] * (double)in[ic];
-                }
-                o[oc] = (float)acc;
-            }
-        }
-    }
+    if (taps > ORC_MAXSEG) return ORC_ECONFIG;
+    /* out[f,pos,oc] = b[oc] + sum_j sum_ic W[j][oc][ic] * ext[out_start+f+j, pos, ic],
+     * accumulated in f64 in (j, ic) order, frames outside [0, ext_f) skipped */
+    float* wT[ORC_MAXSEG];
+    for (uint32_t j = 0; j < taps; ++j) wT[j] = orc_transpose(wts + (size_t)j * C * C, C, C);
+    orc_conv_job J = {ext, ext_f, C, taps, out_start, (size_t)H * W, (size_t)H * W * C,
+                      (const float* const*)wT, bias, out};
+    orc_parallel((size_t)out_len * ((J.npos + 3) / 4), orc_conv_range, &J);
+    for (uint32_t j = 0; j < taps; ++j) free(wT[j]);
     return ORC_OK;
 }
 
@@ -135,6 +287,19 @@ int orc_group_sqdev(const float* v, size_t total, uint32_t C, uint32_t groups,
     return ORC_OK;
 }
 
+typedef struct {
+    const float* v; uint32_t C, gs; const float *gamma, *beta; const double *means, *inv; float* out;
+} orc_norm_job;
+static void orc_norm_range(void* p, size_t lo, size_t hi) {
+    const orc_norm_job* J = (const orc_norm_job*)p;
+    for (size_t i = lo; i < hi; ++i) {
+        const uint32_t ch = (uint32_t)(i % J->C);
+        const uint32_t g = ch / J->gs;
+        J->out[i] = (float)((double)J->gamma[ch] * (((double)J->v[i] - J->means[g]) * J->inv[g]) +
+                            (double)J->beta[ch]);
+    }
+}
+
 int orc_normalize_with_stats(const float* v, size_t total, uint32_t C, uint32_t groups,
                              const float* gamma, const float* beta, float eps,
                              const double* means, const double* vars, float* out) {
@@ -143,12 +308,8 @@ int orc_normalize_with_stats(const float* v, size_t total, uint32_t C, uint32_t 
     const uint32_t gs = C / groups;
     double* inv = (double*)malloc(sizeof(double) * groups);
     for (uint32_t g = 0; g < groups; ++g) inv[g] = 1.0 / sqrt(vars[g] + (double)eps);
-    for (size_t i = 0; i < total; ++i) {
-        const uint32_t ch = (uint32_t)(i % C);
-        const uint32_t g = ch / gs;
-        out[i] = (float)((double)gamma[ch] * (((double)v[i] - means[g]) * inv[g]) +
-                         (double)beta[ch]);
-    }
+    orc_norm_job J = {v, C, gs, gamma, beta, means, inv, out};
+    orc_parallel(total, orc_norm_range, &J);
     free(inv);
     return ORC_OK;
 }
@@ -236,43 +397,70 @@ typedef struct {
     uint8_t* biased;
 } TokenList;
 
+typedef struct {
+    const float* const* kv_src; uint32_t rows;
+    const float* const* q_src; uint32_t nq;
+    float* const* out_at; uint32_t C, heads;
+    const float *wqT, *wkT, *wvT, *woT;
+    float scale, bias;
+    const TokenList* lists;
+    double* row_sums;
+} orc_attn_job;
+
+static void orc_attn_range(void* p, size_t lo, size_t hi) {
+    const orc_attn_job* J = (const orc_attn_job*)p;
+    const uint32_t C = J->C, rows = J->rows, nq = J->nq, heads = J->heads;
+    const uint32_t d = C / heads;
+    float* km = (float*)malloc(sizeof(float) * (size_t)rows * C);
+    float* vm = (float*)malloc(sizeof(float) * (size_t)rows * C);
+    float* qm = (float*)malloc(sizeof(float) * (size_t)nq * C);
+    float* cm = (float*)malloc(sizeof(float) * (size_t)nq * C);
+    uint32_t maxn = 1;
+    for (uint32_t a = 0; a < nq; ++a)
+        if (J->lists[a].n > maxn) maxn = J->lists[a].n;
+    double* logits = (double*)malloc(sizeof(double) * maxn);
+    double* acc = (double*)malloc(sizeof(double) * d);
+    const uint32_t nmax = rows > nq ? rows : nq;
+    const float** xs = (const float**)malloc(sizeof(float*) * nmax);
+    float** ys = (float**)malloc(sizeof(float*) * nmax);
+    for (size_t pos = lo; pos < hi; ++pos) {
+        /* ops.cpp:247-260 project_location: K and V of every row, Q of every query */
+        for (uint32_t r = 0; r < rows; ++r) { xs[r] = J->kv_src[r] + pos * C; ys[r] = km + (size_t)r * C; }
+        orc_project_rows(J->wkT, xs, rows, C, ys);
+        for (uint32_t r = 0; r < rows; ++r) ys[r] = vm + (size_t)r * C;
+        orc_project_rows(J->wvT, xs, rows, C, ys);
+        for (uint32_t a = 0; a < nq; ++a) { xs[a] = J->q_src[a] + pos * C; ys[a] = qm + (size_t)a * C; }
+        orc_project_rows(J->wqT, xs, nq, C, ys);
+        for (uint32_t a = 0; a < nq; ++a) {
+            for (uint32_t h = 0; h < heads; ++h) {
+                double rs = 0.0;
+                attend_tokens(qm + (size_t)a * C + (size_t)h * d, km + (size_t)h * d,
+                              vm + (size_t)h * d, C, J->lists[a].tok, J->lists[a].biased,
+                              J->lists[a].n, J->bias, J->scale, d, cm + (size_t)a * C + (size_t)h * d,
+                              logits, acc, J->row_sums ? &rs : NULL);
+                if (J->row_sums && h == 0) J->row_sums[pos * nq + a] = rs;
+            }
+        }
+        /* ops.cpp:334: out = Wo ctx */
+        for (uint32_t a = 0; a < nq; ++a) { xs[a] = cm + (size_t)a * C; ys[a] = J->out_at[a] + pos * C; }
+        orc_project_rows(J->woT, xs, nq, C, ys);
+    }
+    free(km); free(vm); free(qm); free(cm); free(logits); free(acc); free(xs); free(ys);
+}
+
 static void attention_core(const float* const* kv_src, uint32_t rows, const float* const* q_src,
                            uint32_t nq, float* const* out_at, size_t npos, uint32_t C,
                            const float* wq, const float* wk, const float* wv, const float* wo,
                            float scale, uint32_t heads, const TokenList* lists, float bias,
                            double* row_sums) {
-    const uint32_t d = C / heads;
-    float* km = (float*)malloc(sizeof(float) * (size_t)rows * C);
-    float* vm = (float*)malloc(sizeof(float) * (size_t)rows * C);
-    float* qm = (float*)malloc(sizeof(float) * (size_t)nq * C);
-    float* ctx = (float*)malloc(sizeof(float) * C);
-    uint32_t maxn = 1;
-    for (uint32_t a = 0; a < nq; ++a)
-        if (lists[a].n > maxn) maxn = lists[a].n;
-    double* logits = (double*)malloc(sizeof(double) * maxn);
-    double* acc = (double*)malloc(sizeof(double) * d);
-    size_t probe = 0;
-    for (size_t pos = 0; pos < npos; ++pos) {
-        for (uint32_t r = 0; r < rows; ++r) {
-            const float* x = kv_src[r] + pos * C;
-            orc_project_vec(wk, x, C, km + (size_t)r * C);
-            orc_project_vec(wv, x, C, vm + (size_t)r * C);
-        }
-        for (uint32_t a = 0; a < nq; ++a)
-            orc_project_vec(wq, q_src[a] + pos * C, C, qm + (size_t)a * C);
-        for (uint32_t a = 0; a < nq; ++a) {
-            for (uint32_t h = 0; h < heads; ++h) {
-                double rs = 0.0;
-                attend_tokens(qm + (size_t)a * C + (size_t)h * d, km + (size_t)h * d,
-                              vm + (size_t)h * d, C, lists[a].tok, lists[a].biased, lists[a].n,
-                              bias, scale, d, ctx + (size_t)h * d, logits, acc,
-                              row_sums ? &rs : NULL);
-                if (row_sums && h == 0) row_sums[probe++] = rs;
-            }
-            orc_project_vec(wo, ctx, C, out_at[a] + pos * C);
-        }
-    }
-    free(km); free(vm); free(qm); free(ctx); free(logits); free(acc);
+    float* wqT = orc_transpose(wq, C, C);
+    float* wkT = orc_transpose(wk, C, C);
+    float* wvT = orc_transpose(wv, C, C);
+    float* woT = orc_transpose(wo, C, C);
+    orc_attn_job J = {kv_src, rows, q_src, nq, out_at, C, heads, wqT, wkT, wvT, woT,
+                      scale, bias, lists, row_sums};
+    orc_parallel(npos, orc_attn_range, &J);
+    free(wqT); free(wkT); free(wvT); free(woT);
 }
 
 static void free_lists(TokenList* l, uint32_t n) {

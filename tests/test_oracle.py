@@ -138,3 +138,23 @@ def test_golden_fixtures_match_oracle(oracle):
     y = oracle.block_forward(z["x"], bo, float(z["t"]), int(z["groups"]), n_local=int(z["n_local"]),
                              n_global=int(z["n_global"]))
     assert np.array_equal(y, z["y"])
+
+
+@pytest.mark.parametrize("C,H,W", [(40, 3, 5), (12, 1, 7), (3, 2, 3)])
+def test_oracle_vectorised_threaded_bitwise(oracle, reference, C, H, W, monkeypatch):
+    # the checker vectorises across outputs and splits positions over threads
+    # (vinf_oracle.c orc_rows / orc_parallel); every output must stay bitwise equal to the
+    # reference's scalar loops, for ragged position blocks and C % 8 tails
+    x = oracle.tensor_from_seed((10, H, W, C), 11)
+    bo = oracle.build_block(C, 3, 2)
+    groups = 1 if C % 4 else 4
+    for threads in ("1", "3"):
+        monkeypatch.setenv("ORC_THREADS", threads)
+        assert np.array_equal(oracle.temporal_conv(x, 3, bo.conv_w, bo.conv_b),
+                              reference.conv_over_extended(x, 0, 10, 3, bo.conv_w, bo.conv_b))
+        sc = float(np.float32(1) / np.sqrt(np.float32(C)))
+        a = oracle.dual_scope(x, 900.0, bo.wq, bo.wk, bo.wv, bo.wo, sc, 4, 3, 10.0, 800.0)
+        b = reference.dual_scope(x, 900.0, bo.wq, bo.wk, bo.wv, bo.wo, sc, 4, 3, 10.0, 800.0)
+        assert np.array_equal(a, b)
+        assert np.array_equal(oracle.group_norm(x, groups, bo.gamma, bo.beta),
+                              reference.group_norm(x, groups, bo.gamma, bo.beta))
