@@ -45,7 +45,50 @@ def parse():
                     help="vc2 workload: total frames (uneven clips when the GPU count does not divide it)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the torch.distributed/NCCL exchange path even with one rank")
+    ap.add_argument("--no-f32", action="store_true", help="skip the fp32-mode record")
+    ap.add_argument("--no-vc2", action="store_true", help="skip the configs[3] 2,300-frame stack record")
     return ap.parse_args()
+
+
+# ---- rank launcher --------------------------------------------------------------
+
+
+def plan_launch(gpus: int, visible: int, environ: dict, script: str, argv: list, port: int):
+    """How this invocation runs: None = in this process (WORLD_SIZE set by torchrun, or one
+    GPU), else the argv that re-executes it as `gpus` ranks under torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1). Raises SystemExit when fewer GPUs than
+    requested are visible, so `--gpus N` never silently measures fewer GPUs."""
+    world = int(environ.get("WORLD_SIZE", "0") or 0)
+    if world:
+        if world != gpus:
+            raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}")
+        return None
+    if gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if visible < gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} requested but only {visible} CUDA device(s) visible")
+    if gpus == 1:
+        return None
+    return ["-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", script, *argv]
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """The max of a per-rank time over all ranks (the bench's multi-GPU clock rule)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def kernel_floor_us(frames: int, h: int, w: int, c: int, es: int, hbm_gbs: float, tf: float) -> dict:
@@ -78,25 +121,50 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def tensor_peak(clocks: dict):
+    """The bf16 tensor peak that applies to kernels timed under these clocks: the burst
+    figure when the SM clock held (median >= 95% of max) with no power cap, else the
+    sustained one. Returns (TFLOP/s, which, both)."""
+    _, burst, sus, src = peaks()
+    mhz, mx = clocks.get("sm_mhz"), clocks.get("sm_max_mhz")
+    held = bool(mhz and mx and mhz >= 0.95 * mx and "sw_power_cap" not in clocks.get("reasons", []))
+    which = "burst" if held else "sustained"
+    return (burst if held else sus), which, {"burst": burst, "sustained": sus, "source": src}
+
+
 # ---- reference CPU arm ------------------------------------------------------------
 
 
-def cpu_reference_sample(frames: int, side: int, workers: int):
+def cpu_reference_sample(frames: int, side: int, workers: int, fixed_s: float = 0.0):
     """The reference's own public run path (execute_run, runner.cpp:213-227) on a
     bounded spatial crop (side x side of the 40x64 latent); positions are independent in
-    the temporal layers, so frames/s scales by crop/full positions. Returns
-    (frames/s at the full 40x64 size, wall seconds, threads)."""
+    the temporal layers, so frames/s scales by crop/full positions. The run's fixed cost
+    (model build, thread start: a side = 1 run, `fixed_s`) is subtracted before scaling, so
+    the small crop does not understate the reference. Returns (frames/s at the full 40x64
+    size, wall seconds)."""
     from oracle.oracle import Reference
     ref = Reference()
     wall = ref.execute_run(frames, side, side, C, groups=GROUPS, n_local=N_LOCAL, n_global=N_GLOBAL,
                            blocks=1, steps=1, workers=workers)
-    fps_crop = frames / wall
-    return fps_crop * (side * side) / (H * W), wall
+    work = max(wall - fixed_s, 1e-6)
+    return frames / work * (side * side) / (H * W), wall
+
+
+def cpu_fixed_cost(frames: int, workers: int) -> float:
+    """Wall seconds of the reference run at a 1x1 crop: its per-call fixed cost."""
+    from oracle.oracle import Reference
+    ref = Reference()
+    ws = [ref.execute_run(frames, 1, 1, C, groups=GROUPS, n_local=N_LOCAL, n_global=N_GLOBAL, blocks=1,
+                          steps=1, workers=workers) for _ in range(3)]
+    return sorted(ws)[1]
 
 
 def ref_workers(frames: int) -> int:
+    """The reference's most parallel form on this host: in-process clip-parallel workers
+    (it has no intra-op threading), N <= host cores, N | F, and F / N >= the attention halo
+    (pipeline.cpp:131-143). 0 = its sequential path."""
     cores = os.cpu_count() or 1
-    best = 0  # 0 = sequential oracle path (1 thread)
+    best = 0
     for n in range(2, min(cores, frames) + 1):
         if frames % n == 0 and frames // n >= N_LOCAL // 2:
             best = n
@@ -110,25 +178,25 @@ def run_reference(args):
     frames = FRAMES_PER_GPU * args.gpus
     workers = ref_workers(frames)
     side = args.cpu_sample_hw
-    # keep the whole --steps K --warmup W run within a few minutes: when one sample of the
-    # crop would push the run past ~180 s, halve the crop side (a quarter of the positions;
-    # frames/s is scaled by the positions sampled, so the value stays comparable)
-    _, probe_wall = cpu_reference_sample(frames, side, workers)
-    while side > 2 and probe_wall * (args.steps + args.warmup) > 180.0:
+    fixed = cpu_fixed_cost(frames, workers)
+    # a fixed 8x8 crop; only if K + W samples would run past ~5 minutes is it halved
+    _, probe_wall = cpu_reference_sample(frames, side, workers, fixed)
+    while side > 2 and probe_wall * (args.steps + args.warmup) > 300.0:
         side //= 2
-        probe_wall /= 4.0
+        probe_wall = fixed + (probe_wall - fixed) / 4.0
     for _ in range(max(0, args.warmup - 1)):
-        cpu_reference_sample(frames, side, workers)
+        cpu_reference_sample(frames, side, workers, fixed)
     vals, walls = [], []
     for _ in range(args.steps):
-        v, w = cpu_reference_sample(frames, side, workers)
+        v, w = cpu_reference_sample(frames, side, workers, fixed)
         vals.append(v)
         walls.append(w)
     value = float(sum(vals) / len(vals))
     threads = max(workers, 1)
     sample = (f"reference execute_run (1 block, 1 step) on F={frames} frames of a {side}x{side} "
               f"crop of the 40x64 latent, C={C}, {'in-process clip-parallel x%d' % workers if workers else 'sequential'}; "
-              f"frames/s scaled by {side * side}/{H * W} positions")
+              f"fixed cost {fixed:.3f}s (1x1 crop run) subtracted, then frames/s scaled by "
+              f"{H * W}/{side * side} positions")
     line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * sum(walls) / len(walls), "higher_is_better": True,
@@ -136,7 +204,7 @@ def run_reference(args):
             "impl": "reference",
             "config": workload_config(args.gpus, "f32"),
             "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads,
-                             "kind": "reference", "sample": sample},
+                             "host_cores": os.cpu_count(), "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -216,27 +284,116 @@ class ClockSampler:
 
 # ---- our arm --------------------------------------------------------------------
 
-KERNEL_WORK = None  # filled in main: kernel -> (flops or bytes per launch, bound)
-
-
-def kernel_work(f_clip: int, dtype_bytes: int):
-    """Algorithmic work per launch for each kernel group: GEMM flops
-    2*M*N*K; bandwidth kernels their compulsory bytes."""
-    hw = H * W
+def kernel_work(f_clip: int, dtype_bytes: int, split: bool = False, h: int = H, w: int = W, c: int = C):
+    """Algorithmic work per launch for each kernel group: GEMM flops 2*M*N*K
+    (x3 in the fp32 mode: every product runs as bf16 hi*hi + hi*lo + lo*hi on the tensor
+    pipe, so that is the tensor work against the bf16 peak); bandwidth kernels their
+    compulsory bytes (fp32 mode: Q/K/V and ctx as two bf16 planes = 4 B per element)."""
+    hw = h * w
     M = f_clip * hw
-    E = hw * C
+    E = hw * c
     s = dtype_bytes
+    k = 3.0 if split else 1.0
     return {
-        "conv_gemm": (2.0 * M * C * TAPS * C, "tensor"),
-        "qkv_gemm": (2.0 * M * 3 * C * C, "tensor"),
-        "o_gemm": (2.0 * M * C * C, "tensor"),
+        "conv_gemm": (k * 2.0 * M * c * TAPS * c, "tensor"),
+        "qkv_gemm": (k * 2.0 * M * 3 * c * c, "tensor"),
+        "o_gemm": (k * 2.0 * M * c * c, "tensor"),
         "kv_gemm_ctx": (None, "tensor"),
-        "stub": (f_clip * E * (s + s), "hbm"),
-        "gn_stats": (((M + 31) // 32) * 2 * C * 4, "hbm"),  # the conv epilogue's 32-row partials
-        "gn_apply": (f_clip * E * (s + s), "hbm"),
-        "gn_fold": (3 * C * C * (s + s) + 3 * C * 4, "hbm"),  # W read, W' + b' written
+        "stub": (f_clip * E * (s + (2 * s if split else s)), "hbm"),  # fp32: x in; u (fp32) + hi/lo out
+        "gn_stats": (((M + 31) // 32) * 2 * c * 4, "hbm"),
+        "gn_apply": (f_clip * E * (s + 2 * s), "hbm") if split else (f_clip * E * (s + s), "hbm"),
+        "gn_fold": (3 * c * c * (2 + 2) + 3 * c * 4, "hbm"),  # W read, W' + b' written
         "attn_core": (f_clip * E * s * 4, "hbm"),  # Q, K, V once + ctx write
     }
+
+
+def roofline_of(work: dict, stats: dict, tf: float, hbm: float, steps: int):
+    """Per-kernel achieved rate and fraction of its bound, from per-kernel CUDA-event totals."""
+    per = {}
+    tot_all = sum(v[0] for v in stats.values()) or 1.0
+    for k, (tot, cnt) in stats.items():
+        row = {"ms_per_launch": tot / max(cnt, 1), "launches": cnt, "per_step_ms": tot / steps,
+               "share": tot / tot_all}
+        w_, bound = work.get(k, (None, None))
+        if w_:
+            ach = w_ / (row["ms_per_launch"] / 1000.0) / (1e12 if bound == "tensor" else 1e9)
+            row.update(achieved=ach, unit="TFLOP/s" if bound == "tensor" else "GB/s",
+                       frac=ach / (tf if bound == "tensor" else hbm), bound=bound)
+        per[k] = row
+    return per
+
+
+class _Timer:
+    """K steps between barrier + synchronize on both sides, CUDA events on the launching
+    stream, the max over ranks; clocks sampled during the region."""
+
+    def __init__(self, dev, local, world):
+        self.dev, self.local, self.world = dev, local, world
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(self.dev)
+
+    def run(self, step, steps, sample_clocks=True):
+        import torch
+        stream = torch.cuda.current_stream(self.dev)
+        clocks = ClockSampler(self.local) if sample_clocks else None
+        with (clocks or _Null()):
+            self.barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(steps):
+                step()
+            t1.record(stream)
+            self.barrier()
+        ms = max_over_ranks(t0.elapsed_time(t1), self.dev)
+        return ms, (clocks.summary() if clocks else None)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _block_engine(en, ops, n, rank, dtype, dev, frames_per_gpu=FRAMES_PER_GPU, weight_seed=1):
+    import torch  # noqa: F401
+    F = frames_per_gpu * n
+    desc = en.make_desc(F, n, rank, H, W, C, TAPS, GROUPS, HEADS, N_LOCAL, N_GLOBAL, BIAS,
+                        T_STAR, 1e-5, 0.0, 1, dtype)
+    eng = en.ClipEngine(en.Layout(desc), device=dev)
+    eng.init_weights(weight_seed)
+    # synthetic latent: this rank's frames of tensor_from_seed({F,H,W,C}, 0) (runner.cpp:59-60)
+    fc = frames_per_gpu
+    x = ops.tensor_from_seed((fc, H, W, C), 0, first_elem=rank * fc * H * W * C, dtype=dtype, device=dev)
+    eng.x.copy_(x)
+    return eng, x
+
+
+def _profile(eng, step, steps, timer):
+    """The same K steps again with CUDA events around every kernel group (vinf_engine_profile):
+    they serialise the stream, so this run only gives the per-kernel breakdown."""
+    import torch
+    eng.profile(True)
+    eng.kernel_stats()
+    stream = torch.cuda.current_stream(timer.dev)
+    timer.barrier()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(steps):
+        step()
+    p1.record(stream)
+    timer.barrier()
+    stats = eng.kernel_stats()
+    eng.profile(False)
+    return stats, p0.elapsed_time(p1) / steps
 
 
 def run_ours(args):
@@ -244,14 +401,13 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2406_16260_b200 import engine as en
+    from paper_2406_16260_b200 import ops
     from paper_2406_16260_b200.transport import DistTransport
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     n = max(world, 1)
-    if args.gpus != n and world > 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
@@ -261,78 +417,35 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
         group = en.DistGroup(DistTransport())
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-    F = FRAMES_PER_GPU * n
-    desc = en.make_desc(F, n, rank, H, W, C, TAPS, GROUPS, HEADS, N_LOCAL, N_GLOBAL, BIAS,
-                        T_STAR, 1e-5, 0.0, 1, dtype)
-    eng = en.ClipEngine(en.Layout(desc), device=dev)
-    eng.init_weights(1)
-    # synthetic latent: this rank's frames of tensor_from_seed({F,H,W,C}, 0) (runner.cpp:59-60)
-    from paper_2406_16260_b200 import ops
+    es = 2 if dtype == torch.bfloat16 else 4
     fc = FRAMES_PER_GPU
-    x_dev = ops.tensor_from_seed((fc, H, W, C), 0, first_elem=rank * fc * H * W * C, dtype=dtype,
-                                 device=dev)
-    eng.x.copy_(x_dev)
+    timer = _Timer(dev, local, world)
     stream = torch.cuda.current_stream(dev)
+
+    eng, x_dev = _block_engine(en, ops, n, rank, dtype, dev)
 
     def step():
         en.forward(T_STEP, [eng], group)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
     for _ in range(args.warmup):
         step()
-    barrier()
+    timer.barrier()
 
     # ---- timed region: K device-resident steps (value) ---------------------------
     # The engine's normal path (a single worker replays its CUDA graph; workers > 1 run
-    # the staged loop with the exchanges). Per-kernel CUDA events are NOT recorded here:
-    # they serialise the stream and cost ~13% of the step (scripts/graph_vs_profile.py).
+    # the staged loop with the exchanges). Per-kernel CUDA events are NOT recorded here.
     l0 = eng.launches()
-    clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local)
-    with clocks:
-        barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.steps):
-            step()
-        t1.record(stream)
-        barrier()
+    ms_max, clocks = timer.run(step, args.steps)
     launches = (eng.launches() - l0) // args.steps
-    ms = t0.elapsed_time(t1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
     ms_per_step = ms_max / args.steps
     value = n * fc * args.steps / (ms_max / 1000.0)
-
-    # ---- per-kernel region: the same K steps with CUDA events around every kernel group
-    # (vinf_engine_profile), for the kernel breakdown and the dominant kernel's roofline
-    eng.profile(True)
-    eng.kernel_stats()
-    barrier()
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        step()
-    p1.record(stream)
-    barrier()
-    stats = eng.kernel_stats()
-    eng.profile(False)
-    profiled_ms_per_step = p0.elapsed_time(p1) / args.steps
+    stats, profiled_ms_per_step = _profile(eng, step, args.steps, timer)
 
     # ---- e2e: host buffers in, host buffers out, through the public engine API ----
     # Two engines alternate steps; the upload of step j+1 (H2D stream) and the download of
     # step j-1 (D2H stream) overlap step j's kernels, so PCIe runs both directions while
     # the GPU computes. Every step still moves its whole clip in and its output out.
-    es = 2 if dtype == torch.bfloat16 else 4
-    eng2 = en.ClipEngine(en.Layout(desc), device=dev)
-    eng2.init_weights(1)
+    eng2, _ = _block_engine(en, ops, n, rank, dtype, dev)
     engs = [eng, eng2]
     h_in = torch.empty((fc, H, W, C), dtype=dtype, pin_memory=True)
     h_in.copy_(x_dev.cpu())
@@ -378,43 +491,32 @@ def run_ours(args):
         return start, end
 
     run_e2e(3)
-    barrier()
+    timer.barrier()
     e0, e1 = run_e2e(e_steps)
-    barrier()
-    ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-    e2e_value = n * fc * e_steps / (float(ems.item()) / 1000.0)
+    timer.barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
+    e2e_value = n * fc * e_steps / (e2e_ms / 1000.0)
     clip_bytes = fc * H * W * C * es
     # every step ran the same input: the host copies must equal the device result bitwise
     e2e_ok = bool(torch.equal(h_out[0], eng.y.cpu()) and torch.equal(h_out[1], eng.y.cpu()))
+    del eng2, engs
 
-    # ---- roofline of the dominant kernel -------------------------------------------
+    # ---- roofline of the dominant kernel (peaks chosen by the clocks of the region) ------
     hbm, tf_burst, tf_sus, src = peaks()
-    work = kernel_work(fc, es)
-    per_kernel = {}
-    for k, (tot, cnt) in stats.items():
-        per_kernel[k] = {"ms_per_launch": tot / max(cnt, 1), "launches": cnt,
-                         "share": 0.0}
-    tot_all = sum(v[0] for v in stats.values()) or 1.0
-    for k in per_kernel:
-        per_kernel[k]["share"] = stats[k][0] / tot_all
+    tf, which, both = tensor_peak(clocks)
+    work = kernel_work(fc, es, split=dtype == torch.float32)
+    per_kernel = roofline_of(work, stats, tf, hbm, args.steps)
     dom = max(stats, key=lambda k: stats[k][0]) if stats else None
     roof = None
-    if dom:
-        w_, bound = work.get(dom, (None, "tensor"))
-        avg_ms = per_kernel[dom]["ms_per_launch"]
-        if bound == "tensor" and w_:
-            ach = w_ / (avg_ms / 1000.0) / 1e12
-            roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tf_sus,
-                    "unit": "TFLOP/s", "frac": ach / tf_sus, "traffic": None,
-                    "peak_source": f"{src} bf16 sustained (kernel timed inside the step)",
-                    "work_per_launch": w_}
-        elif w_:
-            ach = w_ / (avg_ms / 1000.0) / 1e9
-            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None, "peak_source": f"{src} HBM copy",
-                    "work_per_launch": w_}
+    if dom and per_kernel[dom].get("frac") is not None:
+        pk = per_kernel[dom]
+        roof = {"kernel": dom, "bound": pk["bound"], "achieved": pk["achieved"],
+                "peak": tf if pk["bound"] == "tensor" else hbm, "unit": pk["unit"], "frac": pk["frac"],
+                "traffic": None,
+                "peak_source": (f"{src} bf16 {which} (SM clock held at max, no power cap)" if which == "burst"
+                                else f"{src} bf16 sustained (clock below max or power capped)")
+                if pk["bound"] == "tensor" else f"{src} HBM copy",
+                "peaks": both, "work_per_launch": work[dom][0]}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture of this
     # workload (dram__bytes_read.sum + dram__bytes_write.sum per launch)
     if roof is not None and args.dtype == "bf16":
@@ -426,35 +528,70 @@ def run_ours(args):
                 roof["traffic_source"] = tr["source"]
         except (OSError, ValueError):
             pass
-    # whole-block roofline: all tensor work of the step at the sustained tensor peak
     flops_step = sum(work[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm"))
-    floor = kernel_floor_us(fc, H, W, C, es, hbm, tf_sus)
+    floor = kernel_floor_us(fc, H, W, C, es, hbm, tf)
     block_roof = {"flops_per_step": flops_step,
                   "achieved_tflops": flops_step / (ms_per_step / 1000.0) / 1e12,
-                  "frac_of_sustained": flops_step / (ms_per_step / 1000.0) / 1e12 / tf_sus,
+                  "frac_of_tensor_peak": flops_step / (ms_per_step / 1000.0) / 1e12 / tf,
+                  "tensor_peak": {"value": tf, "which": which, **both},
                   # per-kernel floor: each kernel at max(tensor time, HBM time) (kernel_floor_us)
                   "kernel_floor_us": sum(floor.values()),
                   "frac_of_kernel_floor": sum(floor.values()) / (ms_per_step * 1000.0),
                   "kernel_floor_parts_us": floor}
-    for k, v in per_kernel.items():
-        w_, bound = work.get(k, (None, None))
-        if w_:
-            v["achieved"] = (w_ / (v["ms_per_launch"] / 1000.0) / (1e12 if bound == "tensor" else 1e9))
-            v["unit"] = "TFLOP/s" if bound == "tensor" else "GB/s"
-            v["frac"] = v["achieved"] / (tf_sus if bound == "tensor" else hbm)
+
+    # ---- fp32 mode (the reference's arithmetic, 1e-4 bar): same workload, timed ---------
+    f32_rec = None
+    if dtype == torch.bfloat16 and not args.no_f32:
+        del eng
+        torch.cuda.empty_cache()
+        e32, _ = _block_engine(en, ops, n, rank, torch.float32, dev)
+
+        def step32():
+            en.forward(T_STEP, [e32], group)
+
+        for _ in range(max(3, args.warmup)):
+            step32()
+        k32 = max(3, min(args.steps, 20))
+        ms32, clk32 = timer.run(step32, k32)
+        st32, _ = _profile(e32, step32, k32, timer)
+        tf32, which32, _ = tensor_peak(clk32)
+        w32 = kernel_work(fc, 4, split=True)
+        pk32 = roofline_of(w32, st32, tf32, hbm, k32)
+        f32_rec = {"value": n * fc * k32 / (ms32 / 1000.0), "unit": "frames/s",
+                   "ms_per_step": ms32 / k32, "steps": k32,
+                   "arithmetic": "bf16x3 split (hi*hi + hi*lo + lo*hi) on the tensor pipe, fp32 accumulate; "
+                                 "parity bar 1e-4 normwise",
+                   "tensor_peak": {"value": tf32, "which": which32},
+                   "kernels": {k: {kk: v[kk] for kk in ("per_step_ms", "frac", "unit") if kk in v}
+                               for k, v in pk32.items()},
+                   "clocks": clk32}
+        del e32
+        torch.cuda.empty_cache()
+    else:
+        del eng
+
+    # ---- configs[3]: the 2,300-frame VideoCrafter2-shaped stack over these N GPUs -----
+    vc2_rec = None
+    if not args.no_vc2:
+        vc2_rec = measure_vc2(en, ops, n, rank, dtype, dev, group, timer, frames=2300,
+                              steps=max(3, min(args.steps, 10)), warmup=2)
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         try:
             side = args.cpu_sample_hw
-            v, wall = cpu_reference_sample(fc, side, 0)
-            cpu = {"value": v, "unit": "frames/s", "cores": 1, "kind": "reference",
-                   "sample": f"reference execute_run, sequential (1 thread), F={fc}, "
-                             f"{side}x{side} crop of 40x64, C={C}, 1 block 1 step, wall "
-                             f"{wall:.2f}s; frames/s scaled by {side * side}/{H * W} positions"}
+            workers = ref_workers(fc)
+            fixed = cpu_fixed_cost(fc, workers)
+            v, wall = cpu_reference_sample(fc, side, workers, fixed)
+            cpu = {"value": v, "unit": "frames/s", "cores": max(workers, 1), "host_cores": os.cpu_count(),
+                   "kind": "reference",
+                   "sample": f"reference execute_run, {'in-process clip-parallel x%d' % workers if workers else 'sequential'} "
+                             f"(its most parallel form: no intra-op threading, F/N >= the 8-frame halo), F={fc}, "
+                             f"{side}x{side} crop of 40x64, C={C}, 1 block 1 step, wall {wall:.2f}s minus "
+                             f"fixed cost {fixed:.3f}s; frames/s scaled by {H * W}/{side * side} positions"}
         except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {ex}"}
+            cpu = {"value": None, "unit": "frames/s", "cores": 0, "host_cores": os.cpu_count(),
+                   "kind": "reference", "sample": f"unavailable: {ex}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
@@ -466,12 +603,14 @@ def run_ours(args):
                 "kernel_timing": {"region": "second run of the same K steps with CUDA events around "
                                             "every kernel group (the headline region runs without "
                                             "them)", "profiled_ms_per_step": profiled_ms_per_step},
+                "f32_mode": f32_rec,
+                "vc2_stack_2300": vc2_rec,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": clip_bytes,
                         "d2h_bytes_per_step": clip_bytes, "steps": e_steps,
                         "pipelining": "2 engines; H2D(j+1) and D2H(j-1) overlap step j",
                         "output_matches_device": e2e_ok},
-                "gpu_launches": int(launches * args.steps), "clocks": clocks.summary()}
+                "gpu_launches": int(launches * args.steps), "clocks": clocks}
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()
@@ -482,12 +621,71 @@ def run_ours(args):
 VC2_LEVELS = [(320, 40, 64), (640, 20, 32), (1280, 10, 16), (1280, 5, 8)]  # (C, H, W), SURVEY §8(a)
 
 
-def run_vc2(args):
+def measure_vc2(en, ops, n, rank, dtype, dev, group, timer, frames, steps, warmup):
     """BASELINE configs[3]: the VideoCrafter2-shaped temporal-layer stack, one dual-scope
     block per level (C, HxW) = (320, 40x64), (640, 20x32), (1280, 10x16), (1280, 5x8), over
-    --frames frames split into N clips (strong scaling; 2,300 over 8 GPUs = clips of 287/288
+    `frames` frames split into n clips (strong scaling: 2,300 over 8 GPUs = clips of 287/288
     frames, the uneven-clip extension). A step = every level's block over this GPU's clip,
-    with the 3-step sync per level when N > 1."""
+    with the 3-step sync per level when n > 1."""
+    import torch
+    engines = []
+    for li, (c, h, w) in enumerate(VC2_LEVELS):
+        desc = en.make_desc(frames, n, rank, h, w, c, TAPS, GROUPS, HEADS, N_LOCAL, N_GLOBAL, BIAS,
+                            T_STAR, 1e-5, 0.0, 1, dtype, uneven=frames % n != 0)
+        lay = en.Layout(desc)
+        fc = lay.f_clip
+        e = en.ClipEngine(lay, device=dev)
+        e.init_weights(1 + li)
+        e.x.copy_(ops.tensor_from_seed((fc, h, w, c), li, first_elem=lay.start * h * w * c,
+                                       dtype=dtype, device=dev))
+        engines.append(e)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for e in engines:
+            en.forward(T_STEP, [e], group)
+
+    for _ in range(warmup):
+        step()
+    ms, clocks = timer.run(step, steps)
+    # per-level split from a second pass with events between levels
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(engines) + 1)] for _ in range(steps)]
+    timer.barrier()
+    for k in range(steps):
+        evs[k][0].record(stream)
+        for li, e in enumerate(engines):
+            en.forward(T_STEP, [e], group)
+            evs[k][li + 1].record(stream)
+    timer.barrier()
+    level_ms = [sum(evs[k][li].elapsed_time(evs[k][li + 1]) for k in range(steps)) / steps
+                for li in range(len(engines))]
+    hbm, _, _, _ = peaks()
+    tf, which, both = tensor_peak(clocks)
+    es = 2 if dtype == torch.bfloat16 else 4
+    k = 1.0 if dtype == torch.bfloat16 else 3.0
+    fcs = [e.layout.f_clip for e in engines]
+    flops = [k * 14.0 * fc * h * w * c * c for fc, (c, h, w) in zip(fcs, VC2_LEVELS)]
+    floors = [sum(kernel_floor_us(fc, h, w, c, es, hbm, tf).values()) for fc, (c, h, w) in zip(fcs, VC2_LEVELS)]
+    levels = [{"channels": c, "height": h, "width": w, "frames_per_gpu": fc, "ms": m,
+               "achieved_tflops": fl / (m / 1000.0) / 1e12, "frac_of_tensor_peak": fl / (m / 1000.0) / 1e12 / tf,
+               "kernel_floor_ms": fu / 1000.0, "frac_of_kernel_floor": fu / 1000.0 / m}
+              for fc, (c, h, w), m, fl, fu in zip(fcs, VC2_LEVELS, level_ms, flops, floors)]
+    del engines
+    torch.cuda.empty_cache()
+    return {"workload": "BASELINE configs[3]: VideoCrafter2-shaped temporal stack, one dual-scope block per "
+                        "level", "frames": frames, "n_gpus": n, "value": frames * steps / (ms / 1000.0),
+            "unit": "frames/s", "scaling": "strong", "ms_per_step": ms / steps, "steps": steps,
+            "clips": "uneven (floor(w*F/N) split)" if frames % n else "even",
+            "levels": levels, "tensor_peak": {"value": tf, "which": which, **both},
+            "block_roofline": {"flops_per_step": sum(flops),
+                               "frac_of_tensor_peak": sum(flops) / (ms / steps / 1000.0) / 1e12 / tf,
+                               "kernel_floor_ms": sum(floors) / 1000.0,
+                               "frac_of_kernel_floor": sum(floors) / 1000.0 / (ms / steps)},
+            "clocks": clocks}
+
+
+def run_vc2(args):
+    """--workload vc2: the configs[3] stack alone (--frames frames over this run's GPUs)."""
     import torch
     import torch.distributed as dist
 
@@ -506,74 +704,18 @@ def run_vc2(args):
         dist.init_process_group("nccl", device_id=dev)
         group = en.DistGroup(DistTransport())
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-    F = args.frames
-    engines = []
-    for li, (c, h, w) in enumerate(VC2_LEVELS):
-        desc = en.make_desc(F, n, rank, h, w, c, TAPS, GROUPS, HEADS, N_LOCAL, N_GLOBAL, BIAS,
-                            T_STAR, 1e-5, 0.0, 1, dtype, uneven=F % n != 0)
-        lay = en.Layout(desc)
-        fc = lay.f_clip
-        e = en.ClipEngine(lay, device=dev)
-        e.init_weights(1 + li)
-        e.x.copy_(ops.tensor_from_seed((fc, h, w, c), li, first_elem=lay.start * h * w * c,
-                                       dtype=dtype, device=dev))
-        engines.append(e)
-    stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    for _ in range(args.warmup):
-        for e in engines:
-            en.forward(T_STEP, [e], group)
-    barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(engines) + 1)]
-           for _ in range(args.steps)]
-    clocks = ClockSampler(local)
-    with clocks:
-        barrier()
-        for k in range(args.steps):
-            evs[k][0].record(stream)
-            for li, e in enumerate(engines):
-                en.forward(T_STEP, [e], group)
-                evs[k][li + 1].record(stream)
-        barrier()
-    total_ms = evs[0][0].elapsed_time(evs[-1][-1])
-    ms_t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
-    value = F * args.steps / (ms / 1000.0)
-    level_ms = [sum(evs[k][li].elapsed_time(evs[k][li + 1]) for k in range(args.steps)) / args.steps
-                for li in range(len(engines))]
-    hbm, tf_burst, tf_sus, src = peaks()
-    flops = [14.0 * fc * h * w * c * c for (c, h, w) in VC2_LEVELS]  # conv 6MC^2 + qkv 6MC^2 + o 2MC^2
-    es = 2 if args.dtype == "bf16" else 4
-    floors = [sum(kernel_floor_us(fc, h, w, c, es, hbm, tf_sus).values()) for (c, h, w) in VC2_LEVELS]
-    levels = [{"channels": c, "height": h, "width": w, "ms": m,
-               "achieved_tflops": fl / (m / 1000.0) / 1e12,
-               "frac_of_sustained": fl / (m / 1000.0) / 1e12 / tf_sus,
-               "kernel_floor_ms": fu / 1000.0, "frac_of_kernel_floor": fu / 1000.0 / m}
-              for (c, h, w), m, fl, fu in zip(VC2_LEVELS, level_ms, flops, floors)]
+    rec = measure_vc2(en, ops, n, rank, dtype, dev, group, _Timer(dev, local, world), args.frames,
+                      args.steps, args.warmup)
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        line = {"metric": METRIC, "value": rec["value"], "unit": "frames/s", "n_gpus": n,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": args.dtype, "data": "synthetic (tensor_from_seed / build_model seeds)",
-                "config": {"workload": "BASELINE configs[3]: VideoCrafter2-shaped temporal stack, one "
-                                       "dual-scope block per level", "frames": F, "frames_per_gpu": fc,
+                "config": {"workload": rec["workload"], "frames": args.frames,
                            "levels": [list(x) for x in VC2_LEVELS], "groups": GROUPS,
                            "n_local": N_LOCAL, "n_global": N_GLOBAL, "t": T_STEP,
-                           "parallelism": f"clip-parallel x{n}",
-                           "clips": "uneven (floor(w*F/N) split)" if F % n else "even"},
-                "block_roofline": {"flops_per_step": sum(flops),
-                                   "achieved_tflops": sum(flops) / (ms / args.steps / 1000.0) / 1e12,
-                                   "frac_of_sustained": sum(flops) / (ms / args.steps / 1000.0) / 1e12 / tf_sus,
-                                   "kernel_floor_ms": sum(floors) / 1000.0,
-                                   "frac_of_kernel_floor": sum(floors) / 1000.0 / (ms / args.steps)},
-                "levels": levels, "clocks": clocks.summary()}
+                           "parallelism": f"clip-parallel x{n}", "clips": rec["clips"]},
+                "block_roofline": rec["block_roofline"], "levels": rec["levels"], "clocks": rec["clocks"]}
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()
@@ -600,8 +742,18 @@ def _stdout_for_result_only() -> None:
 
 
 def main():
-    _stdout_for_result_only()
     args = parse()
+    if args.impl == "ours":
+        try:
+            import torch
+            visible = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            visible = 0
+        argv = plan_launch(args.gpus, visible, os.environ, os.path.abspath(__file__), sys.argv[1:],
+                           _free_port())
+        if argv is not None:  # one process per GPU: re-run this command under torchrun
+            os.execv(sys.executable, [sys.executable, *argv])
+    _stdout_for_result_only()
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "vc2":

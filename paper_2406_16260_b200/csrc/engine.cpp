@@ -136,7 +136,6 @@ struct vinf_engine {
     void stage_qkv(uint32_t b, cudaStream_t s);
     void project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, bool with_q, cudaStream_t s);
     int qkv_ready = -1;  // block whose own-frame Q/K/V projection has already run
-    bool fused = false;  // Q/K/V projection + attention core in one kernel (attn_fused.cu)
     // bf16 mode: GroupNorm folded into the projections. The conv writes the raw GN input
     // straight into the attention buffer (so the exchanges ship raw frames), GN_APPLY
     // becomes one tiny kernel forming W' = W diag(s) and b' = W t, and the O GEMM adds the
@@ -150,7 +149,6 @@ struct vinf_engine {
     bool fold() const {
         return !f32() && fold_env && (ablate == VINF_ABLATE_NONE || ablate == VINF_ABLATE_CONV);
     }
-    bool use_fused() const { return fused && !fold(); }
     DevMat wfold_view() const {  // the folded Q/K/V weights (workspace), hi plane only
         DevMat m;
         m.rows = 3 * L.d.channels;
@@ -195,7 +193,9 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
         br.push_back(int64_t(j) * C);
     }
     Epilogue ep;
-    ep.bias = B.conv_b();
+    // GroupNorm folding stores u1 - b (the bias is absorbed by the fold's shift, group_fold):
+    // a smaller magnitude in bf16; the statistics are of u1 - b in either case
+    ep.bias = fold() ? nullptr : B.conv_b();
     ep.res = f32() ? at(L.off_u0f) : static_cast<void*>(at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E);
     ep.res_ld = C;
     ep.res_bf16 = !f32();
@@ -215,7 +215,8 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     ++launches;
     Span span(this, "gn_stats", s);
     cuda_check(launch_colpart_to_groups(colpart, uint32_t(gemm_colpart_rows(int64_t(rows), int(C))), C, L.d.groups,
-                                        at<double>(L.off_sums), at<double>(L.off_scratch), s),
+                                        B.conv_b(), double(rows), at<double>(L.off_sums),
+                                        at<double>(L.off_scratch), s),
                "gn fold");
     launches += 1;
 }
@@ -234,7 +235,7 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
         const uint32_t C = L.d.channels;
         float* aff = gn_aff();
         cuda_check(launch_group_fold(sums, gn_count(), C, G, B.gamma(), B.beta(), L.d.epsilon, B.wqkv.hi,
-                                     3 * C, wfold_view().hi, aff + 2 * C, aff, s),
+                                     3 * C, wfold_view().hi, aff + 2 * C, aff, B.conv_b(), s),
                    "gn fold");
     } else if (f32()) {
         auto* lo = at<__nv_bfloat16>(L.off_u2lo) + uint64_t(L.ha) * L.E;
@@ -264,11 +265,15 @@ void vinf_engine::project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, boo
     A.rows = uint64_t(L.af) * hw;
     A.cols = C;
     A.ld = C;
-    const size_t qes = f32() ? 4 : 2;
+    // bf16 mode: one bf16 [af*HW, 3C] buffer; fp32 mode: the same as two bf16 planes (hi, lo)
+    // written by the GEMM epilogue, the attention core's bf16x3 operands
+    const uint64_t plane = uint64_t(L.af) * hw * 3 * C;
+    auto* qkv = at<__nv_bfloat16>(L.off_qkv) + uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C);
     Epilogue ep;
     const bool fo = fold();
     if (fo) ep.bias = gn_aff() + 2 * C + (with_q ? 0 : C);
-    ep.out = at(L.off_qkv) + (uint64_t(frame0) * hw * 3 * C + (with_q ? 0 : C)) * qes;
+    ep.out = qkv;
+    ep.out_lo = f32() ? qkv + plane : nullptr;
     ep.out_ld = 3 * C;
     ep.out_bf16 = !f32();
     Span span(this, with_q ? "qkv_gemm" : "kv_gemm_ctx", s);
@@ -280,7 +285,7 @@ void vinf_engine::project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, boo
 // The own frames' Q/K/V projection only: it reads just this clip's normalised frames, so
 // a driver may run it while the attention exchange is in flight (on another stream).
 void vinf_engine::stage_qkv(uint32_t b, cudaStream_t s) {
-    if (!use_fused()) project_qkv(b, L.ha, L.f_clip, true, s);  // fused: the attention kernel projects
+    project_qkv(b, L.ha, L.f_clip, true, s);
     qkv_ready = int(b);
 }
 
@@ -295,15 +300,8 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     auto* ctxlo = f32() ? at<__nv_bfloat16>(L.off_ctxlo) : nullptr;
     const bool own_done = qkv_ready == int(b);
     qkv_ready = -1;
-    if (use_fused() && !abl) {
-        // Q/K/V projection and the attention core in one kernel: Q/K/V never reach HBM
-        Span span(this, "qkv_attn_fused", s);
-        cuda_check(launch_qkv_attention_fused(at(L.off_u2), L.af, L.ha, L.hw, C, L.f_clip, B.wqkv.hi,
-                                              tt[bias_global ? 1 : 0], L.scale, L.d.bias, ctx, s),
-                   "fused attention");
-        ++launches;
-    } else {
-        uint8_t* qkv = at(L.off_qkv);
+    {
+        auto* qkv = at<__nv_bfloat16>(L.off_qkv);
         // own frames: Q, K, V (unless the QKV stage already ran for this block, overlapping
         // the attention exchange)
         if (!own_done) project_qkv(b, L.ha, L.f_clip, true, s);
@@ -319,9 +317,10 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
             project_qkv(b, 2 * L.ha + L.f_clip, nrem, false, s);
         }
         Span span(this, "attn_core", s);
-        cuda_check(launch_attention_core(qkv, uint64_t(L.af) * hw, !f32(), L.hw, C, L.d.heads, L.f_clip,
-                                         L.ha, tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale,
-                                         L.d.bias, ctx, !f32(), f32() ? ctx : nullptr, ctxlo, s),
+        const uint64_t plane = uint64_t(L.af) * hw * 3 * C;
+        cuda_check(launch_attention_core(qkv, f32() ? qkv + plane : nullptr, L.hw, C, L.d.heads, L.f_clip, L.ha,
+                                         tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale, L.d.bias, ctx,
+                                         ctxlo, s),
                    "attention core");
         ++launches;
     }
@@ -372,15 +371,6 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
             cuda_check(cudaMemcpyAsync(p, blob[b].data(), blob[b].size(), cudaMemcpyHostToDevice, s),
                        "tokens");
             e->tt[b] = L.tok[b].view(p);
-        }
-        // fused projection + attention: every query block's K/V tokens are exactly the
-        // clip's own frames in order (the single-worker layout), bf16, one head
-        e->fused = !L.f32 && fused_attention_supported(L.d.channels, L.d.heads, L.f_clip, L.hw);
-        for (int b = 0; b < 2 && e->fused; ++b) {
-            const HostTokens& T = L.tok[b];
-            e->fused = T.nqb == 1 && T.kv_ok && T.kv_count[0] == L.f_clip;
-            for (uint32_t r = 0; e->fused && r < L.f_clip; ++r)
-                e->fused = T.kv_frames[r] == L.ha + r;
         }
         const uint32_t C = L.d.channels;
         e->blocks.resize(L.d.blocks);

@@ -230,15 +230,29 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
                     }
                 }
                 *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else if (p.out_lo) {
+                uint32_t wh[4], wl[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+                    const __nv_bfloat162 l2 = __floats2bfloat162_rn(y[2 * h] - __low2float(b2),
+                                                                    y[2 * h + 1] - __high2float(b2));
+                    wh[h] = *reinterpret_cast<const uint32_t*>(&b2);
+                    wl[h] = *reinterpret_cast<const uint32_t*>(&l2);
+                }
+                const int64_t o = gm * p.out_ld + n;
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + o) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out_lo) + o) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
             } else {
                 *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
                 *reinterpret_cast<float4*>(dst + 4) = make_float4(y[4], y[5], y[6], y[7]);
             }
-            if (ST) {
+            if (ST) {  // statistics of the stored value minus the bias (groupnorm.cu colpart_entry)
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    cs[k] += y[k];
-                    cq[k] = fmaf(y[k], y[k], cq[k]);
+                    const float v = y[k] - b8[k];
+                    cs[k] += v;
+                    cq[k] = fmaf(v, v, cq[k]);
                 }
             }
         }
@@ -694,179 +708,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) dev::tmem_dealloc(tmem_base, Cfg::kTmemCols);
 }
 
-// ---------------------------------------------------------------------------------------
-// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a 256 x BN
-// tile. Each CTA TMA-loads its own 128 rows of A and HALF (BN/2 rows) of B per stage; the
-// leader's single thread issues tcgen05.mma.cta_group::2 (M = 256), which reads both
-// CTAs' shared memory, and each CTA's TMEM holds the accumulator of its 128 rows. Per SM
-// this halves the B bytes pulled through L2 per flop, the bound of the single-CTA kernel
-// at these shapes (ncu: ~14-18 TB/s of L2->SM operand traffic). Barriers: both CTAs'
-// loads complete on the leader's full[s] (expect_tx set once for both halves); the MMA
-// commits multicast to both CTAs' empty[s] / tfull[acc]; both CTAs' epilogue warps release
-// the accumulator on the leader's tempty[acc]. The epilogue is the single-CTA one.
-template <int BN, bool ST = false>
-struct PairCfg {
-    static constexpr uint32_t kBBytes = (BN / 2) * kBK * 2;
-    static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages =
-        std::min<int>(8, (227 * 1024 - 1024 - 1024 - kStgBytes) / kStageBytes);
-    static constexpr uint32_t kAccStride = BN <= 128 ? 128 : 256;
-    static constexpr uint32_t kTmemCols = 2 * kAccStride;
-    static constexpr uint32_t kSmemBytes =
-        kStages * kStageBytes + 1024 /*align*/ + 1024 /*bars*/ + kStgBytes;
-};
-
-template <int BN, bool OBF, bool RES, bool ST>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmParams p) {
-    using Cfg = PairCfg<BN, ST>;
-    constexpr int S = Cfg::kStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* smem_a = smem;
-    uint8_t* smem_b = smem + S * kABytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
-    uint64_t* empty = full + S;
-    uint64_t* tfull = empty + S;   // [2]
-    uint64_t* tempty = tfull + 2;  // [2] (leader's are the ones used)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t rank = dev::cluster_rank();
-    const bool leader = rank == 0;
-
-    const int n_tiles = (p.N + BN - 1) / BN;
-    const int m_pairs = (p.M + 2 * kBM - 1) / (2 * kBM);
-    const int num_tiles = n_tiles * m_pairs;
-    const int kb_per_seg = (p.K + kBK - 1) / kBK;
-    const int k_iters = kb_per_seg * p.nseg;
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-
-    if (warp == 0 && lane == 0) {
-        dev::tma_prefetch_desc(&maps.a[0]);
-        dev::tma_prefetch_desc(&maps.a[1]);
-        dev::tma_prefetch_desc(&maps.b[0]);
-        dev::tma_prefetch_desc(&maps.b[1]);
-    }
-    if (warp == 1 && lane == 0) {
-        for (int s = 0; s < S; ++s) {
-            dev::mbar_init(&full[s], 1);
-            dev::mbar_init(&empty[s], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            dev::mbar_init(&tfull[i], 1);
-            dev::mbar_init(&tempty[i], 2 * kEpiWarps);
-        }
-        dev::fence_barrier_init();
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         dev::smem_u32(tmem_holder)),
-                     "r"(Cfg::kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
-    dev::tc_fence_before();
-    dev::cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated in both
-    dev::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-
-    if (warp == 0) {
-        // ===== TMA producer (both CTAs: own A rows, own half of B) =====
-        if (lane == 0) {
-            uint32_t it = 0;
-            const int b_half = rank * (BN / 2);
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
-                const int m0 = (tile / n_tiles) * 2 * kBM + int(rank) * kBM;
-                const int n0 = (tile % n_tiles) * BN + b_half;
-                for (int k = 0; k < k_iters; ++k, ++it) {
-                    const uint32_t s = it % S;
-                    const uint32_t ph = (it / S) & 1;
-                    dev::mbar_wait(&empty[s], ph ^ 1);
-                    const uint32_t bar = dev::peer_addr(dev::smem_u32(&full[s]), 0);
-                    if (leader) dev::mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
-                    const GemmSeg& sg = p.seg[k / kb_per_seg];
-                    const int kk = (k % kb_per_seg) * kBK;
-                    dev::tma_load_2d_pair(dev::smem_u32(smem_a + s * kABytes), &maps.a[sg.a_map], bar, kk,
-                                     m0 + sg.a_row);
-                    dev::tma_load_2d_pair(dev::smem_u32(smem_b + s * Cfg::kBBytes), &maps.b[sg.b_map], bar,
-                                     kk, n0 + sg.b_row);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ===== MMA issuer (leader CTA only) =====
-        if (leader) {
-            constexpr uint32_t idesc = dev::idesc_bf16_f32(2 * kBM, BN);
-            uint32_t it = 0;
-            uint32_t local = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
-                const uint32_t acc = local & 1;
-                dev::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
-                dev::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * Cfg::kAccStride;
-                for (int k = 0; k < k_iters; ++k, ++it) {
-                    const uint32_t s = it % S;
-                    const uint32_t ph = (it / S) & 1;
-                    dev::mbar_wait(&full[s], ph);
-                    dev::tc_fence_after();
-                    if (lane == 0) {
-                        const uint64_t ad = dev::sw128_kmajor_desc(dev::smem_u32(smem_a + s * kABytes));
-                        const uint64_t bd =
-                            dev::sw128_kmajor_desc(dev::smem_u32(smem_b + s * Cfg::kBBytes));
-#pragma unroll
-                        for (int kk = 0; kk < kBK / 16; ++kk)
-                            dev::umma_bf16_pair(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
-                                           (k > 0 || kk > 0) ? 1u : 0u);
-                        dev::umma_commit_pair(&empty[s]);
-                        if (k == k_iters - 1) dev::umma_commit_pair(&tfull[acc]);
-                    }
-                    __syncwarp();
-                }
-            }
-        }
-    } else if (warp >= 4) {
-        // ===== Epilogue (both CTAs, own 128 rows, all BN columns) =====
-        const int q = warp & 3;
-        const int half = (warp - 4) >> 2;
-        const uint32_t stg =
-            dev::smem_u32(smem + S * Cfg::kStageBytes + 1024) + (warp - 4) * (32 * kStgPitch * 4);
-        uint32_t local = 0;
-        EpiRes<OBF> rr;
-        EpiCol col;
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
-            const uint32_t acc = local & 1;
-            const int m0 = (tile / n_tiles) * 2 * kBM + int(rank) * kBM + q * 32;
-            const int n0 = (tile % n_tiles) * BN;
-            {
-                const int n_lim = min(p.N, n0 + BN);
-                const bool full_t = (m0 + 32 <= p.M) && (n0 + BN <= p.N);
-                if (n0 + 32 * half < n_lim) {
-                    epi_load_res<BN, OBF, RES>(p, rr, lane, m0, n0, 32 * half, full_t, n_lim);
-                    epi_load_col<RES>(p, col, lane, n0, 32 * half, n_lim);
-                }
-            }
-            dev::mbar_wait(&tfull[acc], (local >> 1) & 1);
-            dev::tc_fence_after();
-            epilogue_tile<BN, OBF, RES, ST>(p, tmem_base + acc * Cfg::kAccStride, q, lane, stg, m0, n0,
-                                            half, rr, col);
-            dev::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) dev::mbar_arrive_remote(dev::peer_addr(dev::smem_u32(&tempty[acc]), 0));
-        }
-    }
-
-    dev::tc_fence_before();
-    dev::cluster_sync_all();
-    dev::tc_fence_after();
-    if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(Cfg::kTmemCols)
-                     : "memory");
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -931,44 +772,6 @@ int launch(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
                : launch_cfg<BN, false, false>(maps, p, stream);
 }
 
-template <int BN, bool OBF, bool RES, bool ST = false>
-int launch_pair_cfg(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
-    using Cfg = PairCfg<BN, ST>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<BN, OBF, RES, ST>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(Cfg::kSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        attr_set = true;
-    }
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    const int tiles = ((p.N + BN - 1) / BN) * ((p.M + 2 * kBM - 1) / (2 * kBM));
-    const int clusters = std::max(1, std::min(tiles, g_num_sms / 2));
-    gemm_tc2_kernel<BN, OBF, RES, ST><<<2 * clusters, kThreads, Cfg::kSmemBytes, stream>>>(maps, p);
-    return int(cudaGetLastError());
-}
-
-template <int BN>
-int launch_pair(const GemmMaps& maps, const GemmParams& p, cudaStream_t stream) {
-    const bool res = p.res != nullptr;
-    if (res && p.res_bf16 != p.out_bf16) return int(cudaErrorInvalidValue);
-    if (p.colpart) {
-        if (!res) return int(cudaErrorInvalidValue);
-        return p.out_bf16 ? launch_pair_cfg<BN, true, true, true>(maps, p, stream)
-                          : launch_pair_cfg<BN, false, true, true>(maps, p, stream);
-    }
-    if (p.out_bf16) return res ? launch_pair_cfg<BN, true, true>(maps, p, stream)
-                               : launch_pair_cfg<BN, true, false>(maps, p, stream);
-    return res ? launch_pair_cfg<BN, false, true>(maps, p, stream)
-               : launch_pair_cfg<BN, false, false>(maps, p, stream);
-}
-
 }  // namespace
 
 int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -1007,7 +810,6 @@ static int env_int(const char* name, int dflt) {
 int gemm_colpart_rows(int64_t M, int N) {
     const int bn = gemm_pick_block_n(N);
     const int64_t rb = (M + 31) / 32;
-    if (gemm_use_pair(int(M), N, bn)) return int(rb);
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1047,37 +849,9 @@ int gemm_pick_block_n(int N) {
     return best;
 }
 
-bool gemm_use_pair(int M, int N, int block_n) {
-    // Measured on B200 at the block's shapes (M = 61440; N = 640 / 1920): the pair kernel
-    // is 5-10% slower than the single-CTA kernel (operand traffic is not the bound there),
-    // so it runs only on request (VINF_GEMM_PAIR=1), e.g. for A/B measurements.
-    static int env = -2;
-    if (env == -2) {
-        const char* e = getenv("VINF_GEMM_PAIR");
-        env = e ? atoi(e) : 0;
-    }
-    (void)M;
-    (void)N;
-    (void)block_n;
-    return env == 1;
-}
-
-int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream,
-                   bool pair) {
+int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream) {
     if (p.M <= 0 || p.N <= 0 || p.N % 8 != 0 || p.K <= 0 || p.nseg <= 0 || p.nseg > kGemmMaxSeg)
         return int(cudaErrorInvalidValue);
-    if (pair) {
-        switch (block_n) {
-            case 256: return launch_pair<256>(maps, p, stream);
-            case 240: return launch_pair<240>(maps, p, stream);
-            case 224: return launch_pair<224>(maps, p, stream);
-            case 192: return launch_pair<192>(maps, p, stream);
-            case 160: return launch_pair<160>(maps, p, stream);
-            case 128: return launch_pair<128>(maps, p, stream);
-            case 64: return launch_pair<64>(maps, p, stream);
-            default: return int(cudaErrorInvalidValue);
-        }
-    }
     switch (block_n) {
         case 256: return launch<256>(maps, p, stream);
         case 240: return launch<240>(maps, p, stream);

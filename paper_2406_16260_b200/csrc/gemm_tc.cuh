@@ -47,6 +47,10 @@ struct GemmParams {
     // Partial r is one (CTA group, TMEM quadrant) when every CTA keeps one column tile
     // (4 * gridDim / n_tiles rows), else one 32-row block (ceil(M / 32) rows).
     float* colpart;
+    // fp32 accumulator stored as split bf16 planes (out_bf16 == 0): out = RN(y) and
+    // out_lo = RN(y - RN(y)), both bf16 [M, out_ld]; the fp32-mode Q/K/V projection, whose
+    // consumer (the attention core's bf16x3 mode) reads exactly these planes
+    void* out_lo;
 };
 
 constexpr int32_t kGemmFlagNoStore = 1;  // benchmark-only: skip epilogue global traffic
@@ -71,12 +75,8 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
 // The epilogue's output map: bf16 [rows, cols] (row stride ld_elems), box 32 x 32, 64B swizzle.
 int make_tmap_out_bf16(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems);
 
-// Launches the GEMM on `stream`; picks the N tile. Returns 0 or a cudaError_t.
-// pair: the CTA-pair (cta_group::2) kernel; its B maps must have box rows = block_n / 2.
-int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream,
-                   bool pair = false);
-// Whether a GEMM of this shape uses the CTA-pair kernel (VINF_GEMM_PAIR=0/1 overrides).
-bool gemm_use_pair(int M, int N, int block_n);
+// Launches the GEMM on `stream` with N tile block_n. Returns 0 or a cudaError_t.
+int gemm_tc_launch(const GemmMaps& maps, const GemmParams& p, int block_n, cudaStream_t stream);
 
 // Largest supported N tile for a given N (used to build B tensor maps).
 int gemm_pick_block_n(int N);

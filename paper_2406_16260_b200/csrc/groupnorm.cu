@@ -449,10 +449,33 @@ uint64_t colpart_scratch_elems(uint32_t C) { return uint64_t(kColSegs) * 2 * C; 
 // result is therefore independent of CTA scheduling (bitwise reproducible).
 constexpr uint32_t kFoldSegs = 32;
 
+// The conv epilogue's partials are of v = u - b (the stored value minus the per-column
+// shift b, the conv bias): summing u^2 in fp32 would cancel catastrophically for channels
+// whose mean is far from zero, (u - b)^2 does not. Sums of u follow exactly in f64:
+//   sum u   = sum v + M b
+//   sum u^2 = sum (v^2 + 2 b v) + M b^2
+// so an entry contributes v (which = 0) or v^2 + 2 b v (which = 1; k2 = 2b), and the
+// group's constant M * sum_c b_c (or b_c^2) is added once.
+__device__ __forceinline__ double colpart_entry(const float* base, uint32_t C, uint32_t row, uint32_t c,
+                                                uint32_t which, double k2) {
+    const float* r = base + uint64_t(row) * 2 * C + c;
+    return which ? double(r[C]) + k2 * double(r[0]) : double(r[0]);
+}
+__device__ __forceinline__ double colpart_shift_total(const float* shift, uint32_t c0, uint32_t gs,
+                                                      uint32_t which, double rows) {
+    if (!shift) return 0.0;
+    double t = 0.0;
+    for (uint32_t c = 0; c < gs; ++c) {
+        const double b = double(shift[c0 + c]);
+        t += which ? b * b : b;
+    }
+    return rows * t;
+}
+
 __global__ void __launch_bounds__(128)
     colpart_fold_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C, uint32_t groups,
-                        double* __restrict__ seg, uint32_t* __restrict__ tickets,
-                        double* __restrict__ sums) {
+                        const float* __restrict__ shift, double rows, double* __restrict__ seg,
+                        uint32_t* __restrict__ tickets, double* __restrict__ sums) {
     dev::pdl_wait();
     dev::pdl_trigger();
     __shared__ double red[128];
@@ -461,26 +484,29 @@ __global__ void __launch_bounds__(128)
     const uint32_t which = sg / groups, g = sg % groups, gs = C / groups;
     const uint32_t per = (blocks + kFoldSegs - 1) / kFoldSegs;
     const uint32_t b0 = min(blocks, sid * per), b1 = min(blocks, b0 + per);
-    const float* base = part + uint64_t(which) * C + uint64_t(g) * gs;
+    const float* base = part + uint64_t(g) * gs;
     // thread = (row lane, group column): rows b0 + rl, b0 + rl + nrl, ... of one column;
     // a warp reads whole runs of the group's columns, loads independent (no divisions)
     double a = 0.0;
     const uint32_t nrl = gs <= 128 ? 128 / gs : 1;
     const uint32_t rl = threadIdx.x / gs, c = threadIdx.x % gs;
-    if (rl < nrl && c < gs) {
+    if (rl < nrl && c < gs && gs <= 128) {
+        const double k2 = (which && shift) ? 2.0 * double(shift[g * gs + c]) : 0.0;
         double a1 = 0.0;
         uint32_t b = b0 + rl;
         for (; b + nrl < b1; b += 2 * nrl) {
-            a += double(base[uint64_t(b) * 2 * C + c]);
-            a1 += double(base[uint64_t(b + nrl) * 2 * C + c]);
+            a += colpart_entry(base, C, b, c, which, k2);
+            a1 += colpart_entry(base, C, b + nrl, c, which, k2);
         }
-        if (b < b1) a += double(base[uint64_t(b) * 2 * C + c]);
+        if (b < b1) a += colpart_entry(base, C, b, c, which, k2);
         a += a1;
     }
     if (gs > 128) {  // wide groups: every thread strides the columns as well
         a = 0.0;
-        for (uint32_t cc = threadIdx.x; cc < gs; cc += 128)
-            for (uint32_t b = b0; b < b1; ++b) a += double(base[uint64_t(b) * 2 * C + cc]);
+        for (uint32_t cc = threadIdx.x; cc < gs; cc += 128) {
+            const double k2 = (which && shift) ? 2.0 * double(shift[g * gs + cc]) : 0.0;
+            for (uint32_t b = b0; b < b1; ++b) a += colpart_entry(base, C, b, cc, which, k2);
+        }
     }
     red[threadIdx.x] = a;
     __syncthreads();
@@ -501,7 +527,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (threadIdx.x == 0) {
-            sums[which * groups + g] = t;
+            sums[which * groups + g] = t + colpart_shift_total(shift, g * gs, gs, which, rows);
             tickets[sg] = 0;  // ready for the next fold
         }
     }
@@ -515,23 +541,26 @@ constexpr uint32_t kDirectMaxEntries = 16384;  // rows x group width handled by 
 
 __global__ void __launch_bounds__(kDirectThreads)
     colpart_fold_direct_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C,
-                               uint32_t groups, double* __restrict__ sums) {
+                               uint32_t groups, const float* __restrict__ shift, double rows,
+                               double* __restrict__ sums) {
     dev::pdl_wait();
     dev::pdl_trigger();
     __shared__ double red[kDirectThreads];
     const uint32_t which = blockIdx.x / groups, g = blockIdx.x % groups, gs = C / groups;
-    const float* base = part + uint64_t(which) * C + uint64_t(g) * gs;
+    const float* base = part + uint64_t(g) * gs;
     const uint32_t n = blocks * gs;
     double a0 = 0.0, a1 = 0.0;
     uint32_t i = threadIdx.x;
+    auto k2 = [&](uint32_t c) { return (which && shift) ? 2.0 * double(shift[g * gs + c]) : 0.0; };
     for (; i + kDirectThreads < n; i += 2 * kDirectThreads) {
         const uint32_t r0 = i / gs, r1 = (i + kDirectThreads) / gs;
-        a0 += double(base[uint64_t(r0) * 2 * C + (i - r0 * gs)]);
-        a1 += double(base[uint64_t(r1) * 2 * C + (i + kDirectThreads - r1 * gs)]);
+        const uint32_t c0 = i - r0 * gs, c1 = i + kDirectThreads - r1 * gs;
+        a0 += colpart_entry(base, C, r0, c0, which, k2(c0));
+        a1 += colpart_entry(base, C, r1, c1, which, k2(c1));
     }
     if (i < n) {
-        const uint32_t r0 = i / gs;
-        a0 += double(base[uint64_t(r0) * 2 * C + (i - r0 * gs)]);
+        const uint32_t r0 = i / gs, c0 = i - r0 * gs;
+        a0 += colpart_entry(base, C, r0, c0, which, k2(c0));
     }
     red[threadIdx.x] = a0 + a1;
     __syncthreads();
@@ -539,21 +568,22 @@ __global__ void __launch_bounds__(kDirectThreads)
         if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) sums[which * groups + g] = red[0];
+    if (threadIdx.x == 0) sums[which * groups + g] = red[0] + colpart_shift_total(shift, g * gs, gs, which, rows);
 }
 
 int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,
-                             double* sums, double* scratch, cudaStream_t s) {
+                             const float* shift, double rows, double* sums, double* scratch,
+                             cudaStream_t s) {
     if (groups == 0 || C % groups != 0) return int(cudaErrorInvalidValue);
     if (uint64_t(blocks) * (C / groups) <= kDirectMaxEntries)
         return int(launch_pdl(colpart_fold_direct_kernel, dim3(2 * groups), dim3(kDirectThreads), 0, s,
-                              part, blocks, C, groups, sums));
+                              part, blocks, C, groups, shift, rows, sums));
     // scratch: [2G][kFoldSegs] doubles of segment partials, then 2G uint32 tickets (zero
     // at rest: the workspace is zeroed at creation and every fold resets its tickets)
     double* seg = scratch;
     uint32_t* tickets = reinterpret_cast<uint32_t*>(scratch + uint64_t(2) * groups * kFoldSegs);
     return int(launch_pdl(colpart_fold_kernel, dim3(2 * groups * kFoldSegs), dim3(128), 0, s, part, blocks,
-                          C, groups, seg, tickets, sums));
+                          C, groups, shift, rows, seg, tickets, sums));
 }
 
 // GroupNorm folded into the following projection (bf16 mode): with per-channel
@@ -566,7 +596,7 @@ __global__ void __launch_bounds__(256)
     group_fold_kernel(const double* __restrict__ sums, double count, uint32_t C, uint32_t groups,
                       const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
                       const __nv_bfloat16* __restrict__ w, uint32_t N, __nv_bfloat16* __restrict__ wf,
-                      float* __restrict__ bias, float* __restrict__ st) {
+                      float* __restrict__ bias, float* __restrict__ st, const float* __restrict__ shift) {
     extern __shared__ __align__(16) float tab[];  // [2][C]: s, t
     constexpr int kMaxV = 5;   // 16-byte pieces of a row per lane: C <= 1280
     constexpr int kMaxCh = 8;  // channels per thread for (s, t): C <= 8 * blockDim
@@ -582,12 +612,13 @@ __global__ void __launch_bounds__(256)
         wr[i] = (vec && n < N && v < C / 8) ? __ldg(reinterpret_cast<const uint4*>(w + uint64_t(n) * C) + v)
                                              : make_uint4(0u, 0u, 0u, 0u);
     }
-    float gm[kMaxCh], bt[kMaxCh];
+    float gm[kMaxCh], bt[kMaxCh], sh[kMaxCh];
 #pragma unroll
     for (int i = 0; i < kMaxCh; ++i) {
         const uint32_t ch = threadIdx.x + blockDim.x * i;
         gm[i] = ch < C ? __ldg(gamma + ch) : 0.f;
         bt[i] = ch < C ? __ldg(beta + ch) : 0.f;
+        sh[i] = (ch < C && shift) ? __ldg(shift + ch) : 0.f;
     }
     dev::pdl_wait();
     dev::pdl_trigger();
@@ -604,7 +635,9 @@ __global__ void __launch_bounds__(256)
         double var = fma(-m, m, sums[groups + g] * ic);
         var = var > 0.0 ? var : 0.0;
         const float sc = gm[i] * rsqrtf(float(var + double(eps)));
-        const float t = bt[i] - float(m) * sc;
+        // the normalised tensor holds u - shift (the conv stores its output without the bias):
+        // GN(u) = s (u - shift) + beta - s (mu - shift)
+        const float t = bt[i] - float(m - double(sh[i])) * sc;
         tab[ch] = sc;
         tab[C + ch] = t;
         if (blockIdx.x == 0 && st) {
@@ -653,14 +686,14 @@ __global__ void __launch_bounds__(256)
 
 int launch_group_fold(const double* sums, double count, uint32_t C, uint32_t groups, const float* gamma,
                       const float* beta, float eps, const __nv_bfloat16* w, uint32_t N,
-                      __nv_bfloat16* wf, float* bias, float* st, cudaStream_t s) {
+                      __nv_bfloat16* wf, float* bias, float* st, const float* shift, cudaStream_t s) {
     if (groups == 0 || C % groups != 0 || groups > kMaxGroupsApply || count <= 0.0)
         return int(cudaErrorInvalidValue);
     const size_t shm = sizeof(float) * 2 * C;
     if (shm > 48 * 1024 || C > 8 * 256) return int(cudaErrorInvalidValue);
     const uint32_t grid = (N + 7) / 8;  // one warp per row, 8 per CTA (s, t built per CTA)
     return int(launch_pdl(group_fold_kernel, dim3(grid), dim3(256), shm, s, sums, count, C, groups,
-                          gamma, beta, eps, w, N, wf, bias, st));
+                          gamma, beta, eps, w, N, wf, bias, st, shift));
 }
 
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,

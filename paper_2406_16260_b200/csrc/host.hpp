@@ -79,6 +79,8 @@ struct HostTokens {
         const uint16_t k = count[a];
         if (k >= kMaxTokens) config_error("too many tokens per query (n_local + 1 + n_global)");
         if (!global && nwin[a] != k) config_error("window tokens must precede global tokens");
+        if (row > 0xFFFFu)
+            config_error("attention buffer exceeds 65535 frames (16-bit token rows)");
         rows[size_t(a) * kMaxTokens + k] = uint16_t(row);
         biased[size_t(a) * kMaxTokens + k] = b ? 1 : 0;
         count[a] = k + 1;
@@ -129,6 +131,8 @@ struct Epilogue {
     int64_t out_ld = 0;
     bool out_bf16 = false;
     float* colpart = nullptr;  // fused per-(32-row block, column) (sum, sum of squares)
+    // fp32 output as split bf16 planes: out = hi plane, out_lo = lo plane (both bf16, out_ld)
+    void* out_lo = nullptr;
 };
 
 // out[m, n] = sum_s A[m + a_rows[s]] . B[n + b_rows[s]] (+ bias, + res); M x N, K = A.cols.

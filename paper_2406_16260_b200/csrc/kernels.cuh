@@ -39,12 +39,14 @@ int launch_group_finalize(const double* sums, double count, uint32_t groups, dou
 // scratch: >= 2 * groups * min(4 * SMs, 512) doubles.
 int launch_group_moment_sums(const void* x, bool bf16, uint64_t rows, uint32_t C,
                              uint32_t groups, double* sums, double* scratch, cudaStream_t s);
-// Fold per-(32-row block, column) partials fp32 [blocks][2][C] (sum, sum of squares) into
-// per-group sums f64 [2][groups], in a fixed order (deterministic).
-// scratch: colpart_scratch_elems(C) doubles.
+// Fold the conv epilogue's column partials fp32 [blocks][2][C] (sum and sum of squares of
+// v = u - shift[c], the stored value minus the conv bias) into per-group sums of u, f64
+// [2][groups], in a fixed order (deterministic). rows = the rows the partials cover;
+// shift may be null (no shift). scratch: colpart_scratch_elems(C) doubles.
 uint64_t colpart_scratch_elems(uint32_t C);
 int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,
-                             double* sums, double* scratch, cudaStream_t s);
+                             const float* shift, double rows, double* sums, double* scratch,
+                             cudaStream_t s);
 // sums = [sum x (groups) | sum x^2 (groups)] -> stats = [mean | variance]
 int launch_group_moments(const double* sums, double count, uint32_t groups, double* stats,
                          cudaStream_t s);
@@ -53,18 +55,21 @@ int launch_group_moments(const double* sums, double count, uint32_t groups, doub
 // the moments are formed in the kernel (group_moments_kernel's arithmetic).
 // bf16 mode: GroupNorm folded into the next projection W [N][C] (groupnorm.cu):
 // wf = bf16(W diag(s)), bias = W t, st = [s; t] (f32, 2C) for the residual affine.
+// shift (nullable): the normalised tensor stores u - shift[c]; t absorbs s * shift.
 int launch_group_fold(const double* sums, double count, uint32_t C, uint32_t groups, const float* gamma,
                       const float* beta, float eps, const __nv_bfloat16* w, uint32_t N,
-                      __nv_bfloat16* wf, float* bias, float* st, cudaStream_t s);
+                      __nv_bfloat16* wf, float* bias, float* st, const float* shift, cudaStream_t s);
 int launch_group_apply(const void* x, bool in_bf16, uint64_t rows, uint32_t C, uint32_t groups,
                        const double* means, const double* vars, const float* gamma,
                        const float* beta, float eps, void* y, bool out_bf16, __nv_bfloat16* hi,
                        __nv_bfloat16* lo, cudaStream_t s, double count = 0.0);
 
-// ---- attention.cu ----
+// ---- attention_core.cu ----
 constexpr int kMaxTokens = 160;  // n_local + 1 + n_global upper bound
-constexpr int kQBlock = 32;      // queries per tensor-core attention CTA
-constexpr int kKvMax = 64;       // distinct K/V frames per query block (tensor-core path)
+constexpr int kQBlock = 32;      // queries per attention CTA
+// distinct K/V frames per 32-query block: the window band (32 + n_local) plus the sampled
+// globals never exceeds kQBlock + kMaxTokens - 1 = 191
+constexpr int kKvMax = 192;
 
 struct TokenTable {
     const uint16_t* rows;       // [nq][kMaxTokens] key/value frame row (in QKV frame units)
@@ -81,28 +86,18 @@ struct TokenTable {
     int max_kv;                 // largest K/V list over the blocks
 };
 
-// (hi/lo non-null: only the split bf16 planes are written, the fp32-mode GEMM operand)
-// ctx[a, p, :] = softmax-attention of query frame a at position p over its token list.
-// qkv: [(frames) * HW, 3C] with Q in cols [0,C), K in [C,2C), V in [2C,3C);
-// query frame a lives at QKV frame row q_frame0 + a. ctx: [nq * HW, C].
-// attention_tc.cu: bf16 tensor-core core (head dim % 64 == 0, <= kKvMax K/V frames per
-// 32-query block); launch_attention_core dispatches to it when supported.
-bool attention_tc_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
-int launch_attention_core_tc(const void* qkv, uint64_t qkv_rows, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
-                             uint32_t q_frame0, TokenTable tt, float scale, float bias, void* ctx,
-                             cudaStream_t s);
-
-// qkv_rows: rows of the QKV buffer (bounds of the TMA map the bf16 pipeline kernel reads it by)
-// attn_fused.cu: Q/K/V projection + attention core in one kernel for clips whose K/V
-// tokens are all own frames (the single-worker layout), bf16 mode.
-bool fused_attention_supported(uint32_t C, uint32_t heads, uint32_t F, uint32_t HW);
-int launch_qkv_attention_fused(const void* u2, uint32_t af, uint32_t f_own0, uint32_t HW, uint32_t C,
-                               uint32_t F, const void* wqkv, TokenTable tt, float scale, float bias,
-                               void* ctx, cudaStream_t s);
-
-int launch_attention_core(const void* qkv, uint64_t qkv_rows, bool bf16, uint32_t HW, uint32_t C, uint32_t heads,
-                          uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale, float bias,
-                          void* ctx, bool ctx_bf16, __nv_bfloat16* hi, __nv_bfloat16* lo,
-                          cudaStream_t s);
+// Whether the core runs this configuration: head dim d = C / heads with d % 8 == 0 and
+// every query block's distinct K/V frames <= kKvMax. There is no other attention kernel:
+// the engine and the operator forms reject what this does not cover.
+bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
+// ctx[a, p, :] = softmax-attention of query frame a at position p over its token list
+// (attend_tokens, ops.cpp:209-241). qkv: [(frames) * HW, 3C] bf16 with Q in cols [0, C),
+// K in [C, 2C), V in [2C, 3C); query frame a lives at QKV frame row q_frame0 + a;
+// ctx: [nq * HW, C] bf16.
+// Split (fp32) mode: qkv_lo / ctx_lo non-null are the lo planes (same layout) of the
+// bf16x3 operands; every product runs as hi*hi + hi*lo + lo*hi.
+int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
+                          uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias,
+                          void* ctx, void* ctx_lo, cudaStream_t s);
 
 }  // namespace vinf

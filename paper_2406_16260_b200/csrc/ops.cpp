@@ -79,8 +79,7 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
     if (M <= 0 || N <= 0) return;
     if (split && (!A.lo || !B.lo)) shape_error("gemm: split mode needs lo planes");
     const int bn = gemm_pick_block_n(int(N));
-    const bool pair = gemm_use_pair(int(M), int(N), bn);
-    const uint32_t b_box = uint32_t(pair ? bn / 2 : bn);  // the pair kernel loads half of B per CTA
+    const uint32_t b_box = uint32_t(bn);
     GemmMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     cuda_check(make_tmap_bf16(&maps.a[0], A.hi, A.rows, A.cols, A.ld, 128), "tmap A");
@@ -92,14 +91,28 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         maps.a[1] = maps.a[0];
         maps.b[1] = maps.b[0];
     }
+    std::vector<GemmSeg> segs;
+    for (size_t i = 0; i < a_rows.size(); ++i) {
+        const int32_t ar = int32_t(a_rows[i]), br = int32_t(b_rows[i]);
+        segs.push_back({0, ar, 0, br});
+        if (split) {
+            segs.push_back({0, ar, 1, br});
+            segs.push_back({1, ar, 0, br});
+        }
+    }
+    // More segments than one launch takes: later launches accumulate through the residual
+    // path (res = out), so the TMA residual map (built from ep.res) must not be used, and the
+    // partial sums cannot live in split planes.
+    const bool chunked = segs.size() > size_t(kGemmMaxSeg);
+    if (chunked && ep.out_lo) shape_error("gemm: split-plane output needs <= 12 segments");
     // bf16 output without residual / statistics (the Q/K/V projections): TMA-store epilogue
-    const bool tma_out = ep.out_bf16 && !ep.res && !ep.colpart && !split && !pair &&
+    const bool tma_out = !chunked && ep.out_bf16 && !ep.res && !ep.colpart && !split &&
                          reinterpret_cast<uintptr_t>(ep.out) % 16 == 0 && ep.out_ld % 8 == 0 &&
                          getenv("VINF_GEMM_NO_TMA_OUT") == nullptr;
     // bf16 output with a bf16 residual and no statistics (the O projection): residual in and
     // output out through TMA (the RT epilogue)
     static const bool no_tma_res = getenv("VINF_GEMM_NO_TMA_RES") != nullptr;
-    const bool tma_res = ep.out_bf16 && ep.res && ep.res_bf16 && !ep.colpart && !split && !pair &&
+    const bool tma_res = !chunked && ep.out_bf16 && ep.res && ep.res_bf16 && !ep.colpart && !split &&
                          bn % 32 == 0 && reinterpret_cast<uintptr_t>(ep.out) % 16 == 0 &&
                          ep.out_ld % 8 == 0 && reinterpret_cast<uintptr_t>(ep.res) % 16 == 0 &&
                          ep.res_ld % 8 == 0 && !no_tma_res;
@@ -110,15 +123,6 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         cuda_check(make_tmap_out_bf16(&maps.res, const_cast<void*>(ep.res), uint64_t(M), uint64_t(N),
                                       uint64_t(ep.res_ld)),
                    "tmap residual");
-    std::vector<GemmSeg> segs;
-    for (size_t i = 0; i < a_rows.size(); ++i) {
-        const int32_t ar = int32_t(a_rows[i]), br = int32_t(b_rows[i]);
-        segs.push_back({0, ar, 0, br});
-        if (split) {
-            segs.push_back({0, ar, 1, br});
-            segs.push_back({1, ar, 0, br});
-        }
-    }
     // Chunk into launches of <= kGemmMaxSeg segments; later chunks accumulate via the
     // residual path (res = out).
     for (size_t c0 = 0; c0 < segs.size(); c0 += kGemmMaxSeg) {
@@ -138,9 +142,10 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
         p.out = ep.out;
         p.out_ld = ep.out_ld;
         p.out_bf16 = ep.out_bf16;
+        p.out_lo = ep.out_lo;
         p.flags = g_gemm_debug_flags | (tma_out ? kGemmFlagTmaOut : 0) | (tma_res ? kGemmFlagTmaRes : 0);
         if (c0 + kGemmMaxSeg >= segs.size()) p.colpart = ep.colpart;  // final output only
-        cuda_check(gemm_tc_launch(maps, p, bn, s, pair), "gemm_tc_launch");
+        cuda_check(gemm_tc_launch(maps, p, bn, s), "gemm_tc_launch");
     }
 }
 
@@ -273,22 +278,27 @@ void attention_generic(const void* src, vinf_dtype dt, uint32_t frames, uint32_t
     const bool f32 = dt == VINF_F32;
     const uint64_t rows = uint64_t(frames) * hw;
     ActOperand A(src, dt, rows, C, s);
+    // bf16 Q/K/V, or (fp32) the hi and lo bf16 planes of the split arithmetic
     TmpBuf qkv(rows * 3 * C * (f32 ? 4 : 2), s);
+    auto* qh = static_cast<__nv_bfloat16*>(qkv.p);
     Epilogue e1;
-    e1.out = qkv.p;
+    e1.out = qh;
+    e1.out_lo = f32 ? qh + rows * 3 * C : nullptr;
     e1.out_ld = 3 * C;
     e1.out_bf16 = !f32;
     gemm(A.op, {0}, p->wqkv, {0}, int64_t(rows), 3 * C, e1, f32, s);
     HostTokens tk = tok;
     tk.finalize();
+    if (!tk.kv_ok) config_error("a query block touches more than 192 distinct frames");
+    if ((C / p->heads) % 8 != 0) config_error("attention head dim (C / heads) must be a multiple of 8");
     DevTokens dt_tok;
     dt_tok.upload(tk, s);
     const uint64_t qrows = uint64_t(nq) * hw;
     TmpBuf ctx(qrows * C * 4, s);  // bf16 ctx or hi+lo planes
     auto* hi = static_cast<__nv_bfloat16*>(ctx.p);
     auto* lo = hi + qrows * C;
-    cuda_check(launch_attention_core(qkv.p, rows, !f32, hw, C, p->heads, nq, q0, dt_tok.tt, p->scale,
-                                     bias, hi, !f32, f32 ? hi : nullptr, f32 ? lo : nullptr, s),
+    cuda_check(launch_attention_core(qh, f32 ? e1.out_lo : nullptr, hw, C, p->heads, nq, q0, dt_tok.tt,
+                                     p->scale, bias, hi, f32 ? lo : nullptr, s),
                "attention core");
     Operand O;
     O.hi = hi;

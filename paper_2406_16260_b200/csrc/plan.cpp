@@ -204,10 +204,13 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
         config_error("norm groups must divide channels: groups=" + std::to_string(d.groups) +
                      " channels=" + std::to_string(d.channels));
     if (d.heads == 0 || d.channels % d.heads != 0) config_error("heads must divide channels");
+
     if (d.blocks == 0) config_error("model needs at least one block");
     if (!(d.epsilon > 0.0f)) config_error("group norm epsilon must be > 0");
     if (d.channels % 8 != 0)
         shape_error("the clip engine needs channels % 8 == 0 (16-byte TMA rows)");
+    if ((d.channels / d.heads) % 8 != 0)
+        config_error("attention head dim (channels / heads) must be a multiple of 8");
     if (d.uneven) {
         if (d.workers == 0 || d.frames < d.workers) config_error("uneven clips need frames >= workers >= 1");
     } else {
@@ -257,6 +260,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
     cf = hc + f_clip + hc;
     null_frame = 2 * ha + f_clip + n_remote;
     af = null_frame + 1;
+    if (af > 0xFFFFu) config_error("attention buffer exceeds 65535 frames (16-bit token rows)");
 
     // Token lists (clip_parallel.cpp:285-305): window first, then the global set. With
     // the attention sync ablated the reference attends zero stand-ins for every global
@@ -271,6 +275,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
                 tok[b].push(a, b >= 2 ? null_frame : g_frame[j], (b & 1) == 1, true);
         }
         tok[b].finalize();
+        if (!tok[b].kv_ok) config_error("a query block touches more than 192 distinct frames");
     }
 
     // Workspace regions.

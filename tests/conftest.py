@@ -50,3 +50,22 @@ def lib():
     from paper_2406_16260_b200.build import build
     build()
     return _lib.load()
+
+
+# Parity errors recorded by the GPU tests (name -> (normwise error, tolerance)), printed in
+# the terminal summary so every run shows the measured errors, not only pass/fail.
+PARITY: dict = {}
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    return PARITY
+
+
+def pytest_terminal_summary(terminalreporter):
+    if not PARITY:
+        return
+    tr = terminalreporter
+    tr.section("parity (normwise max|got - want| / max|want|)")
+    for name, (err, tol) in sorted(PARITY.items()):
+        tr.write_line(f"{name:72s} {err:.3e}  (tol {tol:.0e})")

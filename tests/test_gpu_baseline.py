@@ -1,0 +1,223 @@
+"""GPU parity at the BASELINE.json configurations themselves (not scaled-down shapes).
+
+* configs[0]: one dual-scope temporal block, fp32, F = 32 as 2 clip-parallel clips x 16,
+  32x32 latent, C = 320: heads = 1 against the UNMODIFIED reference's own clip-parallel
+  eps_theta (oracle/_ref, clip_parallel.cpp:93-341 via pipeline.cpp:145-172) and its
+  execute_run (runner.cpp:26-73); heads = 8 (d = 40) against the oracle's heads extension
+  of attend_tokens (ops.cpp:209-241).
+* configs[1]: the same block at VideoCrafter2 scale, F = 24, 40x64, C = 640, 16 global
+  frames, in both arithmetic modes, t in {700, 900} (both bias regimes, ops.cpp:298).
+* configs[3] levels: C = 1280 (N = 3C = 3840 projections, d = 1280 or 160).
+* configs[4] long clips: F = 288 (one GPU's clip of 2,304 frames over 8) and n_global up to
+  64 with n_local = 32, where a 32-query block touches > 64 distinct K/V frames.
+* a shifted input (x * 3 + 5) through the GroupNorm-folded bf16 path.
+
+Every comparison is against the oracle run on the SAME fp32 input: the bf16 engine gets
+the bf16-rounded input, so its error includes the input quantisation (north_star:
+"the same synthetic inputs"). Tolerances (normwise): fp32 1e-4, bf16 2e-2."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import TOL_BF16, TOL_F32, normwise, to_np
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: TOL_F32, torch.bfloat16: TOL_BF16}
+NAME = {torch.float32: "f32", torch.bfloat16: "bf16"}
+
+
+@pytest.fixture(scope="module")
+def en(lib):
+    from paper_2406_16260_b200 import engine
+    return engine
+
+
+def _scale(C, heads):
+    return float(np.float32(1) / np.sqrt(np.float32(C // heads)))
+
+
+def run_engines(en, x, dtype, t, workers=1, heads=1, groups=32, n_local=16, n_global=16,
+                weight_seed=1, uneven=False):
+    """The block over `workers` clip engines on this GPU (LocalGroup: exchanges are
+    device-to-device copies of exactly the byte ranges the NCCL path moves)."""
+    F, H, W, C = x.shape
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+    engines = []
+    for w in range(workers):
+        d = en.make_desc(F, workers, w, H, W, C, 3, groups, heads, n_local, n_global, 10.0, 800.0,
+                         1e-5, 0.0, 1, dtype, uneven=uneven)
+        e = en.ClipEngine(en.Layout(d))
+        e.init_weights(weight_seed)
+        s, fc = e.layout.start, e.layout.f_clip
+        e.x.copy_(xd[s:s + fc])
+        engines.append(e)
+    en.forward(t, engines, en.LocalGroup() if workers > 1 else None)
+    return to_np(torch.cat([e.y for e in engines]))
+
+
+def check(parity_log, name, got, want, tol):
+    err = normwise(got, want)
+    parity_log[name] = (err, tol)
+    assert np.isfinite(got).all(), name
+    assert err <= tol, (name, err)
+
+
+# ---- configs[0] -------------------------------------------------------------------
+
+
+CFG0 = dict(F=32, H=32, W=32, C=320)
+
+
+def test_cfg0_fp32_clip_parallel_vs_reference(en, oracle, reference, parity_log):
+    F, H, W, C = CFG0.values()
+    x = oracle.tensor_from_seed((F, H, W, C), 0)
+    got = run_engines(en, x, torch.float32, 900.0, workers=2)
+    # the reference's own clip-parallel block (2 in-process workers, 3-step sync)
+    want = reference.block_forward(x, 3, 32, 1, 900.0, workers=2)
+    check(parity_log, "cfg0 f32 2x16 32x32 C=320 heads=1 t=900 vs reference (2 workers)", got, want, TOL_F32)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("heads", [1, 8])
+@pytest.mark.parametrize("t", [700.0, 900.0])
+def test_cfg0_vs_oracle(en, oracle, parity_log, dtype, heads, t):
+    F, H, W, C = CFG0.values()
+    x = oracle.tensor_from_seed((F, H, W, C), 0)
+    got = run_engines(en, x, dtype, t, workers=2, heads=heads)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, t, 32, heads=heads, scale=_scale(C, heads))
+    check(parity_log, f"cfg0 {NAME[dtype]} 2x16 32x32 C=320 heads={heads} t={t:.0f}", got, want, TOL[dtype])
+
+
+def test_cfg0_run_path_vs_reference_execute_run(en, reference, parity_log):
+    # the reference's public run path (execute_run, in-process clip-parallel x2): x0 after
+    # one Euler step of the block at t = 1000, from the seeded latent
+    F, H, W, C = CFG0.values()
+    _, x0 = reference.execute_run(F, H, W, C, groups=32, n_local=16, n_global=16, blocks=1, steps=1,
+                                  workers=2, want_x0=True)
+    from paper_2406_16260_b200 import ops
+    x = ops.tensor_from_seed((F, H, W, C), 0)
+    engines = []
+    for w in range(2):
+        d = en.make_desc(F, 2, w, H, W, C, 3, 32, 1, 16, 16, 10.0, 800.0, 1e-5, 0.0, 1, torch.float32)
+        e = en.ClipEngine(en.Layout(d))
+        e.init_weights(1)
+        e.x.copy_(x[w * 16:(w + 1) * 16])
+        engines.append(e)
+    en.denoise(1, engines, en.LocalGroup())
+    got = to_np(torch.cat([e.x for e in engines]))
+    check(parity_log, "cfg0 f32 execute_run x0 (1 step, 2 workers) vs reference", got, x0, TOL_F32)
+
+
+# ---- configs[1] -------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def cfg1_oracle(oracle):
+    F, H, W, C = 24, 40, 64, 640
+    x = oracle.tensor_from_seed((F, H, W, C), 0)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    return x, {t: oracle.block_forward(x, bp, t, 32) for t in (700.0, 900.0)}
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("t", [700.0, 900.0])
+def test_cfg1_full_size(en, cfg1_oracle, parity_log, dtype, t):
+    x, want = cfg1_oracle
+    got = run_engines(en, x, dtype, t)
+    check(parity_log, f"cfg1 {NAME[dtype]} F=24 40x64 C=640 t={t:.0f}", got, want[t], TOL[dtype])
+
+
+def test_cfg1_bf16_bitwise_repeatable(en, oracle):
+    x = oracle.tensor_from_seed((24, 40, 64, 640), 0)
+    a = run_engines(en, x, torch.bfloat16, 900.0)
+    b = run_engines(en, x, torch.bfloat16, 900.0)
+    assert np.array_equal(a, b)
+
+
+# ---- configs[3]: the C = 1280 levels ----------------------------------------------------
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("heads", [1, 8])
+def test_vc2_level_c1280(en, oracle, parity_log, dtype, heads):
+    F, H, W, C = 24, 10, 16, 1280
+    x = oracle.tensor_from_seed((F, H, W, C), 2)
+    got = run_engines(en, x, dtype, 900.0, heads=heads, weight_seed=3)
+    bp = oracle.build_block(C, 3, weight_seed=3)
+    want = oracle.block_forward(x, bp, 900.0, 32, heads=heads, scale=_scale(C, heads))
+    check(parity_log, f"vc2 level {NAME[dtype]} F=24 10x16 C=1280 heads={heads}", got, want, TOL[dtype])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_vc2_level_uneven_clips(en, oracle, parity_log, dtype):
+    # 2,300-style uneven split (floor(w F / N)): F = 50 over 4 workers = 12/13/12/13 frames
+    F, H, W, C = 50, 4, 8, 320
+    x = oracle.tensor_from_seed((F, H, W, C), 5)
+    got = run_engines(en, x, dtype, 900.0, workers=4, uneven=True, n_local=8, n_global=8)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 900.0, 32, n_local=8, n_global=8)
+    check(parity_log, f"uneven {NAME[dtype]} F=50 over 4 4x8 C=320", got, want, TOL[dtype])
+
+
+# ---- configs[4]: long clips, wide K/V lists, multi-head --------------------------------
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("n_local,n_global,heads", [(32, 64, 1), (16, 64, 8), (32, 16, 2), (2, 4, 1)])
+def test_cfg4_long_clip(en, oracle, parity_log, dtype, n_local, n_global, heads):
+    F, H, W, C = 288, 2, 4, 320
+    x = oracle.tensor_from_seed((F, H, W, C), 6)
+    got = run_engines(en, x, dtype, 700.0, heads=heads, n_local=n_local, n_global=n_global)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 700.0, 32, n_local=n_local, n_global=n_global, heads=heads,
+                                scale=_scale(C, heads))
+    check(parity_log, f"cfg4 {NAME[dtype]} F=288 C=320 n_local={n_local} n_global={n_global} heads={heads}",
+          got, want, TOL[dtype])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_cfg4_clip_parallel_2304(en, oracle, parity_log, dtype):
+    # 2,304 frames over 8 clip engines with n_global = 64: every worker holds remote globals
+    F, H, W, C = 2304, 1, 2, 64
+    x = oracle.tensor_from_seed((F, H, W, C), 7)
+    got = run_engines(en, x, dtype, 900.0, workers=8, groups=8, n_global=64)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 900.0, 8, n_global=64)
+    check(parity_log, f"cfg4 {NAME[dtype]} F=2304 over 8 C=64 n_global=64", got, want, TOL[dtype])
+
+
+# ---- GroupNorm with shifted inputs ------------------------------------------------------
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_shifted_input(en, oracle, parity_log, dtype):
+    F, H, W, C = 24, 8, 16, 320
+    x = oracle.tensor_from_seed((F, H, W, C), 9) * np.float32(3) + np.float32(5)
+    got = run_engines(en, x, dtype, 900.0)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 900.0, 32)
+    check(parity_log, f"shifted x*3+5 {NAME[dtype]} F=24 8x16 C=320", got, want, TOL[dtype])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("shift", [8.0, 40.0])
+def test_groupnorm_large_mean(en, oracle, parity_log, dtype, shift):
+    # GroupNorm inputs far from zero mean (conv bias + shift): the statistics come from the
+    # conv epilogue's column partials; mean / variance must survive |mu| >> sigma
+    F, H, W, C = 24, 16, 32, 320
+    x = oracle.tensor_from_seed((F, H, W, C), 10)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    bp.conv_b = (bp.conv_b + np.float32(shift)).astype(np.float32)
+    xd = torch.from_numpy(x).to("cuda", dtype)
+    d = en.make_desc(F, 1, 0, H, W, C, 3, 32, 1, 16, 16, 10.0, 800.0, 1e-5, 0.0, 1, dtype)
+    e = en.ClipEngine(en.Layout(d))
+    e.set_block(0, *[torch.from_numpy(a) for a in bp.arrays()])
+    e.x.copy_(xd)
+    en.forward(900.0, [e])
+    want = oracle.block_forward(x, bp, 900.0, 32)
+    # bf16 stores the raw GroupNorm input (|u| ~ shift) in bf16: its rounding step is
+    # shift * 2^-8 against sigma ~ 1, so the bf16 bar only holds for moderate shifts
+    tol = TOL[dtype] if dtype == torch.float32 or shift <= 8.0 else 0.1
+    check(parity_log, f"GN mean shift +{shift:.0f} {NAME[dtype]} F=24 16x32 C=320", to_np(e.y), want, tol)
