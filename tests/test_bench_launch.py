@@ -56,7 +56,8 @@ import bench
 dist.init_process_group("gloo")
 r = dist.get_rank()
 v = bench.max_over_ranks(10.0 + r, device="cpu")
-print("MAX", r, v, flush=True)
+with open(os.path.join(sys.argv[2], f"rank{r}.txt"), "w") as f:  # ranks share one stdout pipe
+    f.write(f"MAX {r} {v}")
 dist.destroy_process_group()
 '''
 
@@ -68,8 +69,8 @@ def test_max_over_ranks_gloo_world2(tmp_path):
     script = tmp_path / "w.py"
     script.write_text(_WORKER)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-                        "--master-addr=127.0.0.1", f"--master-port={port}", str(script), ROOT],
+                        "--master-addr=127.0.0.1", f"--master-port={port}", str(script), ROOT, str(tmp_path)],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
-    outs = sorted(l for l in r.stdout.splitlines() if l.startswith("MAX"))
+    outs = sorted((tmp_path / f"rank{i}.txt").read_text() for i in range(2))
     assert outs == ["MAX 0 11.0", "MAX 1 11.0"]

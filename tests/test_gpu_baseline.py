@@ -217,7 +217,7 @@ def test_groupnorm_large_mean(en, oracle, parity_log, dtype, shift):
     e.x.copy_(xd)
     en.forward(900.0, [e])
     want = oracle.block_forward(x, bp, 900.0, 32)
-    # bf16 stores the raw GroupNorm input (|u| ~ shift) in bf16: its rounding step is
-    # shift * 2^-8 against sigma ~ 1, so the bf16 bar only holds for moderate shifts
-    tol = TOL[dtype] if dtype == torch.float32 or shift <= 8.0 else 0.1
-    check(parity_log, f"GN mean shift +{shift:.0f} {NAME[dtype]} F=24 16x32 C=320", to_np(e.y), want, tol)
+    # the conv epilogue stores u1 - conv_b (the fold's shift absorbs the bias), so the bf16
+    # buffer does not carry the shifted mean: the full bf16 bar holds at +40 (measured 5.8e-3)
+    check(parity_log, f"GN mean shift +{shift:.0f} {NAME[dtype]} F=24 16x32 C=320", to_np(e.y), want,
+          TOL[dtype])
