@@ -47,6 +47,9 @@ def parse():
                     help="run the torch.distributed/NCCL exchange path even with one rank")
     ap.add_argument("--no-f32", action="store_true", help="skip the fp32-mode record")
     ap.add_argument("--no-vc2", action="store_true", help="skip the configs[3] 2,300-frame stack record")
+    ap.add_argument("--executor", default="native", choices=["native", "python"],
+                    help="N>1: native = the C++ executor (vinf_engine_forward_dist over an NCCL "
+                         "communicator, CUDA-graph replay); python = the torch.distributed stage loop")
     return ap.parse_args()
 
 
@@ -218,6 +221,7 @@ def workload_config(n: int, dtype: str) -> dict:
             "width": W, "channels": C, "taps": TAPS, "groups": GROUPS, "heads": HEADS,
             "n_local": N_LOCAL, "n_global": N_GLOBAL, "bias": BIAS, "t": T_STEP, "blocks": 1,
             "parallelism": f"clip-parallel x{n}",
+            "executor": "C++ vinf_engine_forward_dist over NCCL (N>1); CUDA-graph replay of the block",
             "l2": "per-step working set ~1 GB >> 126 MB L2; the step's input is re-read cold",
             "dtype": dtype}
 
@@ -396,13 +400,22 @@ def _profile(eng, step, steps, timer):
     return stats, p0.elapsed_time(p1) / steps
 
 
+def make_group(en, executor: str):
+    """The clip-parallel executor of this rank: the C++ one over an NCCL communicator
+    (default), or the Python stage loop over torch.distributed."""
+    if executor == "native":
+        from paper_2406_16260_b200.comm import NcclComm
+        return en.CommGroup([NcclComm.create()])
+    from paper_2406_16260_b200.transport import DistTransport
+    return en.DistGroup(DistTransport())
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2406_16260_b200 import engine as en
     from paper_2406_16260_b200 import ops
-    from paper_2406_16260_b200.transport import DistTransport
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -415,7 +428,7 @@ def run_ours(args):
         if world == 1 and "MASTER_ADDR" not in os.environ:  # single-rank NCCL group (path check)
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=dev)
-        group = en.DistGroup(DistTransport())
+        group = make_group(en, args.executor)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     es = 2 if dtype == torch.bfloat16 else 4
     fc = FRAMES_PER_GPU
@@ -691,7 +704,6 @@ def run_vc2(args):
 
     from paper_2406_16260_b200 import engine as en
     from paper_2406_16260_b200 import ops
-    from paper_2406_16260_b200.transport import DistTransport
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -702,7 +714,7 @@ def run_vc2(args):
     group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        group = en.DistGroup(DistTransport())
+        group = make_group(en, args.executor)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     rec = measure_vc2(en, ops, n, rank, dtype, dev, group, _Timer(dev, local, world), args.frames,
                       args.steps, args.warmup)

@@ -284,12 +284,78 @@ int vinf_engine_profile(vinf_engine* e, int enable);
 int vinf_engine_kernel_stats(vinf_engine* e, char* names, uint32_t name_cap, double* total_ms,
                              uint64_t* counts, uint32_t cap, uint32_t* n_out);
 
+/* ---- clip-parallel executor: the paper's 3-step context sync in C++ ------------
+ * Replaces the reference's Transport (transport.hpp:20-43: point-to-point messages
+ * matched by (peer, tag) plus the GroupNorm statistics exchange) and its worker loop
+ * eps_theta_worker (pipeline.cpp:145-172) + sync_contexts (clip_parallel.cpp:93-192).
+ * One communicator per worker:
+ *   vinf_comm_create_nccl  : NCCL over NVLink / NVSwitch, one process (or thread) per GPU;
+ *                            every rank passes the id rank 0 got from
+ *                            vinf_comm_nccl_unique_id (distributed out of band);
+ *   vinf_comm_create_local : N in-process workers (threads; device copies between their
+ *                            workspaces, the all-reduce summed in worker order), the
+ *                            shape of run_inproc_workers (transport_inproc.cpp:148-189);
+ *   vinf_comm_create_ops   : caller callbacks (any transport; pointers are whatever the
+ *                            exchanged workspace is: device memory, or host memory when
+ *                            a plan is run on a CPU host with vinf_layout_run_exchange). */
+typedef struct vinf_comm vinf_comm;
+typedef struct {
+    void* ctx;
+    /* optional: bracket the messages of one exchange; all must be complete (in stream
+     * order) when group_end returns */
+    int (*group_start)(void* ctx);
+    int (*send)(void* ctx, uint32_t peer, uint32_t tag, const void* ptr, uint64_t bytes, void* stream);
+    int (*recv)(void* ctx, uint32_t peer, uint32_t tag, void* ptr, uint64_t bytes, void* stream);
+    int (*group_end)(void* ctx, void* stream);
+    /* in-place sum over all ranks, identical result on every rank */
+    int (*allreduce_sum_f64)(void* ctx, double* ptr, uint64_t count, void* stream);
+} vinf_transport_ops;
+int vinf_comm_nccl_unique_id(uint8_t id[128]);
+/* Collective over the ranks: binds the communicator to the CURRENT CUDA device. */
+int vinf_comm_create_nccl(const uint8_t id[128], uint32_t nranks, uint32_t rank, vinf_comm** out);
+/* out: array of nranks communicators sharing one in-process hub (one per worker thread). */
+int vinf_comm_create_local(uint32_t nranks, vinf_comm** out);
+int vinf_comm_create_ops(const vinf_transport_ops* ops, uint32_t nranks, uint32_t rank, vinf_comm** out);
+void vinf_comm_destroy(vinf_comm* c);
+/* In-process workers: wakes every worker blocked in an exchange of this hub with a
+ * VINF_ERR_TRANSPORT error (call it when one worker fails). No-op for other kinds. */
+void vinf_comm_abort(vinf_comm* c);
+int vinf_comm_info(const vinf_comm* c, uint32_t* nranks, uint32_t* rank, uint64_t* bytes_sent,
+                   uint64_t* messages_sent);
+int vinf_comm_allreduce_sum_f64(vinf_comm* c, double* ptr, uint64_t count, void* stream);
+/* Runs one exchange stage of a layout's plan over `comm`, `base` = the workspace (pure
+ * host logic + the communicator's calls: usable on a CPU host with an ops transport). */
+int vinf_layout_run_exchange(const vinf_layout* l, int stage, void* base, vinf_comm* comm, void* stream);
+/* The engine's exchanges / GroupNorm all-reduce over a communicator, on `stream`. */
+int vinf_engine_exchange(vinf_engine* e, int stage, vinf_comm* comm, void* stream);
+int vinf_engine_allreduce_sums(vinf_engine* e, vinf_comm* comm, void* stream);
+/* One worker's whole block stack with the 3-step sync, all in C++ (the caller's thread
+ * only enqueues): per block
+ *   stub of the clip's boundary frames -> conv halo exchange on the engine's comm stream
+ *     || stub of the interior frames;
+ *   conv (+ GroupNorm partial sums) -> all-reduce of the 2*groups sums;
+ *   GroupNorm fold / apply -> attention halo + remote-global exchange on the comm stream
+ *     || the own frames' Q/K/V projection;
+ *   halo / remote-global K/V projection, attention core, O projection + residual.
+ * Exchanges of the kind set with vinf_engine_set_ablation are skipped. With an NCCL
+ * communicator the stack of each timestep regime is captured into a CUDA graph once
+ * and replayed (use_graph != 0). Every worker must call it with the same t. */
+int vinf_engine_forward_dist(vinf_engine* e, double t, vinf_comm* comm, int use_graph, void* stream);
+/* worker_denoise (pipeline.cpp:174-191) over the communicator. */
+int vinf_engine_denoise_dist(vinf_engine* e, uint32_t steps, vinf_comm* comm, int use_graph, void* stream);
+
 /* ---- diagnostics ---------------------------------------------------------------
  * Times the segmented tcgen05 GEMM alone on synthetic bf16 data: out[M,N] (bf16) =
  * sum over nseg segments of A[M,K] B[N,K]^T (+ bf16 residual); flags = 1 skips the
  * epilogue's global stores (isolates the main loop). Average ms over iters launches. */
 int vinf_gemm_bench(uint32_t M, uint32_t N, uint32_t K, uint32_t nseg, int flags, int residual,
                     int iters, float* avg_ms);
+/* The attention core alone on a single-worker engine layout's token table (t > t_star),
+ * over a synthetic Q/K/V buffer; pos_major = 1 views it as [HW][frames][3C]. */
+int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint32_t channels, uint32_t heads,
+                         uint32_t n_local, uint32_t n_global, int f32, int pos_major, int iters, float* avg_ms);
+/* Streaming 16-byte loads over `bytes` of device memory. */
+int vinf_read_bw_bench(uint64_t bytes, int iters, float* avg_ms);
 
 #ifdef __cplusplus
 }

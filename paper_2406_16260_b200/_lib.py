@@ -73,6 +73,19 @@ class Xfer(C.Structure):
                 ("reserved", C.c_uint32), ("offset", C.c_uint64), ("bytes", C.c_uint64)]
 
 
+# vinf_transport_ops callbacks (int return; ctx, ...)
+SEND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p)
+RECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p)
+GROUP_START_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
+GROUP_END_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
+class TransportOps(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("group_start", GROUP_START_FN), ("send", SEND_FN),
+                ("recv", RECV_FN), ("group_end", GROUP_END_FN), ("allreduce_sum_f64", ALLREDUCE_FN)]
+
+
 _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)
 _vp = C.c_void_p
@@ -147,6 +160,22 @@ _SIGS = {
                                   C.c_int, C.POINTER(C.c_float)]),
     "vinf_engine_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.c_uint32, C.POINTER(C.c_double),
                                            _u64p, C.c_uint32, _u32p]),
+    "vinf_attention_bench": (C.c_int, [C.c_uint32] * 7 + [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
+    "vinf_read_bw_bench": (C.c_int, [C.c_uint64, C.c_int, C.POINTER(C.c_float)]),
+    # clip-parallel executor (communicators)
+    "vinf_comm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "vinf_comm_create_nccl": (C.c_int, [C.POINTER(C.c_uint8), C.c_uint32, C.c_uint32, C.POINTER(_vp)]),
+    "vinf_comm_create_local": (C.c_int, [C.c_uint32, C.POINTER(_vp)]),
+    "vinf_comm_create_ops": (C.c_int, [C.POINTER(TransportOps), C.c_uint32, C.c_uint32, C.POINTER(_vp)]),
+    "vinf_comm_destroy": (None, [_vp]),
+    "vinf_comm_abort": (None, [_vp]),
+    "vinf_comm_info": (C.c_int, [_vp, _u32p, _u32p, _u64p, _u64p]),
+    "vinf_comm_allreduce_sum_f64": (C.c_int, [_vp, _vp, C.c_uint64, _vp]),
+    "vinf_layout_run_exchange": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
+    "vinf_engine_exchange": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "vinf_engine_allreduce_sums": (C.c_int, [_vp, _vp, _vp]),
+    "vinf_engine_forward_dist": (C.c_int, [_vp, C.c_double, _vp, C.c_int, _vp]),
+    "vinf_engine_denoise_dist": (C.c_int, [_vp, C.c_uint32, _vp, C.c_int, _vp]),
 }
 
 _lib = None

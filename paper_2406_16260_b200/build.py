@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libvinf_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["gemm_tc.cu", "elementwise.cu", "groupnorm.cu", "attention_core.cu", "plan.cpp", "ops.cpp",
-           "engine.cpp", "capi.cpp", "runapi.cpp"]
+           "engine.cpp", "comm.cpp", "capi.cpp", "runapi.cpp", "diag.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

@@ -1,57 +1,78 @@
 // Dual-scope attention core (attend_tokens, ops.cpp:209-241, applied per spatial position
 // as in dual_scope_reference ops.cpp:318-336 and attention_parallel clip_parallel.cpp:311-334).
 // The Q/K/V projections run before it as tcgen05 GEMMs; this kernel does only the banded +
-// global token mixing, which is ~1.5% of the block's flops and bound by reading Q/K/V once
-// and writing ctx once. One kernel serves every configuration:
+// global token mixing, ~1.5% of the block's flops, bound by reading Q/K/V once and writing
+// ctx once. One kernel serves every configuration:
 //
-//   * per spatial position p and block of 32 query frames, R = the distinct K/V frames the
-//     block's queries touch (window band + sampled globals, <= kKvMax = 192);
-//   * S = Q K^T [32 x R] over the head dim in 64-wide chunks, the reference's explicit token
-//     softmax on S (window tokens then globals, duplicates kept, +bias on the flagged side)
-//     in column form, then ctx = P V [32 x d] in 64-wide output chunks;
-//   * mma.sync m16n8k16 bf16 -> fp32 (tcgen05 needs M >= 64; a block has 32 queries, 24 at
+//   * work item = (spatial position p, block of 32 query frames); R = the distinct K/V
+//     frames the block's queries touch (window band + sampled globals, <= kKvMax = 192);
+//   * persistent CTAs, warp-specialised: warp 8 issues TMA loads (4-D tensor maps over the
+//     [frames][HW][3 x heads][d] Q/K/V buffer, 128-byte swizzle, 64-wide head-dim chunks,
+//     zero-filled past the head dim) into an mbarrier ring; the K/V frames of a block come
+//     as a host-built program of boxes of 32/16/8/4/2/1 consecutive frames; warps 0-7
+//     consume: S = Q K^T per head over the chunks, the reference's explicit token softmax
+//     (window tokens then globals, duplicates kept, +bias on the flagged side) in column
+//     form, ctx = P V chunk by chunk, stored straight from the accumulators;
+//   * mma.sync m16n8k16 bf16 -> fp32 (tcgen05 needs M >= 64; a block has <= 32 queries, 24 at
 //     the VideoCrafter2 clip);
-//   * any head dim d = C / heads with d % 8 == 0: the last 64-wide chunk of a head is
-//     zero-filled past d (cp.async src-size 0), e.g. d = 40 / 80 / 160 for 8 heads at
-//     C = 320 / 640 / 1280;
-//   * bf16 mode: Q/K/V and ctx are bf16;
-//     split mode (the fp32 engine mode): Q/K/V and ctx are each two bf16 planes hi = RN(x),
-//     lo = RN(x - hi), and every product runs as hi*hi + hi*lo + lo*hi (S and PV), the
-//     same bf16x3 arithmetic as the fp32-mode GEMMs (relative error ~2^-16 per product).
+//   * bf16 mode: Q/K/V and ctx are bf16; split mode (the fp32 engine mode): each is two bf16
+//     planes hi = RN(x), lo = RN(x - hi) and every product runs as hi*hi + hi*lo + lo*hi (S
+//     and PV), the same bf16x3 arithmetic as the fp32-mode GEMMs.
 //
-// All Q/K/V chunk loads stream through one NS-deep cp.async ring with a fixed prefetch
-// distance (NS - 1 chunks), so a head's V loads are in flight while its softmax runs.
+// The ring keeps loading the next item's chunks while the consumers run a softmax or finish
+// the last PV chunks, so HBM stays busy across items; no __syncthreads in the steady state
+// (two named barriers of the consumer warps per head around the softmax).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace vinf {
 
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn();
+int g_attn_pos_major = 0;
+
 namespace {
 
 constexpr int kDC = 64;  // head-dim chunk (one 128-byte swizzle row of bf16)
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr uint32_t kSmemPerSm = 228 * 1024;
+constexpr int kConsumerWarps = 4;
+constexpr int kWQ = kConsumerWarps / 2;  // warps per 16-query m tile
+constexpr int kON = 8 / kWQ;              // PV: n8 output tiles per warp in a 64-wide chunk
+constexpr uint32_t kOPitch = kON * 16 + 16;  // ctx staging row pitch (bytes, conflict-free)
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr uint32_t kQT = kQBlock * 128;  // one plane of a Q chunk (32 rows x 128 B)
+
+struct AttnMaps {
+    CUtensorMap box[2][kBoxKinds];  // [plane][kind]: boxes {64, 1, 1, 32 >> kind}
+};
+
+struct AttnArgs {
+    uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items;
+    float scale, bias;
+    __nv_bfloat16* ctx;
+    int64_t ctx_lo;  // elements from ctx to its lo plane (split mode)
+    TokenTable tt;
+};
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-    // byte offset of 16B chunk `chunk` of a 128-byte row (XOR swizzle: ldmatrix conflict-free)
+    // byte offset of 16B chunk `chunk` of a 128-byte row (the TMA 128B swizzle)
     return row * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
-// 16-byte async copy; src_bytes = 0 zero-fills the destination (head-dim chunk past d)
-__device__ __forceinline__ void cp_async16(uint32_t smem, const void* g, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem), "l"(g), "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1, int32_t c2, int32_t c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(dev::smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -60,9 +81,7 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
                  : "r"(addr));
 }
 __device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
-                 : "=r"(r0), "=r"(r1)
-                 : "r"(addr));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -89,209 +108,244 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
     lo = pack_bf16(a - __low2float(h), b - __high2float(h));
 }
 
-// Shared-memory layout (bytes). NTL = K/V rows / 8 (launch-wide max of the blocks' R,
-// padded to 16); PL = bf16 planes per operand (2 in split mode).
-//   ring[NS]  : stage = [Q hi | Q lo] (32 x 128 B each) + [K-or-V hi | lo] (RP x 128 B each)
-//   pb        : P as bf16 (PL planes), 64-column blocks of 32 x 128 B
-//   sp        : S, then P (fp32), 32 x SP
-//   ost       : ctx staging, 2 buffers x PL planes x 32 x 128 B; aliases pb/sp when P lives
-//               in registers for the PV phase (PREG), since S and the smem P are dead then
-//   zinv[32]
-template <int NTL, int NS, bool SPLIT>
+// Shared memory (bytes). RP = K/V tile rows (NTL * 8, a multiple of 16); PL = planes.
+//   qk[NQ] : S-phase stage = [Q planes: PL x 32 x 128 B][K planes: PL x RP x 128 B]
+//   v[NV]  : PV-phase stage = [V planes: PL x RP x 128 B]            (stages 1 KB aligned)
+//   sp     : S (fp32), 32 x SP
+//   pb     : P (bf16, PL planes), ceil(RP/64) blocks of 32 x 128 B (swizzled rows)
+//   bars   : full/empty of both rings
+// Two rings: the V chunks of an item wait in their own ring through its S phase and softmax,
+// while the S-phase ring is already streaming the next item's Q/K chunks.
+template <int NTL, bool SPLIT>
 struct CoreLay {
     static constexpr uint32_t RP = NTL * 8;
     static constexpr uint32_t SP = RP + 4;
     static constexpr uint32_t PL = SPLIT ? 2 : 1;
-    static constexpr bool PREG = NTL <= 8;
-    static constexpr uint32_t QT = kQBlock * 128;
+    static constexpr bool PREG = NTL <= 8;  // P fragments held in registers for PV
     static constexpr uint32_t KT = RP * 128;
-    static constexpr uint32_t stage = PL * (QT + KT);
+    static constexpr uint32_t QKST = (PL * (kQT + KT) + 1023) / 1024 * 1024;
+    static constexpr uint32_t VST = (PL * KT + 1023) / 1024 * 1024;
     static constexpr uint32_t PB = ((RP + 63) / 64) * kQBlock * 128;
-    static constexpr uint32_t pb = NS * stage;
-    static constexpr uint32_t sp = pb + PL * PB;
-    static constexpr uint32_t sp_end = sp + kQBlock * SP * 4;
-    static constexpr uint32_t OST = 2 * PL * QT;
-    static constexpr uint32_t ost = PREG ? pb : sp_end;
-    static constexpr uint32_t zinv = PREG ? (sp_end > pb + OST ? sp_end : pb + OST) : sp_end + OST;
-    static constexpr uint32_t total = zinv + kQBlock * 4;
-    static constexpr int blocks = int(kSmemPerSm / (total + 1024)) > 4 ? 4 : int(kSmemPerSm / (total + 1024));
+    static constexpr uint32_t OST = PL * 16 * kOPitch;  // per-warp ctx staging: 16 rows
+    static constexpr uint32_t scratch = kQBlock * SP * 4 + PL * PB + kConsumerWarps * OST + 2 * 20 * 8 + 1024;
+    // up to four CTAs per SM (each a 5-warp producer/consumer pipeline) while rings of
+    // 2 + 3 stages fit
+    static constexpr uint32_t need = 2 * QKST + 3 * VST + scratch;
+    static constexpr int ctas = need <= 56 * 1024 ? 4 : (need <= 75 * 1024 ? 3 : (need <= 112 * 1024 ? 2 : 1));
+    static constexpr uint32_t budget = (ctas == 4 ? 56u : ctas == 3 ? 75u : ctas == 2 ? 112u : 224u) * 1024u - scratch;
+    static constexpr uint32_t nv0 = (budget / 2) / VST;
+    static constexpr int NV = nv0 > 10 ? 10 : (nv0 < 1 ? 1 : int(nv0));
+    static constexpr uint32_t nq0 = (budget - NV * VST) / QKST;
+    static constexpr int NQ = nq0 > 8 ? 8 : (nq0 < 1 ? 1 : int(nq0));
+    static constexpr uint32_t vring = NQ * QKST;
+    static constexpr uint32_t sp = vring + NV * VST;
+    static constexpr uint32_t pb = sp + kQBlock * SP * 4;
+    static constexpr uint32_t ost = pb + PL * PB;
+    static constexpr uint32_t bars = (ost + kConsumerWarps * OST + 15) / 16 * 16;
+    static constexpr uint32_t total = bars + 2 * (NQ + NV) * 8 + 1024;  // + alignment slack
+    static_assert(total <= 227 * 1024, "attention core shared memory");
 };
 
-template <int NTL, int NS, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
-    attention_core_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_lo, uint32_t HW, uint32_t C,
-                          uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale,
-                          float bias, __nv_bfloat16* __restrict__ ctx, int64_t ctx_lo) {
-    dev::pdl_wait();
-    dev::pdl_trigger();
-    using LL = CoreLay<NTL, NS, SPLIT>;
+// Position in a ring of N stages: slot and the parity of its current use.
+template <int N>
+struct Ring {
+    uint32_t slot = 0, phase = 0;
+    __device__ __forceinline__ void next() {
+        if (++slot == uint32_t(N)) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+template <int NTL, bool SPLIT>
+__global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
+    attention_core_kernel(const __grid_constant__ AttnMaps maps, const AttnArgs a) {
+    using LL = CoreLay<NTL, SPLIT>;
     constexpr uint32_t RP = LL::RP;
     constexpr int SP = int(LL::SP);
-    constexpr int KR = (int(RP) + 31) / 32;  // K/V rows per loading thread
+    constexpr int NQ = LL::NQ, NV = LL::NV;
     constexpr int KC = (int(RP) + 31) / 32;  // softmax columns per lane
-    constexpr int NJ = (NTL + 3) / 4;         // S n8 tiles per warp
+    constexpr int NJ = (NTL + kWQ - 1) / kWQ;  // S n8 tiles per warp
+    constexpr int NA = NJ == 1 ? 2 : 1;       // S accumulators per tile (ILP when NJ == 1)
     static_assert(NTL % 2 == 0 && RP <= uint32_t(kKvMax), "K/V rows padded to a multiple of 16");
-    extern __shared__ __align__(128) uint8_t sm[];
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // query blocks of one position are adjacent in launch order: their shared K/V rows
-    // (the sampled globals, the overlapping window bands) are re-read from L2, not HBM
-    const uint32_t nqb = (nq + kQBlock - 1) / kQBlock;
-    const uint32_t p = blockIdx.x / nqb, qb = blockIdx.x - p * nqb;
-    const uint32_t a0 = qb * kQBlock;
-    const uint32_t nqh = min(uint32_t(kQBlock), nq - a0);
-    const uint32_t R = tt.kv_count[qb];
-    const uint32_t d = C / heads, nch = (d + kDC - 1) / kDC;
-    const uint64_t ld = 3ull * C;
     const uint32_t sbase = dev::smem_u32(sm);
+    uint64_t* qfull = reinterpret_cast<uint64_t*>(sm + LL::bars);
+    uint64_t* qempty = qfull + NQ;
+    uint64_t* vfull = qempty + NQ;
+    uint64_t* vempty = vfull + NV;
     float* sp = reinterpret_cast<float*>(sm + LL::sp);
-    float* zinv = reinterpret_cast<float*>(sm + LL::zinv);
 
-    // K/V pad rows [R, RP) of every slot and plane are never loaded: zero them once (P is 0
-    // there and must meet finite V values)
-    for (uint32_t i = tid; i < (RP - R) * 8; i += kThreads) {
-        const uint32_t off = swz(R + (i >> 3), i & 7);
-#pragma unroll
-        for (int st = 0; st < NS; ++st)
-#pragma unroll
-            for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                *reinterpret_cast<uint4*>(sm + st * LL::stage + LL::PL * LL::QT + pl * LL::KT + off) =
-                    make_uint4(0, 0, 0, 0);
+    // zero the ring and P once: rows no load of an item writes (K/V padding rows, Q rows
+    // past the block) then always hold finite values, and P = 0 meets finite V rows
+    for (uint32_t i = tid * 16; i < LL::bars; i += kThreads * 16)
+        *reinterpret_cast<uint4*>(sm + i) = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+        for (int s = 0; s < NQ; ++s) {
+            dev::mbar_init(&qfull[s], 1);
+            dev::mbar_init(&qempty[s], kConsumerWarps);
+        }
+        for (int s = 0; s < NV; ++s) {
+            dev::mbar_init(&vfull[s], 1);
+            dev::mbar_init(&vempty[s], kConsumerWarps);
+        }
+        dev::fence_barrier_init();
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeroed smem before TMA writes
+    __syncthreads();
+    dev::pdl_wait();
+    dev::pdl_trigger();
 
-    // this thread's 16-byte pieces of every Q / K / V chunk: piece lp of row lr (Q) and of
-    // rows lr + 32k (K/V)
-    const uint32_t lr = tid >> 3, lp = tid & 7;
-    const bool q_ok = lr < nqh;
-    const uint16_t* kvf = tt.kv_frames + qb * kKvMax;
-    const __nv_bfloat16* q_src = qkv + uint64_t((q_frame0 + a0 + min(lr, nqh - 1)) * HW + p) * ld + lp * 8;
-    const __nv_bfloat16* k_src[KR];
-#pragma unroll
-    for (int k = 0; k < KR; ++k)
-        k_src[k] = qkv + uint64_t(uint32_t(kvf[min(lr + 32 * k, R - 1)]) * HW + p) * ld + lp * 8;
-    uint32_t ld_h = 0, ld_w = 0, ld_slot = 0;
-    auto issue = [&]() {
-        if (ld_h < heads) {
-            const bool qk = ld_w < nch;
-            const uint32_t ch = qk ? ld_w : ld_w - nch;
-            const uint32_t col = ld_h * d + ch * kDC;
-            const uint32_t bytes = lp * 8 < d - ch * kDC ? 16u : 0u;  // zero-fill past the head dim
-            const uint32_t st = sbase + ld_slot * LL::stage;
-            if (qk && q_ok) {
-                cp_async16(st + swz(lr, lp), q_src + col, bytes);
-                if (SPLIT) cp_async16(st + LL::QT + swz(lr, lp), q_src + qkv_lo + col, bytes);
-            }
-            const uint32_t kc = (qk ? C : 2 * C) + col;
-#pragma unroll
-            for (int k = 0; k < KR; ++k) {
-                if (lr + 32 * k < R) {
-                    const uint32_t dst = st + LL::PL * LL::QT + swz(lr + 32 * k, lp);
-                    cp_async16(dst, k_src[k] + kc, bytes);
-                    if (SPLIT) cp_async16(dst + LL::KT, k_src[k] + qkv_lo + kc, bytes);
+    const uint32_t heads = a.heads, nch = a.nch;
+    if (warp == kConsumerWarps) {
+        // ---------------- producer: one thread issues every TMA load ----------------
+        if (lane != 0) return;
+        for (int pl = 0; pl < int(LL::PL); ++pl)
+            for (int k = 0; k < kBoxKinds; ++k) dev::tma_prefetch_desc(&maps.box[pl][k]);
+        Ring<NQ> rq;
+        Ring<NV> rv;
+        for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+            const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
+            const uint32_t nb = a.tt.kv_nbox[qb];
+            const uint32_t kvb = uint32_t(a.tt.kv_load_rows[qb]) * 128u * LL::PL;
+            const uint32_t* prog = a.tt.kv_box + size_t(qb) * kKvMax;
+            const uint32_t nqh = min(uint32_t(kQBlock), a.nq - qb * kQBlock);
+            const int32_t qf = int32_t(a.q_frame0 + qb * kQBlock);
+            for (uint32_t h = 0; h < heads; ++h) {
+                for (uint32_t ch = 0; ch < nch; ++ch, rq.next()) {  // S phase: Q + K chunks
+                    const int32_t c0 = int32_t(ch * kDC);
+                    dev::mbar_wait(&qempty[rq.slot], rq.phase ^ 1u);
+                    uint64_t* bar = &qfull[rq.slot];
+                    dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
+                    const uint32_t st = sbase + rq.slot * LL::QKST;
+                    // the block's query rows exactly: boxes of 16, 8, ... rows (32 = one box)
+                    for (uint32_t k = 0, r = 0; k < uint32_t(kBoxKinds); ++k)
+                        if (nqh & (32u >> k)) {
+                            for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                                tma_load_4d(st + pl * kQT + r * 128u, &maps.box[pl][k], bar, c0, int32_t(h),
+                                            int32_t(p), qf + int32_t(r));
+                            r += 32u >> k;
+                        }
+                    const int32_t c1 = int32_t(heads + h);
+                    for (uint32_t b = 0; b < nb; ++b) {
+                        const uint32_t e = prog[b];
+                        const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
+                        for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                            tma_load_4d(st + LL::PL * kQT + pl * LL::KT + row * 128u, &maps.box[pl][kind], bar,
+                                        c0, c1, int32_t(p), int32_t(e & 0xFFFFu));
+                    }
+                }
+                for (uint32_t ch = 0; ch < nch; ++ch, rv.next()) {  // PV phase: V chunks
+                    const int32_t c0 = int32_t(ch * kDC);
+                    dev::mbar_wait(&vempty[rv.slot], rv.phase ^ 1u);
+                    uint64_t* bar = &vfull[rv.slot];
+                    dev::mbar_arrive_expect_tx(bar, kvb);
+                    const uint32_t st = sbase + LL::vring + rv.slot * LL::VST;
+                    const int32_t c1 = int32_t(2 * heads + h);
+                    for (uint32_t b = 0; b < nb; ++b) {
+                        const uint32_t e = prog[b];
+                        const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
+                        for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                            tma_load_4d(st + pl * LL::KT + row * 128u, &maps.box[pl][kind], bar, c0, c1,
+                                        int32_t(p), int32_t(e & 0xFFFFu));
+                    }
                 }
             }
-            if (++ld_w == 2 * nch) {
-                ld_w = 0;
-                ++ld_h;
-            }
         }
-        cp_commit();
-        ld_slot = ld_slot + 1 == NS ? 0 : ld_slot + 1;
-    };
-#pragma unroll
-    for (int i = 0; i < NS - 1; ++i) issue();
+        return;
+    }
 
-    // per-lane ldmatrix offsets: the XOR swizzle only involves lane bits
-    const int mt = warp & 1, wq = warp >> 1;
+    // ---------------- consumers: warps 0 .. kConsumerWarps-1 ----------------
+    const int mt = warp & 1, wq = warp >> 1;  // m tile (16 queries), column group
     const uint32_t r7 = lane & 7, hb = lane >> 4, b1 = (lane >> 3) & 1;
     uint32_t a_off[4], b_off[4];
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
         a_off[kk] = (mt * 16 + r7 + b1 * 8) * 128 + (((kk * 2 + hb) ^ r7) << 4);
-        b_off[kk] = LL::PL * LL::QT + r7 * 128 + (((kk * 2 + b1) ^ r7) << 4);
+        b_off[kk] = LL::PL * kQT + r7 * 128 + (((kk * 2 + b1) ^ r7) << 4);
     }
-    const uint32_t v_off = LL::PL * LL::QT + (r7 + b1 * 8) * 128 + (((2 * wq + hb) ^ r7) << 4);
+    // V fragments (ldmatrix.trans) of n8 tiles kON*wq + 2i + {0, 1}, within a V stage
+    uint32_t v_off[kON / 2];
+#pragma unroll
+    for (int i = 0; i < kON / 2; ++i)
+        v_off[i] = (r7 + b1 * 8) * 128 + (((uint32_t(kON * wq + 2 * i) + hb) ^ r7) << 4);
     const int g = lane >> 2, t4 = lane & 3;
     auto p_addr = [&](int kq) {  // P fragment (A operand) of k16 step kq, plane 0
         return sbase + LL::pb + uint32_t(kq >> 2) * (kQBlock * 128) + (mt * 16 + r7 + b1 * 8) * 128 +
                ((((kq & 3) * 2 + hb) ^ r7) << 4);
     };
-    auto store_ctx = [&](uint32_t buf, uint32_t c0, uint32_t vw) {  // staged chunk -> ctx rows
-        if (tid < int(nqh) * 8) {
-            const uint32_t r = tid >> 3, c = tid & 7;
-            if (c * 8 < vw) {
-                const uint8_t* ost = sm + LL::ost + buf * (LL::PL * LL::QT);
-                const uint64_t o = (uint64_t(a0 + r) * HW + p) * C + c0 + c * 8;
-                *reinterpret_cast<uint4*>(ctx + o) = *reinterpret_cast<const uint4*>(ost + swz(r, c));
-                if (SPLIT)
-                    *reinterpret_cast<uint4*>(ctx + ctx_lo + o) =
-                        *reinterpret_cast<const uint4*>(ost + LL::QT + swz(r, c));
-            }
-        }
-    };
-
-    uint32_t cslot = 0, och = 0;
-    for (uint32_t h = 0; h < heads; ++h) {
-        // ---------------- S = Q K^T ----------------
-        // warp: m tile mt (16 queries) x n8 tiles wq, wq + 4, ... of the RP key columns
-        float acc[NJ][4];
+    const float bw = a.tt.wflag ? a.bias : 0.f, bg = a.tt.gflag ? a.bias : 0.f;
+    const uint64_t ldc = a.C;
+    Ring<NQ> rq;
+    Ring<NV> rv;
+    for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+        const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
+        const uint32_t a0 = qb * kQBlock;
+        const uint32_t nqh = min(uint32_t(kQBlock), a.nq - a0);
+        const uint32_t R = a.tt.kv_count[qb];
+        const uint8_t* gm = a.tt.gmult + size_t(qb) * kKvMax;
+        for (uint32_t h = 0; h < heads; ++h) {
+            // ---------------- S = Q K^T ----------------
+            // warp: m tile mt (16 queries) x n8 tiles wq, wq + kWQ, ... of the RP key columns
+            float acc[NJ][NA][4];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-        for (uint32_t ch = 0; ch < nch; ++ch) {
-            cp_wait<NS - 2>();
-            __syncthreads();
-            issue();
-            const uint32_t st = sbase + cslot * LL::stage;
-            cslot = cslot + 1 == NS ? 0 : cslot + 1;
-            const uint32_t vw = min(uint32_t(kDC), d - ch * kDC);
+            for (int j = 0; j < NJ; ++j)
 #pragma unroll
-            for (int kk = 0; kk < kDC / 16; ++kk) {
-                if (kk * 16 >= int(vw)) break;  // zero-filled past the head dim
-                uint32_t a[4], al[4];
-                ldsm_x4(st + a_off[kk], a);
-                if (SPLIT) ldsm_x4(st + LL::QT + a_off[kk], al);
+                for (int x = 0; x < NA; ++x) acc[j][x][0] = acc[j][x][1] = acc[j][x][2] = acc[j][x][3] = 0.f;
+            for (uint32_t ch = 0; ch < nch; ++ch, rq.next()) {
+                dev::mbar_wait(&qfull[rq.slot], rq.phase);
+                const uint32_t st = sbase + rq.slot * LL::QKST;
+                const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    if (wq + 4 * j < NTL) {
-                        uint32_t k0, k1;
-                        ldsm_x2(st + b_off[kk] + (wq + 4 * j) * 1024, k0, k1);
-                        mma_bf16(acc[j], a, k0, k1);
-                        if (SPLIT) {
-                            uint32_t l0, l1;
-                            ldsm_x2(st + LL::KT + b_off[kk] + (wq + 4 * j) * 1024, l0, l1);
-                            mma_bf16(acc[j], a, l0, l1);
-                            mma_bf16(acc[j], al, k0, k1);
+                for (int kk = 0; kk < kDC / 16; ++kk) {
+                    if (kk * 16 >= int(vw)) break;  // zero-filled past the head dim
+                    uint32_t qa[4], ql[4];
+                    ldsm_x4(st + a_off[kk], qa);
+                    if (SPLIT) ldsm_x4(st + kQT + a_off[kk], ql);
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) {
+                        if (wq + kWQ * j < NTL) {
+                            float(&c)[4] = acc[j][NA == 2 ? (kk & 1) : 0];
+                            uint32_t k0, k1;
+                            ldsm_x2(st + b_off[kk] + (wq + kWQ * j) * 1024, k0, k1);
+                            mma_bf16(c, qa, k0, k1);
+                            if (SPLIT) {
+                                uint32_t l0, l1;
+                                ldsm_x2(st + LL::KT + b_off[kk] + (wq + kWQ * j) * 1024, l0, l1);
+                                mma_bf16(c, qa, l0, l1);
+                                mma_bf16(c, ql, k0, k1);
+                            }
                         }
                     }
                 }
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(&qempty[rq.slot]);
             }
-        }
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int nt = wq + 4 * j;
-            if (nt < NTL) {
-                const int col = nt * 8 + t4 * 2;
-                *reinterpret_cast<float2*>(&sp[(mt * 16 + g) * SP + col]) = make_float2(acc[j][0], acc[j][1]);
-                *reinterpret_cast<float2*>(&sp[(mt * 16 + g + 8) * SP + col]) = make_float2(acc[j][2], acc[j][3]);
+            for (int j = 0; j < NJ; ++j) {
+                const int nt = wq + kWQ * j;
+                if (nt < NTL) {
+                    float v[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[e] = NA == 2 ? acc[j][0][e] + acc[j][NA - 1][e] : acc[j][0][e];
+                    const int col = nt * 8 + t4 * 2;
+                    *reinterpret_cast<float2*>(&sp[(mt * 16 + g) * SP + col]) = make_float2(v[0], v[1]);
+                    *reinterpret_cast<float2*>(&sp[(mt * 16 + g + 8) * SP + col]) = make_float2(v[2], v[3]);
+                }
             }
-        }
-        __syncthreads();
-        // ---------------- softmax over the token lists, per column -> P (in place) ----------
-        // The reference's token list (window, then globals, duplicates kept; ops.cpp:209-241)
-        // in column form: column c carries the window token iff wlo <= c <= whi and gmult[c]
-        // global tokens; p_c = [window] e^(l_w - m) + gmult[c] e^(l_g - m), summed one token
-        // at a time. Lane l owns columns l + 32k: no token-list walk, no smem atomics.
-        for (uint32_t a = warp; a < uint32_t(kQBlock); a += kWarps) {
-            float* row = sp + a * SP;
-            float pv[KC];
-            float zi = 0.f;
-#pragma unroll
-            for (int k = 0; k < KC; ++k) pv[k] = 0.f;
-            if (a < nqh) {
-                const uint32_t qa = a0 + a;
-                const int lo = tt.wlo[qa], hi = tt.whi[qa];
-                const uint8_t* gm = tt.gmult + size_t(qb) * kKvMax;
-                const float bw = tt.wflag ? bias : 0.f, bg = tt.gflag ? bias : 0.f;
-                float sv[KC];
+            dev::named_bar(1, kConsumerWarps * 32);
+            // ---------------- softmax over the token lists, per row -> P (bf16) ----------
+            // Column c of the block's K/V list carries query qa's window token iff
+            // wlo <= c <= whi, and gmult[c] global tokens; p_c = [window] e^(l_w - m) +
+            // gmult[c] e^(l_g - m), summed one token at a time. A warp owns whole rows.
+            for (uint32_t r = warp; r < nqh; r += kConsumerWarps) {
+                const float* row = sp + r * SP;
+                const uint32_t qa = a0 + r;
+                const int lo = a.tt.wlo[qa], hi = a.tt.whi[qa];
+                float sv[KC], pv[KC];
                 bool inw[KC];
                 int ng[KC];
                 float m = -INFINITY;
@@ -299,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
                 for (int k = 0; k < KC; ++k) {
                     const int c = lane + 32 * k;
                     const bool ok = c < int(R);
-                    sv[k] = ok ? scale * row[c] : 0.f;
+                    sv[k] = ok ? a.scale * row[c] : 0.f;
                     inw[k] = ok && c >= lo && c <= hi;
                     ng[k] = ok ? gm[c] : 0;
                     if (inw[k]) m = fmaxf(m, sv[k] + bw);
@@ -320,148 +374,179 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-                zi = 1.0f / z;
-            }
-            __syncwarp();
+                const float zi = 1.0f / z;
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const int c = lane + 32 * k;
-                if (c < SP) row[c] = pv[k];
+                for (int k = 0; k < KC; ++k) {
+                    const uint32_t c = lane + 32 * k;
+                    if (c < RP) {
+                        const uint32_t off = LL::pb + (c >> 6) * (kQBlock * 128) + swz(r, (c & 63) >> 3) + (c & 7) * 2;
+                        const float v = pv[k] * zi;
+                        const __nv_bfloat16 vh = __float2bfloat16_rn(v);
+                        *reinterpret_cast<__nv_bfloat16*>(sm + off) = vh;
+                        if (SPLIT)
+                            *reinterpret_cast<__nv_bfloat16*>(sm + off + LL::PB) =
+                                __float2bfloat16_rn(v - __bfloat162float(vh));
+                    }
+                }
             }
-            if (lane < SP - 32 * KC) row[32 * KC + lane] = 0.f;
-            if (lane == 0) zinv[a] = zi;
-        }
-        __syncthreads();
-        // P = S_normalised -> bf16 planes (64-column blocks in the swizzled row layout)
-        for (int i = tid; i < int(kQBlock * RP / 8); i += kThreads) {
-            const uint32_t r = i / (RP / 8), c8 = i % (RP / 8);
-            const float zi = zinv[r];
-            const float4 s0 = *reinterpret_cast<const float4*>(sp + r * SP + c8 * 8);
-            const float4 s1 = *reinterpret_cast<const float4*>(sp + r * SP + c8 * 8 + 4);
-            const float v[8] = {s0.x * zi, s0.y * zi, s0.z * zi, s0.w * zi,
-                                s1.x * zi, s1.y * zi, s1.z * zi, s1.w * zi};
-            const uint32_t off = LL::pb + (c8 >> 3) * (kQBlock * 128) + swz(r, c8 & 7);
-            uint32_t w[4], wl[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (SPLIT)
-                    split2(v[2 * k], v[2 * k + 1], w[k], wl[k]);
-                else
-                    w[k] = pack_bf16(v[2 * k], v[2 * k + 1]);
-            }
-            *reinterpret_cast<uint4*>(sm + off) = make_uint4(w[0], w[1], w[2], w[3]);
-            if (SPLIT) *reinterpret_cast<uint4*>(sm + off + LL::PB) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
-        }
-        __syncthreads();
-        // ---------------- ctx = P V ----------------
-        // warp: m tile mt, n8 tiles 2wq, 2wq + 1 of each 64-wide output chunk
-        uint32_t pa[LL::PREG ? NTL / 2 : 1][4], pal[LL::PREG && SPLIT ? NTL / 2 : 1][4];
-        if (LL::PREG) {
-#pragma unroll
-            for (int kq = 0; kq < NTL / 2; ++kq) {
-                ldsm_x4(p_addr(kq), pa[LL::PREG ? kq : 0]);
-                if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pal[LL::PREG && SPLIT ? kq : 0]);
-            }
-        }
-        for (uint32_t ch = 0; ch < nch; ++ch, ++och) {
-            cp_wait<NS - 2>();
-            __syncthreads();
-            if (ch > 0) store_ctx((och - 1) & 1, h * d + (ch - 1) * kDC, min(uint32_t(kDC), d - (ch - 1) * kDC));
-            issue();
-            const uint32_t st = sbase + cslot * LL::stage;
-            cslot = cslot + 1 == NS ? 0 : cslot + 1;
-            const uint32_t vw = min(uint32_t(kDC), d - ch * kDC);
-            float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-            if (uint32_t(wq) * 16 < vw) {  // this warp's 16 output columns hold data
+            dev::named_bar(1, kConsumerWarps * 32);
+            // ---------------- ctx = P V ----------------
+            // warp: m tile mt, n8 tiles kON*wq .. kON*wq + kON-1 of each 64-wide output chunk;
+            // the tile goes through a per-warp staging block to 16-byte row stores
+            uint32_t pa[LL::PREG ? NTL / 2 : 1][4], pal[LL::PREG && SPLIT ? NTL / 2 : 1][4];
+            if (LL::PREG) {
 #pragma unroll
                 for (int kq = 0; kq < NTL / 2; ++kq) {
-                    uint32_t b[4], bl[4], a[4], al[4];
-                    ldsm_x4_t(st + v_off + kq * 2048, b);
-                    if (LL::PREG) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) a[k] = pa[LL::PREG ? kq : 0][k];
-                        if (SPLIT)
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) al[k] = pal[LL::PREG && SPLIT ? kq : 0][k];
-                    } else {
-                        ldsm_x4(p_addr(kq), a);
-                        if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, al);
-                    }
-                    mma_bf16(o[0], a, b[0], b[1]);
-                    mma_bf16(o[1], a, b[2], b[3]);
-                    if (SPLIT) {
-                        ldsm_x4_t(st + LL::KT + v_off + kq * 2048, bl);
-                        mma_bf16(o[0], a, bl[0], bl[1]);
-                        mma_bf16(o[1], a, bl[2], bl[3]);
-                        mma_bf16(o[0], al, b[0], b[1]);
-                        mma_bf16(o[1], al, b[2], b[3]);
-                    }
+                    ldsm_x4(p_addr(kq), pa[LL::PREG ? kq : 0]);
+                    if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pal[LL::PREG && SPLIT ? kq : 0]);
                 }
             }
-            uint8_t* ost = sm + LL::ost + (och & 1) * (LL::PL * LL::QT);
+            uint8_t* ost = sm + LL::ost + warp * LL::OST;
+            for (uint32_t ch = 0; ch < nch; ++ch, rv.next()) {
+                dev::mbar_wait(&vfull[rv.slot], rv.phase);
+                const uint32_t st = sbase + LL::vring + rv.slot * LL::VST;
+                const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
+                const uint32_t c0w = uint32_t(wq) * kON * 8;  // this warp's first column in the chunk
+                const bool live = c0w < vw;
+                float o[kON][4];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const uint32_t col = (2 * wq + j) * 8 + t4 * 2;
-                const uint32_t r0 = mt * 16 + g;
-                const uint32_t o0 = swz(r0, col >> 3) + (col & 7) * 2, o1 = swz(r0 + 8, col >> 3) + (col & 7) * 2;
-                if (SPLIT) {
-                    uint32_t h0, l0, h1, l1;
-                    split2(o[j][0], o[j][1], h0, l0);
-                    split2(o[j][2], o[j][3], h1, l1);
-                    *reinterpret_cast<uint32_t*>(ost + o0) = h0;
-                    *reinterpret_cast<uint32_t*>(ost + o1) = h1;
-                    *reinterpret_cast<uint32_t*>(ost + LL::QT + o0) = l0;
-                    *reinterpret_cast<uint32_t*>(ost + LL::QT + o1) = l1;
-                } else {
-                    *reinterpret_cast<uint32_t*>(ost + o0) = pack_bf16(o[j][0], o[j][1]);
-                    *reinterpret_cast<uint32_t*>(ost + o1) = pack_bf16(o[j][2], o[j][3]);
+                for (int n = 0; n < kON; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+                if (live) {
+#pragma unroll
+                    for (int kq = 0; kq < NTL / 2; ++kq) {
+                        uint32_t pf[4], pfl[4];
+                        if (LL::PREG) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) pf[k] = pa[LL::PREG ? kq : 0][k];
+                            if (SPLIT)
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) pfl[k] = pal[LL::PREG && SPLIT ? kq : 0][k];
+                        } else {
+                            ldsm_x4(p_addr(kq), pf);
+                            if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pfl);
+                        }
+#pragma unroll
+                        for (int i2 = 0; i2 < kON / 2; ++i2) {
+                            uint32_t b[4];
+                            ldsm_x4_t(st + v_off[i2] + kq * 2048, b);
+                            mma_bf16(o[2 * i2], pf, b[0], b[1]);
+                            mma_bf16(o[2 * i2 + 1], pf, b[2], b[3]);
+                            if (SPLIT) {
+                                uint32_t bl[4];
+                                ldsm_x4_t(st + LL::KT + v_off[i2] + kq * 2048, bl);
+                                mma_bf16(o[2 * i2], pf, bl[0], bl[1]);
+                                mma_bf16(o[2 * i2 + 1], pf, bl[2], bl[3]);
+                                mma_bf16(o[2 * i2], pfl, b[0], b[1]);
+                                mma_bf16(o[2 * i2 + 1], pfl, b[2], b[3]);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(&vempty[rv.slot]);
+                if (live) {
+                    // accumulators -> staging [16 rows][kON*8 cols] (bf16; lo plane after it)
+#pragma unroll
+                    for (int n = 0; n < kON; ++n) {
+                        const uint32_t o0 = uint32_t(g) * kOPitch + (n * 8 + t4 * 2) * 2, o1 = o0 + 8 * kOPitch;
+                        if (SPLIT) {
+                            uint32_t h0, l0, h1, l1;
+                            split2(o[n][0], o[n][1], h0, l0);
+                            split2(o[n][2], o[n][3], h1, l1);
+                            *reinterpret_cast<uint32_t*>(ost + o0) = h0;
+                            *reinterpret_cast<uint32_t*>(ost + o1) = h1;
+                            *reinterpret_cast<uint32_t*>(ost + 16 * kOPitch + o0) = l0;
+                            *reinterpret_cast<uint32_t*>(ost + 16 * kOPitch + o1) = l1;
+                        } else {
+                            *reinterpret_cast<uint32_t*>(ost + o0) = pack_bf16(o[n][0], o[n][1]);
+                            *reinterpret_cast<uint32_t*>(ost + o1) = pack_bf16(o[n][2], o[n][3]);
+                        }
+                    }
+                    __syncwarp();
+                    // 16 rows x kON 16-byte pieces: row r -> query a0 + 16 mt + r
+                    constexpr int kPieces = 16 * kON;
+#pragma unroll
+                    for (int i2 = 0; i2 < (kPieces + 31) / 32; ++i2) {
+                        const uint32_t pc = lane + 32 * i2;
+                        const uint32_t r = pc / kON, part = pc % kON;
+                        const uint32_t q = mt * 16 + r, col = c0w + part * 8;
+                        if (pc < uint32_t(kPieces) && q < nqh && col < vw) {
+                            __nv_bfloat16* dst =
+                                a.ctx + (uint64_t(a0 + q) * a.HW + p) * ldc + h * a.d + ch * kDC + col;
+                            *reinterpret_cast<uint4*>(dst) =
+                                *reinterpret_cast<const uint4*>(ost + r * kOPitch + part * 16);
+                            if (SPLIT)
+                                *reinterpret_cast<uint4*>(dst + a.ctx_lo) =
+                                    *reinterpret_cast<const uint4*>(ost + 16 * kOPitch + r * kOPitch + part * 16);
+                        }
+                    }
+                    __syncwarp();  // staging is rewritten by the next chunk
                 }
             }
         }
-        __syncthreads();
-        store_ctx((och - 1) & 1, h * d + (nch - 1) * kDC, min(uint32_t(kDC), d - (nch - 1) * kDC));
-        // the staging buffer and S / P scratch are rewritten only after the next head's
-        // first S-phase barrier
     }
-    cp_wait<0>();
 }
 
-template <int NTL, int NS, bool SPLIT>
-int launch_core(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
-                uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
-                cudaStream_t s) {
-    using LL = CoreLay<NTL, NS, SPLIT>;
-    static_assert(LL::total <= 227 * 1024, "attention core shared memory");
+int g_sms = 0;
+
+// 4-D view of the [frames][HW][3 x heads][d] Q/K/V buffer (one bf16 plane): boxes of
+// {64 head-dim elements, 1 head, 1 position, 32 >> kind frames}, 128-byte swizzle; head-dim
+// elements past d read as zero.
+int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames, uint32_t HW, uint32_t C,
+              uint32_t heads) {
+    auto fn = get_encode_fn();
+    if (!fn) return int(cudaErrorNotSupported);
+    const uint32_t d = C / heads;
+    for (int pl = 0; pl < 2; ++pl) {
+        const void* base = pl == 0 ? qkv : qkv_lo;
+        for (int k = 0; k < kBoxKinds; ++k) {
+            if (!base) {
+                m.box[pl][k] = m.box[0][k];
+                continue;
+            }
+            cuuint64_t gdim[4] = {d, 3ull * heads, HW, frames};
+            // frame-major [frames][HW][3C] rows (position stride 3C, frame stride HW 3C), or
+            // position-major [HW][frames][3C] (diagnostics: g_attn_pos_major)
+            const uint64_t row = uint64_t(C) * 3 * 2;
+            cuuint64_t gstride[3] = {uint64_t(d) * 2, g_attn_pos_major ? row * frames : row,
+                                     g_attn_pos_major ? row : row * HW};
+            cuuint32_t box[4] = {uint32_t(kDC), 1, 1, 32u >> k};
+            cuuint32_t estride[4] = {1, 1, 1, 1};
+            const CUresult r = fn(&m.box[pl][k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim,
+                                  gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
+        }
+    }
+    return 0;
+}
+
+template <int NTL, bool SPLIT>
+int launch_core(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
+    using LL = CoreLay<NTL, SPLIT>;
     static bool attr = false;
     if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, NS, SPLIT>,
+        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, SPLIT>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(LL::total));
         if (e != cudaSuccess) return int(e);
         attr = true;
     }
-    dim3 grid(HW * ((nq + kQBlock - 1) / kQBlock));
-    return int(launch_pdl(attention_core_kernel<NTL, NS, SPLIT>, grid, dim3(kThreads), LL::total, s,
-                          static_cast<const __nv_bfloat16*>(qkv), qkv_lo, HW, C, heads, nq, q_frame0, tt,
-                          scale, bias, static_cast<__nv_bfloat16*>(ctx), ctx_lo));
-}
-
-// ring depth per (K/V width, mode): deep rings for the narrow tiles (4 CTAs/SM at cfg2),
-// shallower where one CTA's tiles are wide
-template <int NTL, bool SPLIT>
-int launch_ntl(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
-               uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
-               cudaStream_t s) {
-    constexpr int NS = NTL <= 4 ? 5 : (NTL <= 8 ? 4 : (SPLIT ? 2 : 3));
-    return launch_core<NTL, NS, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s);
+    if (g_sms == 0) {
+        int dv = 0;
+        cudaGetDevice(&dv);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dv);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    const uint32_t slots = uint32_t(g_sms) * LL::ctas;
+    const uint32_t grid = args.items < slots ? args.items : slots;
+    return int(launch_pdl(attention_core_kernel<NTL, SPLIT>, dim3(grid), dim3(kThreads), LL::total, s, maps, args));
 }
 
 template <bool SPLIT>
-int launch_mode(uint32_t RP, const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
-                uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx,
-                int64_t ctx_lo, cudaStream_t s) {
+int launch_mode(uint32_t RP, const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
 #define CORE(NTL) \
     case NTL * 8: \
-        return launch_ntl<NTL, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s)
+        return launch_core<NTL, SPLIT>(maps, args, s)
     switch (RP) {
         CORE(2); CORE(4); CORE(6); CORE(8); CORE(10); CORE(12);
         CORE(14); CORE(16); CORE(18); CORE(20); CORE(22); CORE(24);
@@ -477,21 +562,70 @@ bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt) 
            tt.max_kv <= kKvMax;
 }
 
-int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
-                          uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias,
-                          void* ctx, void* ctx_lo, cudaStream_t s) {
-    if (HW == 0 || !qkv || !ctx || (qkv_lo == nullptr) != (ctx_lo == nullptr))
-        return int(cudaErrorInvalidValue);
+int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_frames, uint32_t HW, uint32_t C,
+                          uint32_t heads, uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale,
+                          float bias, void* ctx, void* ctx_lo, cudaStream_t s) {
+    if (HW == 0 || !qkv || !ctx || (qkv_lo == nullptr) != (ctx_lo == nullptr)) return int(cudaErrorInvalidValue);
     if (nq == 0) return 0;
     if (!attention_core_supported(C, heads, tt)) return int(cudaErrorInvalidValue);
+    if (reinterpret_cast<uintptr_t>(qkv) % 16 || reinterpret_cast<uintptr_t>(qkv_lo) % 16)
+        return int(cudaErrorInvalidValue);
+    AttnMaps maps;
+    const int rc = make_maps(maps, qkv, qkv_lo, qkv_frames, HW, C, heads);
+    if (rc) return rc;
+    AttnArgs args;
+    args.HW = HW;
+    args.C = C;
+    args.heads = heads;
+    args.d = C / heads;
+    args.nch = (args.d + kDC - 1) / kDC;
+    args.nq = nq;
+    args.nqb = (nq + kQBlock - 1) / kQBlock;
+    args.q_frame0 = q_frame0;
+    args.items = HW * args.nqb;
+    args.scale = scale;
+    args.bias = bias;
+    args.ctx = static_cast<__nv_bfloat16*>(ctx);
+    args.ctx_lo = ctx_lo ? static_cast<__nv_bfloat16*>(ctx_lo) - static_cast<__nv_bfloat16*>(ctx) : 0;
+    args.tt = tt;
     const uint32_t RP = (uint32_t(tt.max_kv) + 15) & ~15u;
-    using bf = __nv_bfloat16;
-    if (qkv_lo) {
-        const int64_t ql = static_cast<const bf*>(qkv_lo) - static_cast<const bf*>(qkv);
-        const int64_t cl = static_cast<bf*>(ctx_lo) - static_cast<bf*>(ctx);
-        return launch_mode<true>(RP, qkv, ql, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, cl, s);
+    return qkv_lo ? launch_mode<true>(RP, maps, args, s) : launch_mode<false>(RP, maps, args, s);
+}
+
+namespace {
+__global__ void read_bw_kernel(const uint4* __restrict__ p, uint64_t n, uint32_t* sink) {
+    uint32_t acc = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint4 v = __ldcs(p + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
     }
-    return launch_mode<false>(RP, qkv, 0, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, 0, s);
+    if (acc == 0x12345678u) *sink = acc;
+}
+}  // namespace
+
+// Diagnostics: streaming 16-byte loads over `bytes` (average ms over iters).
+int read_bw_bench(uint64_t bytes, int iters, float* ms) {
+    void* buf = nullptr;
+    if (cudaMalloc(&buf, bytes + 64) != cudaSuccess) return int(cudaErrorMemoryAllocation);
+    cudaMemset(buf, 1, bytes + 64);
+    if (g_sms == 0) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const uint64_t n = bytes / 16;
+    read_bw_kernel<<<g_sms * 8, 256>>>(static_cast<const uint4*>(buf), n, static_cast<uint32_t*>(buf) + bytes / 4);
+    cudaEventRecord(a);
+    for (int i = 0; i < iters; ++i)
+        read_bw_kernel<<<g_sms * 8, 256>>>(static_cast<const uint4*>(buf), n, static_cast<uint32_t*>(buf) + bytes / 4);
+    cudaEventRecord(b);
+    const cudaError_t e = cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    *ms = t / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    return int(e);
 }
 
 }  // namespace vinf

@@ -1,0 +1,87 @@
+// Diagnostics (not on the product path): micro-benchmarks of the attention core on a
+// single-worker engine layout's token table, and a streaming-read bandwidth probe.
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <vector>
+
+#include "host.hpp"
+#include "layout.hpp"
+#include "ops.hpp"
+
+namespace vinf {
+int guarded_call(const std::function<void()>& f);
+int read_bw_bench(uint64_t bytes, int iters, float* ms);
+}  // namespace vinf
+
+using namespace vinf;
+
+extern "C" {
+
+int vinf_read_bw_bench(uint64_t bytes, int iters, float* ms) {
+    return guarded_call([&] {
+        if (!ms || iters <= 0 || bytes < 16) shape_error("bad arguments");
+        cuda_check(read_bw_bench(bytes, iters, ms), "read bandwidth probe");
+    });
+}
+
+// The attention core alone over the Q/K/V buffer of a single-worker engine layout
+// (t > t_star token table), average ms over iters launches; pos_major = 1 views the
+// buffer as [HW][frames][3C] instead of [frames][HW][3C].
+int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint32_t channels, uint32_t heads,
+                         uint32_t n_local, uint32_t n_global, int f32, int pos_major, int iters, float* ms) {
+    return guarded_call([&] {
+        if (!ms || iters <= 0) shape_error("bad arguments");
+        vinf_engine_desc d{};
+        d.frames = frames;
+        d.workers = 1;
+        d.height = height;
+        d.width = width;
+        d.channels = channels;
+        d.taps = 3;
+        d.groups = 8;
+        d.heads = heads;
+        d.n_local = n_local;
+        d.n_global = n_global;
+        d.bias = 10.f;
+        d.t_star = 800.0;
+        d.epsilon = 1e-5f;
+        d.blocks = 1;
+        d.dtype = f32 ? VINF_F32 : VINF_BF16;
+        Layout L(d);
+        DevTokens tok;
+        cudaStream_t s = nullptr;
+        cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+        tok.upload(L.tok[1], s);
+        const uint64_t plane = uint64_t(L.af) * L.hw * 3 * channels;
+        const uint64_t ctxn = uint64_t(L.f_clip) * L.hw * channels;
+        TmpBuf qkv(plane * 2 * (f32 ? 2 : 1), s), ctx(ctxn * 2 * (f32 ? 2 : 1), s);
+        cuda_check(cudaMemsetAsync(qkv.p, 0x3c, plane * 2 * (f32 ? 2 : 1), s), "fill");
+        auto* q = static_cast<__nv_bfloat16*>(qkv.p);
+        auto* c = static_cast<__nv_bfloat16*>(ctx.p);
+        g_attn_pos_major = pos_major;
+        auto launch = [&] {
+            cuda_check(launch_attention_core(q, f32 ? q + plane : nullptr, L.af, L.hw, channels, heads, L.f_clip,
+                                             L.ha, tok.tt, L.scale, d.bias, c, f32 ? c + ctxn : nullptr, s),
+                       "attention core");
+        };
+        launch();
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        for (int i = 0; i < iters; ++i) launch();
+        cudaEventRecord(b, s);
+        cuda_check(cudaEventSynchronize(b), "attention bench");
+        cudaEventElapsedTime(ms, a, b);
+        *ms /= float(iters);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        g_attn_pos_major = 0;
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        tok.release();
+        cudaStreamDestroy(s);
+    });
+}
+
+}  // extern "C"

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <functional>
 
+#include "comm.hpp"
 #include "host.hpp"
 #include "layout.hpp"
 #include "ops.hpp"
@@ -57,17 +58,31 @@ struct vinf_engine {
     // on a private stream (the caller's may be the legacy stream), launched on the caller's.
     struct Graph {
         cudaGraphExec_t exec = nullptr;
-        uint64_t nlaunch = 0;
+        uint64_t nlaunch = 0, nbytes = 0, nmsgs = 0;
         int calls = 0;
     };
     Graph graphs[2];
     cudaStream_t cap_stream = nullptr;
+    // Clip-parallel executor (vinf_engine_forward_dist): the exchanges run on a side
+    // stream, ordered against the compute stream by events; the exchange lists are sorted
+    // once into the order both ends of a message pair post them.
+    struct Dist {
+        cudaStream_t cs = nullptr;
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        std::vector<vinf_xfer> xconv, xattn;
+        Graph graphs[2];
+        const vinf_comm* graph_comm = nullptr;
+    } dist;
+    void dist_init();
+    void dist_block(uint32_t b, double t, vinf_comm* comm, cudaStream_t s);
     bool use_graphs = getenv("VINF_NO_GRAPH") == nullptr;
     void drop_graphs() {
-        for (auto& g : graphs) {
-            if (g.exec) cudaGraphExecDestroy(g.exec);
-            g = Graph{};
-        }
+        for (Graph* gs : {graphs, dist.graphs})
+            for (int i = 0; i < 2; ++i) {
+                if (gs[i].exec) cudaGraphExecDestroy(gs[i].exec);
+                gs[i] = Graph{};
+            }
+        dist.graph_comm = nullptr;
     }
 
     // Optional per-kernel timing: CUDA events recorded on the launching stream around
@@ -129,7 +144,8 @@ struct vinf_engine {
             if (!x.send) cuda_check(cudaMemsetAsync(ws + x.offset, 0, x.bytes, s), "ablation zero");
     }
 
-    void stage_stub(uint32_t b, cudaStream_t s);
+    void stage_stub(uint32_t b, cudaStream_t s) { stub_frames(b, 0, L.f_clip, s); }
+    void stub_frames(uint32_t b, uint32_t f0, uint32_t nf, cudaStream_t s);  // own frames [f0, f0+nf)
     void stage_conv(uint32_t b, cudaStream_t s);
     void stage_gn_apply(uint32_t b, cudaStream_t s);
     void stage_attention(uint32_t b, double t, cudaStream_t s);
@@ -159,19 +175,20 @@ struct vinf_engine {
     float* gn_aff() const { return at<float>(L.off_gnaff); }  // [s; t; b'(3C)]
 };
 
-void vinf_engine::stage_stub(uint32_t b, cudaStream_t s) {
+void vinf_engine::stub_frames(uint32_t b, uint32_t f0, uint32_t nf, cudaStream_t s) {
+    if (!nf) return;
     const EngineBlock& B = blocks.at(b);
-    const uint64_t n = clip_elems();
-    auto* u0 = at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E;
+    const uint64_t n = uint64_t(nf) * L.E, off = uint64_t(f0) * L.E;
+    auto* u0 = at<__nv_bfloat16>(L.off_u0) + uint64_t(L.hc) * L.E + off;
+    const void* x = static_cast<const uint8_t*>(x_of(b)) + off * (f32() ? 4 : 2);
     Span span(this, "stub", s);
     if (f32()) {
-        auto* lo = at<__nv_bfloat16>(L.off_u0lo) + uint64_t(L.hc) * L.E;
-        cuda_check(launch_stub(x_of(b), false, n, L.d.channels, B.stub_a(), B.stub_c(),
-                               at(L.off_u0f), false, u0, lo, s),
+        auto* lo = at<__nv_bfloat16>(L.off_u0lo) + uint64_t(L.hc) * L.E + off;
+        cuda_check(launch_stub(x, false, n, L.d.channels, B.stub_a(), B.stub_c(), at<float>(L.off_u0f) + off,
+                               false, u0, lo, s),
                    "stub");
     } else {
-        cuda_check(launch_stub(x_of(b), true, n, L.d.channels, B.stub_a(), B.stub_c(), u0, true,
-                               nullptr, nullptr, s),
+        cuda_check(launch_stub(x, true, n, L.d.channels, B.stub_a(), B.stub_c(), u0, true, nullptr, nullptr, s),
                    "stub");
     }
     ++launches;
@@ -318,7 +335,7 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
         }
         Span span(this, "attn_core", s);
         const uint64_t plane = uint64_t(L.af) * hw * 3 * C;
-        cuda_check(launch_attention_core(qkv, f32() ? qkv + plane : nullptr, L.hw, C, L.d.heads, L.f_clip, L.ha,
+        cuda_check(launch_attention_core(qkv, f32() ? qkv + plane : nullptr, L.af, L.hw, C, L.d.heads, L.f_clip, L.ha,
                                          tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale, L.d.bias, ctx,
                                          ctxlo, s),
                    "attention core");
@@ -345,6 +362,148 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
     gemm(O, {0}, B.wo, {0}, int64_t(L.f_clip) * hw, C, ep, f32(), s);
     ++launches;
 }
+
+
+// ---- clip-parallel executor ----------------------------------------------------------
+
+void vinf_engine::dist_init() {
+    if (dist.cs) return;
+    int lo = 0, hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+    // the exchanges' copy / NCCL kernels are scheduled ahead of queued compute blocks
+    cuda_check(cudaStreamCreateWithPriority(&dist.cs, cudaStreamNonBlocking, hi), "comm stream");
+    for (auto& e : dist.ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    dist.xconv = matching_order(L.xconv);
+    dist.xattn = matching_order(L.xattn);
+}
+
+// One block of eps_theta_worker (pipeline.cpp:150-170) with the paper's 3-step sync:
+//  1. conv halo: the clip's boundary frames are stubbed first and shipped on the comm
+//     stream while the interior frames are stubbed (sync_contexts T2/T3,
+//     clip_parallel.cpp:160-188, minus the even/odd staging NVSwitch does not need);
+//  2. GroupNorm: one all-reduce of the 2*groups (sum, sum of squares) partials on the
+//     compute stream (the reference's two all-gather rounds, clip_parallel.cpp:242-253);
+//  3. attention context: halo frames + the sampled global frames each receiver lacks
+//     (T1, clip_parallel.cpp:114-148) on the comm stream while the own frames are
+//     projected to Q/K/V; their K/V projection and the attention core wait for it.
+// Every comm-stream operation starts after an event of the compute stream and the
+// compute stream waits for it before the receive slots are read, so all communicator
+// operations of a worker are ordered in time (one communicator serves both streams).
+void vinf_engine::dist_block(uint32_t b, double t, vinf_comm* comm, cudaStream_t s) {
+    const bool multi = comm->nranks > 1;
+    cudaStream_t cs = dist.cs;
+    const bool x_conv = multi && ablate != VINF_ABLATE_CONV && !dist.xconv.empty();
+    if (x_conv) {
+        const uint32_t h = L.hc, fc = L.f_clip;
+        const bool split = 2 * h < fc;
+        if (split) {
+            stub_frames(b, 0, h, s);
+            stub_frames(b, fc - h, h, s);
+        } else {
+            stage_stub(b, s);
+        }
+        cuda_check(cudaEventRecord(dist.ev[0], s), "event");
+        cuda_check(cudaStreamWaitEvent(cs, dist.ev[0], 0), "wait");
+        {
+            Span span(this, "xchg_conv", cs);
+            run_exchange(comm, dist.xconv, ws, cs);
+        }
+        cuda_check(cudaEventRecord(dist.ev[1], cs), "event");
+        if (split) stub_frames(b, h, fc - 2 * h, s);
+        cuda_check(cudaStreamWaitEvent(s, dist.ev[1], 0), "wait");
+    } else {
+        stage_stub(b, s);
+    }
+    stage_conv(b, s);
+    if (multi && ablate != VINF_ABLATE_GROUPNORM) {
+        Span span(this, "allreduce_gn", s);
+        comm->allreduce_sum_f64(at<double>(L.off_sums), 2ull * L.d.groups, s);
+    }
+    const bool x_attn = multi && ablate != VINF_ABLATE_ATTENTION && !dist.xattn.empty();
+    auto start_attn = [&] {
+        cuda_check(cudaEventRecord(dist.ev[2], s), "event");
+        cuda_check(cudaStreamWaitEvent(cs, dist.ev[2], 0), "wait");
+        Span span(this, "xchg_attn", cs);
+        run_exchange(comm, dist.xattn, ws, cs);
+        cuda_check(cudaEventRecord(dist.ev[3], cs), "event");
+    };
+    // GroupNorm folded (bf16): the conv already wrote the raw frames the exchange ships,
+    // so it overlaps the fold as well; otherwise it ships the normalised frames
+    if (x_attn && fold()) start_attn();
+    stage_gn_apply(b, s);
+    if (x_attn && !fold()) start_attn();
+    if (x_attn) {
+        stage_qkv(b, s);
+        cuda_check(cudaStreamWaitEvent(s, dist.ev[3], 0), "wait");
+    }
+    stage_attention(b, t, s);
+}
+
+namespace {
+
+void dist_stack(vinf_engine* e, double t, vinf_comm* comm, cudaStream_t s) {
+    for (uint32_t b = 0; b < e->blocks.size(); ++b) e->dist_block(b, t, comm, s);
+}
+
+// NCCL operations are graph-capturable: the stack of each timestep regime is captured
+// once (after one eager pass) and replayed, like the single-worker path.
+void forward_dist(vinf_engine* e, double t, vinf_comm* comm, bool use_graph, cudaStream_t s) {
+    e->dist_init();
+    if (!use_graph || e->profiling || !comm->capturable() || !e->use_graphs) {
+        dist_stack(e, t, comm, s);
+        return;
+    }
+    if (e->dist.graph_comm != comm) {
+        e->drop_graphs();
+        e->dist.graph_comm = comm;
+    }
+    auto& g = e->dist.graphs[t > e->L.d.t_star ? 1 : 0];
+    if (!g.exec && g.calls++ >= 1) {
+        if (!e->cap_stream)
+            cuda_check(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking), "capture stream");
+        const uint64_t l0 = e->launches;
+        const uint64_t b0 = comm->bytes_sent, m0 = comm->messages_sent;
+        cuda_check(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            dist_stack(e, t, comm, e->cap_stream);
+        } catch (...) {
+            cudaGraph_t broken = nullptr;
+            cudaStreamEndCapture(e->cap_stream, &broken);
+            if (broken) cudaGraphDestroy(broken);
+            e->launches = l0;
+            throw;
+        }
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamEndCapture(e->cap_stream, &graph), "end capture");
+        const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(ie, "graph instantiate");
+        g.nlaunch = e->launches - l0;
+        g.nbytes = comm->bytes_sent - b0;
+        g.nmsgs = comm->messages_sent - m0;
+        e->launches = l0;
+        comm->bytes_sent = b0;
+        comm->messages_sent = m0;
+    }
+    if (g.exec) {
+        cuda_check(cudaGraphLaunch(g.exec, s), "graph launch");
+        e->launches += g.nlaunch;
+        comm->bytes_sent += g.nbytes;
+        comm->messages_sent += g.nmsgs;
+    } else {
+        dist_stack(e, t, comm, s);
+    }
+}
+
+void check_comm(const vinf_engine* e, const vinf_comm* comm) {
+    if (!comm) shape_error("null communicator");
+    if (comm->nranks != e->L.d.workers || comm->rank != e->L.d.worker)
+        config_error("communicator rank " + std::to_string(comm->rank) + " of " + std::to_string(comm->nranks) +
+                     " does not match the engine's worker " + std::to_string(e->L.d.worker) + " of " +
+                     std::to_string(e->L.d.workers));
+}
+
+}  // namespace
 
 // ---- C ABI (engine part) ---------------------------------------------------------
 
@@ -390,6 +549,9 @@ void vinf_engine_destroy(vinf_engine* e) {
     if (!e) return;
     e->drop_graphs();
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    if (e->dist.cs) cudaStreamDestroy(e->dist.cs);
+    for (cudaEvent_t ev : e->dist.ev)
+        if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : e->pool) cudaEventDestroy(ev);
     for (auto& B : e->blocks) {
         if (B.f32) cudaFree(B.f32);
@@ -641,6 +803,64 @@ int vinf_engine_kernel_stats(vinf_engine* e, char* names, uint32_t name_cap, dou
         }
         e->recs.clear();
         e->pool_used = 0;
+    });
+}
+
+int vinf_layout_run_exchange(const vinf_layout* l, int stage, void* base, vinf_comm* comm, void* stream) {
+    return guarded_call([&] {
+        if (!l || !comm) shape_error("null argument");
+        if (!base) shape_error("null workspace");
+        if (stage != VINF_XCHG_CONV && stage != VINF_XCHG_ATTN) range_error("unknown exchange stage");
+        if (comm->nranks != l->L.d.workers || comm->rank != l->L.d.worker)
+            config_error("communicator rank does not match the layout's worker");
+        run_exchange(comm, matching_order(stage == VINF_XCHG_CONV ? l->L.xconv : l->L.xattn),
+                     static_cast<uint8_t*>(base), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int vinf_engine_exchange(vinf_engine* e, int stage, vinf_comm* comm, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        check_comm(e, comm);
+        if (stage != VINF_XCHG_CONV && stage != VINF_XCHG_ATTN) range_error("unknown exchange stage");
+        e->dist_init();
+        auto s = static_cast<cudaStream_t>(stream);
+        vinf_engine::Span span(e, stage == VINF_XCHG_CONV ? "xchg_conv" : "xchg_attn", s);
+        run_exchange(comm, stage == VINF_XCHG_CONV ? e->dist.xconv : e->dist.xattn, e->ws, s);
+    });
+}
+
+int vinf_engine_allreduce_sums(vinf_engine* e, vinf_comm* comm, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        check_comm(e, comm);
+        auto s = static_cast<cudaStream_t>(stream);
+        vinf_engine::Span span(e, "allreduce_gn", s);
+        comm->allreduce_sum_f64(e->at<double>(e->L.off_sums), 2ull * e->L.d.groups, s);
+    });
+}
+
+int vinf_engine_forward_dist(vinf_engine* e, double t, vinf_comm* comm, int use_graph, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        check_comm(e, comm);
+        forward_dist(e, t, comm, use_graph != 0, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int vinf_engine_denoise_dist(vinf_engine* e, uint32_t steps, vinf_comm* comm, int use_graph, void* stream) {
+    return guarded_call([&] {
+        if (!e) shape_error("null engine");
+        check_comm(e, comm);
+        if (steps == 0) config_error("denoising needs at least one step");
+        auto s = static_cast<cudaStream_t>(stream);
+        for (uint32_t j = steps; j >= 1; --j) {  // timestep_grid (pipeline.cpp:75-81)
+            const double t = 1000.0 * j / steps;
+            forward_dist(e, t, comm, use_graph != 0, s);
+            cuda_check(launch_euler(e->at(e->L.off_x), e->at(e->L.off_y), !e->f32(), e->clip_elems(), 1.0 / steps, s),
+                       "euler");
+            e->launches += 1;
+        }
     });
 }
 

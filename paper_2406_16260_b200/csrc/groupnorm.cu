@@ -461,16 +461,6 @@ __device__ __forceinline__ double colpart_entry(const float* base, uint32_t C, u
     const float* r = base + uint64_t(row) * 2 * C + c;
     return which ? double(r[C]) + k2 * double(r[0]) : double(r[0]);
 }
-__device__ __forceinline__ double colpart_shift_total(const float* shift, uint32_t c0, uint32_t gs,
-                                                      uint32_t which, double rows) {
-    if (!shift) return 0.0;
-    double t = 0.0;
-    for (uint32_t c = 0; c < gs; ++c) {
-        const double b = double(shift[c0 + c]);
-        t += which ? b * b : b;
-    }
-    return rows * t;
-}
 
 __global__ void __launch_bounds__(128)
     colpart_fold_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C, uint32_t groups,
@@ -526,8 +516,16 @@ __global__ void __launch_bounds__(128)
         double t = reinterpret_cast<const volatile double*>(seg)[uint64_t(sg) * kFoldSegs + threadIdx.x];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        double st = 0.0;  // the shift constant, one column per lane (loads in parallel)
+        if (shift)
+            for (uint32_t cc = threadIdx.x; cc < gs; cc += 32) {
+                const double bb = double(shift[g * gs + cc]);
+                st += which ? bb * bb : bb;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) st += __shfl_xor_sync(0xffffffffu, st, o);
         if (threadIdx.x == 0) {
-            sums[which * groups + g] = t + colpart_shift_total(shift, g * gs, gs, which, rows);
+            sums[which * groups + g] = t + rows * st;
             tickets[sg] = 0;  // ready for the next fold
         }
     }
@@ -543,32 +541,51 @@ __global__ void __launch_bounds__(kDirectThreads)
     colpart_fold_direct_kernel(const float* __restrict__ part, uint32_t blocks, uint32_t C,
                                uint32_t groups, const float* __restrict__ shift, double rows,
                                double* __restrict__ sums) {
-    dev::pdl_wait();
-    dev::pdl_trigger();
     __shared__ double red[kDirectThreads];
     const uint32_t which = blockIdx.x / groups, g = blockIdx.x % groups, gs = C / groups;
-    const float* base = part + uint64_t(g) * gs;
-    const uint32_t n = blocks * gs;
-    double a0 = 0.0, a1 = 0.0;
-    uint32_t i = threadIdx.x;
-    auto k2 = [&](uint32_t c) { return (which && shift) ? 2.0 * double(shift[g * gs + c]) : 0.0; };
-    for (; i + kDirectThreads < n; i += 2 * kDirectThreads) {
-        const uint32_t r0 = i / gs, r1 = (i + kDirectThreads) / gs;
-        const uint32_t c0 = i - r0 * gs, c1 = i + kDirectThreads - r1 * gs;
-        a0 += colpart_entry(base, C, r0, c0, which, k2(c0));
-        a1 += colpart_entry(base, C, r1, c1, which, k2(c1));
+    // thread = (row lane rl, group column c): rows rl, rl + nrl, ... of one column, four
+    // independent loads in flight; the column's shift (the conv bias, a weight) is read
+    // before the dependency wait and its constant rows * b (or b^2) joins the same tree
+    const uint32_t nrl = gs <= kDirectThreads ? kDirectThreads / gs : 1;
+    const uint32_t rl = threadIdx.x / gs, c = threadIdx.x - rl * gs;
+    const bool active = gs <= kDirectThreads && rl < nrl;
+    const double b = (active && shift) ? double(__ldg(shift + g * gs + c)) : 0.0;
+    const double k2 = which ? 2.0 * b : 0.0;
+    dev::pdl_wait();
+    dev::pdl_trigger();
+    double a = 0.0;
+    if (active) {
+        const float* col = part + uint64_t(g) * gs + c;
+        auto entry = [&](uint32_t r) {
+            const float* e = col + uint64_t(r) * 2 * C;
+            return which ? double(e[C]) + k2 * double(e[0]) : double(e[0]);
+        };
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        uint32_t r = rl;
+        for (; r + 3 * nrl < blocks; r += 4 * nrl) {
+            a0 += entry(r);
+            a1 += entry(r + nrl);
+            a2 += entry(r + 2 * nrl);
+            a3 += entry(r + 3 * nrl);
+        }
+        for (; r < blocks; r += nrl) a0 += entry(r);
+        a = (a0 + a1) + (a2 + a3);
+        if (rl == 0 && shift) a += rows * (which ? b * b : b);
+    } else if (gs > kDirectThreads) {  // wide groups: every thread strides the columns too
+        for (uint32_t cc = threadIdx.x; cc < gs; cc += kDirectThreads) {
+            const double bb = shift ? double(shift[g * gs + cc]) : 0.0;
+            const double kk = which ? 2.0 * bb : 0.0;
+            for (uint32_t r = 0; r < blocks; ++r) a += colpart_entry(part + uint64_t(g) * gs, C, r, cc, which, kk);
+            a += rows * (which ? bb * bb : bb);
+        }
     }
-    if (i < n) {
-        const uint32_t r0 = i / gs, c0 = i - r0 * gs;
-        a0 += colpart_entry(base, C, r0, c0, which, k2(c0));
-    }
-    red[threadIdx.x] = a0 + a1;
+    red[threadIdx.x] = a;
     __syncthreads();
     for (uint32_t w = kDirectThreads / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) sums[which * groups + g] = red[0] + colpart_shift_total(shift, g * gs, gs, which, rows);
+    if (threadIdx.x == 0) sums[which * groups + g] = red[0];
 }
 
 int launch_colpart_to_groups(const float* part, uint32_t blocks, uint32_t C, uint32_t groups,

@@ -57,6 +57,8 @@ struct HostTokens {
     // the bias iff wflag / gflag (uniform per table, checked).
     std::vector<uint16_t> nwin;
     std::vector<uint8_t> wlo, whi, gmult;
+    std::vector<uint32_t> kv_box;  // TMA box program per block (TokenTable::kv_box)
+    std::vector<uint16_t> kv_nbox, kv_load_rows;
     int wflag = 0, gflag = 0;
     uint32_t nq = 0, nqb = 0;
     bool kv_ok = true;
@@ -73,6 +75,9 @@ struct HostTokens {
         wlo.assign(n, 0);
         whi.assign(n, 0);
         gmult.assign(size_t(nqb) * kKvMax, 0);
+        kv_box.assign(size_t(nqb) * kKvMax, 0);
+        kv_nbox.assign(nqb, 0);
+        kv_load_rows.assign(nqb, 0);
     }
     // Window tokens first, then (global = true) the sampled global tokens.
     void push(uint32_t a, uint32_t row, bool b, bool global = false) {

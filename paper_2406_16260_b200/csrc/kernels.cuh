@@ -84,7 +84,15 @@ struct TokenTable {
     int wflag, gflag;           // window / global tokens carry +bias
     int kv_ok;                  // every block's K/V list fits kKvMax
     int max_kv;                 // largest K/V list over the blocks
+    // TMA load program of each block's K/V list: the sorted distinct frames split into
+    // contiguous runs, each run into boxes of 32/16/8/4/2/1 frame rows (kind 0..5), box i
+    // packed as frame | smem row << 16 | kind << 24 in kv_box[qb][i]. kv_load_rows = the rows
+    // those boxes write (= kv_count: the transaction bytes of a K or V stage / 128 B).
+    const uint32_t* kv_box;     // [nqb][kKvMax]
+    const uint16_t* kv_nbox;    // [nqb]
+    const uint16_t* kv_load_rows;  // [nqb]
 };
+constexpr int kBoxKinds = 6;  // box heights 32 >> kind
 
 // Whether the core runs this configuration: head dim d = C / heads with d % 8 == 0 and
 // every query block's distinct K/V frames <= kKvMax. There is no other attention kernel:
@@ -96,8 +104,11 @@ bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
 // ctx: [nq * HW, C] bf16.
 // Split (fp32) mode: qkv_lo / ctx_lo non-null are the lo planes (same layout) of the
 // bf16x3 operands; every product runs as hi*hi + hi*lo + lo*hi.
-int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
-                          uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias,
-                          void* ctx, void* ctx_lo, cudaStream_t s);
+// Diagnostics knob: 1 = the qkv buffer is position-major [HW][frames][3C].
+extern int g_attn_pos_major;
+// qkv_frames: frames of the qkv buffer (the TMA tensor maps' outer extent).
+int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_frames, uint32_t HW, uint32_t C,
+                          uint32_t heads, uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale,
+                          float bias, void* ctx, void* ctx_lo, cudaStream_t s);
 
 }  // namespace vinf

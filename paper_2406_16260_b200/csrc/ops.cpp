@@ -105,6 +105,8 @@ void gemm(const Operand& A, const std::vector<int64_t>& a_rows, const DevMat& B,
     // partial sums cannot live in split planes.
     const bool chunked = segs.size() > size_t(kGemmMaxSeg);
     if (chunked && ep.out_lo) shape_error("gemm: split-plane output needs <= 12 segments");
+    // later chunks re-read the partial sum as their residual: in bf16 that would round it
+    if (chunked && ep.out_bf16) shape_error("gemm: bf16 output needs <= 12 segments (taps <= 12)");
     // bf16 output without residual / statistics (the Q/K/V projections): TMA-store epilogue
     const bool tma_out = !chunked && ep.out_bf16 && !ep.res && !ep.colpart && !split &&
                          reinterpret_cast<uintptr_t>(ep.out) % 16 == 0 && ep.out_ld % 8 == 0 &&
@@ -297,7 +299,7 @@ void attention_generic(const void* src, vinf_dtype dt, uint32_t frames, uint32_t
     TmpBuf ctx(qrows * C * 4, s);  // bf16 ctx or hi+lo planes
     auto* hi = static_cast<__nv_bfloat16*>(ctx.p);
     auto* lo = hi + qrows * C;
-    cuda_check(launch_attention_core(qh, f32 ? e1.out_lo : nullptr, hw, C, p->heads, nq, q0, dt_tok.tt,
+    cuda_check(launch_attention_core(qh, f32 ? e1.out_lo : nullptr, frames, hw, C, p->heads, nq, q0, dt_tok.tt,
                                      p->scale, bias, hi, f32 ? lo : nullptr, s),
                "attention core");
     Operand O;

@@ -138,11 +138,38 @@ void HostTokens::finalize() {
     }
     if (wflag < 0) wflag = 0;
     if (gflag < 0) gflag = 0;
+    // TMA box program: runs of consecutive frames, each covered exactly by boxes of 32,
+    // 16, ... 1 rows (no box reads a frame the block does not use: every byte is traffic)
+    for (uint32_t qb = 0; qb < nqb && kv_ok; ++qb) {
+        const uint16_t* fr = &kv_frames[size_t(qb) * kKvMax];
+        const uint32_t R = kv_count[qb];
+        uint32_t nb = 0, rows = 0;
+        for (uint32_t c0 = 0; c0 < R;) {
+            uint32_t len = 1;
+            while (c0 + len < R && fr[c0 + len] == fr[c0] + len) ++len;
+            uint32_t at = 0;
+            while (at < len) {
+                const uint32_t left = len - at;
+                int kind = 0;
+                while ((32u >> kind) > left) ++kind;
+                const uint32_t h = 32u >> kind;
+                if (nb >= uint32_t(kKvMax)) config_error("attention K/V load program too long");
+                kv_box[size_t(qb) * kKvMax + nb++] =
+                    uint32_t(fr[c0 + at]) | (c0 + at) << 16 | uint32_t(kind) << 24;
+                rows += h;
+                at += h;
+            }
+            c0 += len;
+        }
+        kv_nbox[qb] = uint16_t(nb);
+        kv_load_rows[qb] = uint16_t(rows);
+    }
 }
 
 size_t HostTokens::blob_bytes() const {
-    return rows.size() * 2 + biased.size() + col.size() + count.size() * 2 +
-           kv_frames.size() * 2 + kv_count.size() * 2 + wlo.size() + whi.size() + gmult.size() + 64;
+    return kv_box.size() * 4 + rows.size() * 2 + biased.size() + col.size() + count.size() * 2 +
+           kv_frames.size() * 2 + kv_count.size() * 2 + kv_nbox.size() * 2 + kv_load_rows.size() * 2 +
+           wlo.size() + whi.size() + gmult.size() + 64;
 }
 
 void HostTokens::pack(uint8_t* dst) const {
@@ -151,8 +178,11 @@ void HostTokens::pack(uint8_t* dst) const {
         if (n) std::memcpy(dst + o, src, n);
         o += n;
     };
+    put(kv_box.data(), kv_box.size() * 4);
     put(rows.data(), rows.size() * 2);
     put(kv_frames.data(), kv_frames.size() * 2);
+    put(kv_nbox.data(), kv_nbox.size() * 2);
+    put(kv_load_rows.data(), kv_load_rows.size() * 2);
     put(count.data(), count.size() * 2);
     put(kv_count.data(), kv_count.size() * 2);
     put(biased.data(), biased.size());
@@ -165,10 +195,16 @@ void HostTokens::pack(uint8_t* dst) const {
 TokenTable HostTokens::view(const uint8_t* base) const {
     TokenTable t{};
     size_t o = 0;
+    t.kv_box = reinterpret_cast<const uint32_t*>(base + o);
+    o += kv_box.size() * 4;
     t.rows = reinterpret_cast<const uint16_t*>(base + o);
     o += rows.size() * 2;
     t.kv_frames = reinterpret_cast<const uint16_t*>(base + o);
     o += kv_frames.size() * 2;
+    t.kv_nbox = reinterpret_cast<const uint16_t*>(base + o);
+    o += kv_nbox.size() * 2;
+    t.kv_load_rows = reinterpret_cast<const uint16_t*>(base + o);
+    o += kv_load_rows.size() * 2;
     t.count = reinterpret_cast<const uint16_t*>(base + o);
     o += count.size() * 2;
     t.kv_count = reinterpret_cast<const uint16_t*>(base + o);

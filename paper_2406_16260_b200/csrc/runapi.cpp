@@ -218,6 +218,14 @@ std::vector<std::string> violations(const RunConfig& c) {
              c.ablate == "attention",
          "ablate must be none, conv, groupnorm, or attention (got '" + c.ablate + "')");
     need(c.dtype == "f32" || c.dtype == "bf16", "dtype must be f32 or bf16 (got '" + c.dtype + "')");
+    // Limits of the device backend that the reference (CPU) does not have; listed after the
+    // reference's own checks so a config it rejects reports the same messages first
+    // (INTEGRATION.md §4): 16-byte TMA rows and the attention core's K/V tile.
+    need(c.channels == 0 || c.channels % 8 == 0,
+         "device backend: channels must be a multiple of 8 (got " + s(c.channels) + ")");
+    need(uint64_t(c.n_local) + 1 + c.n_global <= uint64_t(kMaxTokens),
+         "device backend: n_local + 1 + n_global must be <= " + s(kMaxTokens) + " (got " +
+             s(uint64_t(c.n_local) + 1 + c.n_global) + ")");
     return v;
 }
 

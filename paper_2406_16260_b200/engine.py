@@ -7,7 +7,8 @@ paper's 3-step context sync.
     eng.init_weights(weight_seed=1)          # build_model (pipeline.cpp:35-67) on device
     eng.x.copy_(clip)                        # [f_clip, H, W, C] in the engine dtype
     forward(t=900.0, engines=[eng])          # single worker: one C call
-    forward(t, [eng], DistGroup(transport))  # clip-parallel over torch.distributed
+    forward(t, [eng], DistGroup(transport))  # clip-parallel, Python stage loop over torch.distributed
+    forward(t, [eng], CommGroup([NcclComm.create()]))  # clip-parallel, the C++ executor over NCCL
 
 Exchanges are the workspace byte ranges the C++ layout lists (halo frames into the
 neighbours' halo slots, remote global frames into global slots), so the transport moves
@@ -61,11 +62,15 @@ class Layout:
         return off.value, n.value, fb.value
 
     def exchange(self, stage: int) -> list[_lib.Xfer]:
-        n = C.c_uint32()
-        cap = 4096
-        arr = (_lib.Xfer * cap)()
-        _lib.check(self._lib.vinf_layout_exchange(self._h, stage, arr, cap, C.byref(n)))
-        return [arr[i] for i in range(n.value)]
+        """The stage's transfer list (computed once per layout; the plan is immutable)."""
+        cache = self.__dict__.setdefault("_xcache", {})
+        if stage not in cache:
+            n = C.c_uint32()
+            _lib.check(self._lib.vinf_layout_exchange(self._h, stage, None, 0, C.byref(n)))
+            arr = (_lib.Xfer * max(n.value, 1))()
+            _lib.check(self._lib.vinf_layout_exchange(self._h, stage, arr, n.value, C.byref(n)))
+            cache[stage] = [arr[i] for i in range(n.value)]
+        return cache[stage]
 
     def reference_traffic(self):
         a, b, c = (C.c_uint64 * 3)(), (C.c_uint64 * 3)(), (C.c_uint64 * 3)()
@@ -183,16 +188,82 @@ class LocalGroup:
             e.gn_sums.copy_(total)
 
 
+class CommGroup:
+    """The C++ clip-parallel executor: every engine runs its whole block stack with the
+    3-step sync in one vinf_engine_forward_dist call over its worker's communicator
+    (comm.NcclComm: one process per GPU; comm.local_comms: in-process workers, one host
+    thread each, e.g. N clips on one GPU). Exchanges of the kind an engine ablates
+    (ClipEngine.set_ablation) are skipped by the engine itself."""
+
+    def __init__(self, comms, use_graph: bool = True):
+        self.comms = {c.info()["rank"]: c for c in comms}
+        self.use_graph = use_graph
+        self._streams: dict = {}
+
+    def _call(self, fn_name: str, engines: list[ClipEngine], arg) -> None:
+        lib = _lib.load()
+        fn = getattr(lib, fn_name)
+        if len(engines) == 1:
+            e = engines[0]
+            _lib.check(fn(e._h, arg, self.comms[e.layout.desc.worker].handle, int(self.use_graph), e._stream()))
+            return
+        # in-process workers: one thread per engine, each on its own stream (the hub blocks
+        # a worker's host thread until its peers post their messages)
+        import threading
+        dev = engines[0].device
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        main = torch.cuda.current_stream(dev)
+        streams = []
+        for e in engines:
+            st = self._streams.get(id(e))
+            if st is None:
+                st = self._streams[id(e)] = torch.cuda.Stream(dev)
+            st.wait_stream(main)
+            streams.append(st)
+        errors: list = []
+
+        def work(e, st):
+            try:
+                torch.cuda.set_device(dev)
+                _lib.check(fn(e._h, arg, self.comms[e.layout.desc.worker].handle, int(self.use_graph),
+                              C.c_void_p(st.cuda_stream)))
+            except BaseException as ex:  # noqa: BLE001
+                errors.append(ex)
+                self.comms[e.layout.desc.worker].abort()
+
+        ts = [threading.Thread(target=work, args=(e, st)) for e, st in zip(engines, streams)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for st in streams:
+            main.wait_stream(st)
+        if errors:
+            real = [x for x in errors if "aborted" not in str(x)]
+            raise (real or errors)[0]
+
+    def forward(self, t: float, engines: list[ClipEngine]) -> None:
+        self._call("vinf_engine_forward_dist", engines, C.c_double(t))
+
+    def denoise(self, steps: int, engines: list[ClipEngine]) -> None:
+        self._call("vinf_engine_denoise_dist", engines, C.c_uint32(steps))
+
+
 class DistGroup:
     """One engine per process; exchanges over a Transport (torch.distributed / NCCL)."""
 
     def __init__(self, transport: Transport):
         self.t = transport
+        self._msgs: dict = {}
 
     def exchange(self, engines: list[ClipEngine], stage: int) -> None:
         (e,) = engines
-        msgs = [Msg(x.peer, bool(x.send), e.ws[x.offset:x.offset + x.bytes], x.tag)
-                for x in e.layout.exchange(stage)]
+        key = (id(e), stage)
+        msgs = self._msgs.get(key)
+        if msgs is None:  # workspace views built once per engine and stage
+            msgs = self._msgs[key] = [Msg(x.peer, bool(x.send), e.ws[x.offset:x.offset + x.bytes], x.tag)
+                                      for x in e.layout.exchange(stage)]
         self.t.exchange(msgs)
 
     def allreduce_sums(self, engines: list[ClipEngine]) -> None:
@@ -206,6 +277,9 @@ def forward(t: float, engines: list[ClipEngine], group=None, ablate: str | None 
     [one all-reduce of 2*groups f64] -> GN apply -> [attention halo + global sync] ->
     dual-scope attention + residual. `ablate` skips that kind's sync (engines configured
     with set_ablation(ablate))."""
+    if isinstance(group, CommGroup):
+        group.forward(t, engines)
+        return
     blocks = engines[0].layout.desc.blocks
     if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1 and not ablate:
         engines[0].forward_single(t)
@@ -262,6 +336,9 @@ def denoise(steps: int, engines: list[ClipEngine], group=None, ablate: str | Non
     sync when clip-parallel), then x -= y / steps."""
     if group is None and len(engines) == 1 and engines[0].layout.desc.workers == 1 and not ablate:
         engines[0].denoise_single(steps)
+        return
+    if isinstance(group, CommGroup):
+        group.denoise(steps, engines)
         return
     for t in timestep_grid(steps):
         forward(t, engines, group, ablate)

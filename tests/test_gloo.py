@@ -1,6 +1,8 @@
-"""The N>1 host path on CPU: two processes over torch.distributed (gloo) run the SAME
-transport code the B200 ranks run over NCCL — the reference-API sync_contexts and
-group-norm all-reduce, and the clip engine's workspace exchange plan (DistGroup)."""
+"""The N>1 host path on CPU: two / three processes over torch.distributed (gloo) run the
+SAME transport code the B200 ranks run over NCCL — the reference-API sync_contexts and
+group-norm all-reduce, the clip engine's workspace exchange plan (DistGroup), and the C++
+executor's exchange runner (vinf_layout_run_exchange over a callback communicator: the
+code path vinf_engine_forward_dist takes, with gloo in place of NCCL)."""
 import os
 import socket
 import sys
@@ -34,7 +36,7 @@ def _worker(rank, world, port, errq):
 
         t = DistTransport()
         # (1) reference-API sync: halo + global frames land bitwise (test_clip_parallel.cpp:94-149)
-        F = 16
+        F = 48
         full = torch.arange(F * 2 * 2 * 4, dtype=torch.float32).reshape(F, 2, 2, 4)
         plan = cp.make_plan(F, world)
         clip = full[rank * plan.f_clip:(rank + 1) * plan.f_clip].contiguous()
@@ -58,7 +60,7 @@ def _worker(rank, world, port, errq):
         t.allreduce_sum_(s)
         assert torch.allclose(s, torch.full((4,), float(world * (world + 1) / 2), dtype=torch.float64))
         # (3) engine exchange plan over the transport, on a CPU workspace
-        n_local, n_global, Fe = 8, 16, 32
+        n_local, n_global, Fe = 8, 16, 48
         L = en.Layout(en.make_desc(Fe, world, rank, 2, 2, 16, groups=4, n_local=n_local,
                                    n_global=n_global, dtype=torch.bfloat16))
 
@@ -85,6 +87,44 @@ def _worker(rank, world, port, errq):
         remote = [g for g in cp.build_global_index_set(Fe, n_global) if not lo <= g < hi]
         for slot, g in enumerate(remote):
             assert (fr(2 * ha + fc + slot) == g).all()
+        # (4) the C++ executor: the same plans through vinf_layout_run_exchange over an
+        # OpsComm (gloo on host pointers), both stages, plus its f64 all-reduce
+        from paper_2406_16260_b200.comm import GlooPointerTransport, OpsComm
+        comm = OpsComm(GlooPointerTransport())
+        ws = torch.zeros(L.workspace_bytes, dtype=torch.uint8)
+        coff, _, cfb = L.region(_lib.VINF_BUF_CONV_IN)
+        for f in range(fc):
+            ws[off + (ha + f) * fb: off + (ha + f + 1) * fb] = (rank * fc + f) % 251
+            ws[coff + (1 + f) * cfb: coff + (2 + f) * cfb] = (rank * fc + f + 7) % 251
+        base = ws.data_ptr()
+        for stage in (_lib.VINF_XCHG_CONV, _lib.VINF_XCHG_ATTN):
+            _lib.check(_lib.load().vinf_layout_run_exchange(L._h, stage, base, comm.handle, None))
+        assert not comm.errors, comm.errors
+        fa = lambda k: ws[off + k * fb: off + (k + 1) * fb]  # noqa: E731
+        fcv = lambda k: ws[coff + k * cfb: coff + (k + 1) * cfb]  # noqa: E731
+        if rank > 0:
+            assert (fcv(0) == (rank * fc - 1 + 7) % 251).all()
+            for k in range(ha):
+                assert (fa(k) == (rank * fc - ha + k) % 251).all()
+        else:
+            assert (fcv(0) == 0).all()
+        if rank + 1 < world:
+            assert (fcv(1 + fc) == ((rank + 1) * fc + 7) % 251).all()
+            for k in range(ha):
+                assert (fa(ha + fc + k) == ((rank + 1) * fc + k) % 251).all()
+        for slot, g in enumerate(remote):
+            assert (fa(2 * ha + fc + slot) == g % 251).all()
+        info = comm.info()
+        sent = sum(x.bytes for st in (0, 1) for x in L.exchange(st) if x.send)
+        assert info["bytes_sent"] == sent and info["rank"] == rank and info["nranks"] == world
+        red = torch.arange(6, dtype=torch.float64) * (rank + 1)
+        comm.allreduce_sum_f64(red.data_ptr(), 6)
+        assert torch.equal(red, torch.arange(6, dtype=torch.float64) * (world * (world + 1) / 2))
+        # a mismatched communicator is refused before any message moves
+        with pytest.raises(_lib.ConfigError):
+            L0 = en.Layout(en.make_desc(Fe, world, (rank + 1) % world, 2, 2, 16, groups=4, n_local=n_local,
+                                        n_global=n_global, dtype=torch.bfloat16))
+            _lib.check(_lib.load().vinf_layout_run_exchange(L0._h, 0, base, comm.handle, None))
         dist.barrier()
         dist.destroy_process_group()
     except BaseException as ex:  # noqa: BLE001
@@ -93,8 +133,8 @@ def _worker(rank, world, port, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_world2(world, lib):
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_world(world, lib):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
     port = _free_port()
@@ -102,7 +142,7 @@ def test_gloo_world2(world, lib):
     for p in procs:
         p.start()
     for p in procs:
-        p.join(120)
+        p.join(180)
     errs = []
     while not errq.empty():
         errs.append(errq.get())

@@ -96,6 +96,24 @@ def test_validation_matches_reference(api, refapi, values):
     assert len(ours_msg.splitlines()) == len(ref_msg.splitlines())
 
 
+@pytest.mark.parametrize("values,what", [
+    ({"channels": 4, "groups": 2}, "channels must be a multiple of 8"),  # test_capi.cpp set_small_job
+    ({"frames": 200, "n_local": 100, "n_global": 100}, "n_local + 1 + n_global must be <= 160"),
+])
+def test_device_limits_reported_by_validate(api, refapi, values, what):
+    # configs the reference accepts but the device backend cannot run: validate names the
+    # limit (after the reference's own checks), vinf_run refuses them before any work
+    from paper_2406_16260_b200 import _lib
+    h, rc = refapi.config(values)
+    assert rc == 0
+    assert refapi.lib.vinf_config_validate(h) == 0
+    refapi.free(h)
+    cfg = api.RunConfig(values)
+    assert _lib.load().vinf_config_validate(cfg._h) == _lib.VINF_ERR_CONFIG
+    msg = _lib.load().vinf_last_error().decode()
+    assert "device backend: " + what in msg and len(msg.splitlines()) == 2
+
+
 def test_config_file_parsing(api, refapi, tmp_path):
     from paper_2406_16260_b200 import _lib
     p = tmp_path / "run.cfg"
