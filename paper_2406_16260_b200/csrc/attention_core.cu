@@ -43,18 +43,20 @@ namespace {
 
 constexpr int kDC = 64;  // head-dim chunk (one 128-byte swizzle row of bf16)
 constexpr int kConsumerWarps = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + the producer warp
 constexpr int kWQ = kConsumerWarps / 2;  // warps per 16-query m tile
 constexpr int kON = 8 / kWQ;              // PV: n8 output tiles per warp in a 64-wide chunk
 constexpr uint32_t kOPitch = kON * 16 + 16;  // ctx staging row pitch (bytes, conflict-free)
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr uint32_t kQT = kQBlock * 128;  // one plane of a Q chunk (32 rows x 128 B)
 
 struct AttnMaps {
     CUtensorMap box[2][kBoxKinds];  // [plane][kind]: boxes {64, 1, 1, 32 >> kind}
+    CUtensorMap g4[2];              // [plane]: 2-D rows x 3C view, box {64, 1}, for row gathers
 };
 
 struct AttnArgs {
-    uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items;
+    uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items, ns, frames, pos_major;
+    uint32_t load_only;  // diagnostics: consumers only wait for and release the stages
     float scale, bias;
     __nv_bfloat16* ctx;
     int64_t ctx_lo;  // elements from ctx to its lo plane (split mode)
@@ -109,13 +111,16 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
 }
 
 // Shared memory (bytes). RP = K/V tile rows (NTL * 8, a multiple of 16); PL = planes.
-//   qk[NQ] : S-phase stage = [Q planes: PL x 32 x 128 B][K planes: PL x RP x 128 B]
-//   v[NV]  : PV-phase stage = [V planes: PL x RP x 128 B]            (stages 1 KB aligned)
-//   sp     : S (fp32), 32 x SP
-//   pb     : P (bf16, PL planes), ceil(RP/64) blocks of 32 x 128 B (swizzled rows)
-//   bars   : full/empty of both rings
-// Two rings: the V chunks of an item wait in their own ring through its S phase and softmax,
-// while the S-phase ring is already streaming the next item's Q/K chunks.
+//   ring[NS] : FIFO of stages in the consumers' order: per (item, head) nch S-phase stages
+//              [Q planes: PL x 32 x 128 B | K planes: PL x RP x 128 B], then ceil(nch / VPS)
+//              PV-phase stages of VPS V chunks [PL x RP x 128 B each] (stages 1 KB aligned)
+//   sp       : S (fp32), 32 x SP
+//   pb       : P (bf16, PL planes), ceil(RP/64) blocks of 32 x 128 B (swizzled rows)
+//   ost      : per-warp ctx staging (16 rows)
+//   bars     : full[NS], empty[NS]
+// One FIFO keeps a fixed prefetch distance across phases and items: V chunks load during the
+// softmax, the next item's Q/K chunks during the PV phase. Several CTAs per SM interleave
+// their phases, so the memory pipe never drains.
 template <int NTL, bool SPLIT>
 struct CoreLay {
     static constexpr uint32_t RP = NTL * 8;
@@ -123,35 +128,42 @@ struct CoreLay {
     static constexpr uint32_t PL = SPLIT ? 2 : 1;
     static constexpr bool PREG = NTL <= 8;  // P fragments held in registers for PV
     static constexpr uint32_t KT = RP * 128;
-    static constexpr uint32_t QKST = (PL * (kQT + KT) + 1023) / 1024 * 1024;
-    static constexpr uint32_t VST = (PL * KT + 1023) / 1024 * 1024;
+    static constexpr uint32_t VPS = (kQT + KT) / KT;  // V chunks per stage
+    static constexpr uint32_t ST = (PL * (kQT + KT) + 1023) / 1024 * 1024;
     static constexpr uint32_t PB = ((RP + 63) / 64) * kQBlock * 128;
-    static constexpr uint32_t OST = PL * 16 * kOPitch;  // per-warp ctx staging: 16 rows
-    static constexpr uint32_t scratch = kQBlock * SP * 4 + PL * PB + kConsumerWarps * OST + 2 * 20 * 8 + 1024;
-    // up to four CTAs per SM (each a 5-warp producer/consumer pipeline) while rings of
-    // 2 + 3 stages fit
-    static constexpr uint32_t need = 2 * QKST + 3 * VST + scratch;
-    static constexpr int ctas = need <= 56 * 1024 ? 4 : (need <= 75 * 1024 ? 3 : (need <= 112 * 1024 ? 2 : 1));
-    static constexpr uint32_t budget = (ctas == 4 ? 56u : ctas == 3 ? 75u : ctas == 2 ? 112u : 224u) * 1024u - scratch;
-    static constexpr uint32_t nv0 = (budget / 2) / VST;
-    static constexpr int NV = nv0 > 10 ? 10 : (nv0 < 1 ? 1 : int(nv0));
-    static constexpr uint32_t nq0 = (budget - NV * VST) / QKST;
-    static constexpr int NQ = nq0 > 8 ? 8 : (nq0 < 1 ? 1 : int(nq0));
-    static constexpr uint32_t vring = NQ * QKST;
-    static constexpr uint32_t sp = vring + NV * VST;
+    static constexpr uint32_t OST = PL * 16 * kOPitch;
+    static constexpr uint32_t scratch = (kQBlock * SP * 4 + PL * PB + kConsumerWarps * OST + 127) / 128 * 128;
+    // as many CTAs per SM (up to 4) as leave a ring of >= 4 stages each
+    static constexpr int pick_ctas() {
+        for (int c = 4; c > 1; --c)
+            if (c * (scratch + 4 * ST + 2048) <= 226u * 1024u) return c;
+        return 1;
+    }
+    // measured (scripts/attn_micro.py): 3 CTAs per SM for bf16 (deeper rings beat a fourth
+    // CTA on long clips, equal at cfg2), 2 for the split mode
+    static constexpr int ctas = pick_ctas() < (SPLIT ? 2 : 3) ? pick_ctas() : (SPLIT ? 2 : 3);
+    // scratch first, then the ring (NS stages, chosen at launch), then its barriers
+    static constexpr uint32_t sp = 0;
     static constexpr uint32_t pb = sp + kQBlock * SP * 4;
     static constexpr uint32_t ost = pb + PL * PB;
-    static constexpr uint32_t bars = (ost + kConsumerWarps * OST + 15) / 16 * 16;
-    static constexpr uint32_t total = bars + 2 * (NQ + NV) * 8 + 1024;  // + alignment slack
-    static_assert(total <= 227 * 1024, "attention core shared memory");
+    static constexpr uint32_t ring = (ost + kConsumerWarps * OST + 1023) / 1024 * 1024;
+    static constexpr uint32_t bars(int ns) { return ring + uint32_t(ns) * ST; }
+    static constexpr uint32_t total(int ns) { return bars(ns) + 2u * uint32_t(ns) * 8u + 1024u; }
+    // the deepest ring (<= 16 stages) that lets `c` CTAs share an SM
+    static constexpr int stages(int c) {
+        int ns = 16;
+        while (ns > 2 && uint32_t(c) * total(ns) > 227u * 1024u) --ns;
+        return ns;
+    }
+    static_assert(total(2) <= 227 * 1024, "attention core shared memory");
 };
 
 // Position in a ring of N stages: slot and the parity of its current use.
-template <int N>
 struct Ring {
-    uint32_t slot = 0, phase = 0;
+    uint32_t n, slot = 0, phase = 0;
+    __device__ explicit Ring(uint32_t stages) : n(stages) {}
     __device__ __forceinline__ void next() {
-        if (++slot == uint32_t(N)) {
+        if (++slot == n) {
             slot = 0;
             phase ^= 1u;
         }
@@ -164,33 +176,28 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
     using LL = CoreLay<NTL, SPLIT>;
     constexpr uint32_t RP = LL::RP;
     constexpr int SP = int(LL::SP);
-    constexpr int NQ = LL::NQ, NV = LL::NV;
-    constexpr int KC = (int(RP) + 31) / 32;  // softmax columns per lane
+    const uint32_t NS = a.ns;
+    constexpr uint32_t VPS = LL::VPS;
+    constexpr int KC = (int(RP) + 31) / 32;     // softmax columns per lane
     constexpr int NJ = (NTL + kWQ - 1) / kWQ;  // S n8 tiles per warp
-    constexpr int NA = NJ == 1 ? 2 : 1;       // S accumulators per tile (ILP when NJ == 1)
+    constexpr int NA = NJ <= 2 ? 2 : 1;         // S accumulators per tile (shorter MMA chains)
     static_assert(NTL % 2 == 0 && RP <= uint32_t(kKvMax), "K/V rows padded to a multiple of 16");
     extern __shared__ uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = dev::smem_u32(sm);
-    uint64_t* qfull = reinterpret_cast<uint64_t*>(sm + LL::bars);
-    uint64_t* qempty = qfull + NQ;
-    uint64_t* vfull = qempty + NQ;
-    uint64_t* vempty = vfull + NV;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + LL::bars(int(NS)));
+    uint64_t* empty = full + NS;
     float* sp = reinterpret_cast<float*>(sm + LL::sp);
 
-    // zero the ring and P once: rows no load of an item writes (K/V padding rows, Q rows
+    // zero the ring and scratch once: rows no load of an item writes (K/V padding rows, Q rows
     // past the block) then always hold finite values, and P = 0 meets finite V rows
-    for (uint32_t i = tid * 16; i < LL::bars; i += kThreads * 16)
+    for (uint32_t i = tid * 16; i < LL::bars(int(NS)); i += kThreads * 16)
         *reinterpret_cast<uint4*>(sm + i) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
-        for (int s = 0; s < NQ; ++s) {
-            dev::mbar_init(&qfull[s], 1);
-            dev::mbar_init(&qempty[s], kConsumerWarps);
-        }
-        for (int s = 0; s < NV; ++s) {
-            dev::mbar_init(&vfull[s], 1);
-            dev::mbar_init(&vempty[s], kConsumerWarps);
+        for (uint32_t s = 0; s < NS; ++s) {
+            dev::mbar_init(&full[s], 1);
+            dev::mbar_init(&empty[s], kConsumerWarps);
         }
         dev::fence_barrier_init();
     }
@@ -199,14 +206,15 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
     dev::pdl_wait();
     dev::pdl_trigger();
 
-    const uint32_t heads = a.heads, nch = a.nch;
+    const uint32_t heads = a.heads, nch = a.nch, nvs = (nch + VPS - 1) / VPS;
     if (warp == kConsumerWarps) {
         // ---------------- producer: one thread issues every TMA load ----------------
         if (lane != 0) return;
-        for (int pl = 0; pl < int(LL::PL); ++pl)
+        for (int pl = 0; pl < int(LL::PL); ++pl) {
             for (int k = 0; k < kBoxKinds; ++k) dev::tma_prefetch_desc(&maps.box[pl][k]);
-        Ring<NQ> rq;
-        Ring<NV> rv;
+            dev::tma_prefetch_desc(&maps.g4[pl]);
+        }
+        Ring r(NS);
         for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
             const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
             const uint32_t nb = a.tt.kv_nbox[qb];
@@ -214,44 +222,64 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
             const uint32_t* prog = a.tt.kv_box + size_t(qb) * kKvMax;
             const uint32_t nqh = min(uint32_t(kQBlock), a.nq - qb * kQBlock);
             const int32_t qf = int32_t(a.q_frame0 + qb * kQBlock);
+            // Layouts of the Q/K/V buffer (a.pos_major): 0 = frame-major rows [frames][HW][3C],
+            // 1 = position-major rows [HW][frames][3C], 2 = chunked [HW][3C/64][frames][64]
+            // (the 64-channel chunk of a position's frames contiguous). box: `rows` frames from
+            // f0 of 64-wide chunk ch of (which, head h); gathers: 2-D row of frame f.
+            const uint32_t nchk = 3 * a.C / kDC;
+            auto box4 = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, uint32_t which, uint32_t h,
+                            uint32_t ch, uint32_t f0) {
+                if (a.pos_major == 2)
+                    tma_load_4d(dst, map, bar, 0, int32_t(f0), int32_t((which * a.C + h * a.d) / kDC + ch), int32_t(p));
+                else
+                    tma_load_4d(dst, map, bar, int32_t(ch * kDC), int32_t(which * heads + h), int32_t(p), int32_t(f0));
+            };
+            auto grow = [&](uint32_t chunk, uint32_t f) {
+                return int32_t(a.pos_major == 2 ? (p * nchk + chunk) * a.frames + f
+                                                : (a.pos_major ? p * a.frames + f : f * a.HW + p));
+            };
+            // K or V chunk ch (which = 1 / 2) of head h into the stage at dst
+            auto load_kv = [&](uint32_t dst, uint64_t* bar, uint32_t which, uint32_t h, uint32_t ch) {
+                for (uint32_t b = 0; b < nb; ++b) {
+                    const uint32_t e = prog[b];
+                    const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
+                    if (kind == uint32_t(kBoxGather4)) {
+                        const uint32_t e1 = prog[b + 1], e2 = prog[b + 2];
+                        b += 2;
+                        const uint32_t chunk = (which * a.C + h * a.d) / kDC + ch;
+                        const int32_t col = a.pos_major == 2 ? 0 : int32_t(which * a.C + h * a.d + ch * kDC);
+                        for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                            dev::tma_gather4(dst + pl * LL::KT + row * 128u, &maps.g4[pl], bar, col,
+                                             grow(chunk, e & 0xFFFFu), grow(chunk, e1 & 0xFFFFu),
+                                             grow(chunk, e1 >> 16), grow(chunk, e2 & 0xFFFFu));
+                        continue;
+                    }
+                    for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                        box4(dst + pl * LL::KT + row * 128u, &maps.box[pl][kind], bar, which, h, ch, e & 0xFFFFu);
+                }
+            };
             for (uint32_t h = 0; h < heads; ++h) {
-                for (uint32_t ch = 0; ch < nch; ++ch, rq.next()) {  // S phase: Q + K chunks
-                    const int32_t c0 = int32_t(ch * kDC);
-                    dev::mbar_wait(&qempty[rq.slot], rq.phase ^ 1u);
-                    uint64_t* bar = &qfull[rq.slot];
+                for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {  // S phase: Q + K chunk
+                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
+                    uint64_t* bar = &full[r.slot];
                     dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
-                    const uint32_t st = sbase + rq.slot * LL::QKST;
+                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     // the block's query rows exactly: boxes of 16, 8, ... rows (32 = one box)
-                    for (uint32_t k = 0, r = 0; k < uint32_t(kBoxKinds); ++k)
+                    for (uint32_t k = 0, q = 0; k < uint32_t(kBoxKinds); ++k)
                         if (nqh & (32u >> k)) {
                             for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                                tma_load_4d(st + pl * kQT + r * 128u, &maps.box[pl][k], bar, c0, int32_t(h),
-                                            int32_t(p), qf + int32_t(r));
-                            r += 32u >> k;
+                                box4(st + pl * kQT + q * 128u, &maps.box[pl][k], bar, 0, h, ch, uint32_t(qf) + q);
+                            q += 32u >> k;
                         }
-                    const int32_t c1 = int32_t(heads + h);
-                    for (uint32_t b = 0; b < nb; ++b) {
-                        const uint32_t e = prog[b];
-                        const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
-                        for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                            tma_load_4d(st + LL::PL * kQT + pl * LL::KT + row * 128u, &maps.box[pl][kind], bar,
-                                        c0, c1, int32_t(p), int32_t(e & 0xFFFFu));
-                    }
+                    load_kv(st + LL::PL * kQT, bar, 1, h, ch);
                 }
-                for (uint32_t ch = 0; ch < nch; ++ch, rv.next()) {  // PV phase: V chunks
-                    const int32_t c0 = int32_t(ch * kDC);
-                    dev::mbar_wait(&vempty[rv.slot], rv.phase ^ 1u);
-                    uint64_t* bar = &vfull[rv.slot];
-                    dev::mbar_arrive_expect_tx(bar, kvb);
-                    const uint32_t st = sbase + LL::vring + rv.slot * LL::VST;
-                    const int32_t c1 = int32_t(2 * heads + h);
-                    for (uint32_t b = 0; b < nb; ++b) {
-                        const uint32_t e = prog[b];
-                        const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
-                        for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                            tma_load_4d(st + pl * LL::KT + row * 128u, &maps.box[pl][kind], bar, c0, c1,
-                                        int32_t(p), int32_t(e & 0xFFFFu));
-                    }
+                for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {  // PV phase: VPS V chunks
+                    const uint32_t n = min(VPS, nch - vs * VPS);
+                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
+                    uint64_t* bar = &full[r.slot];
+                    dev::mbar_arrive_expect_tx(bar, kvb * n);
+                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    for (uint32_t i = 0; i < n; ++i) load_kv(st + i * LL::PL * LL::KT, bar, 2, h, vs * VPS + i);
                 }
             }
         }
@@ -267,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
         a_off[kk] = (mt * 16 + r7 + b1 * 8) * 128 + (((kk * 2 + hb) ^ r7) << 4);
         b_off[kk] = LL::PL * kQT + r7 * 128 + (((kk * 2 + b1) ^ r7) << 4);
     }
-    // V fragments (ldmatrix.trans) of n8 tiles kON*wq + 2i + {0, 1}, within a V stage
+    // V fragments (ldmatrix.trans) of n8 tiles kON*wq + 2i + {0, 1}, within a V chunk
     uint32_t v_off[kON / 2];
 #pragma unroll
     for (int i = 0; i < kON / 2; ++i)
@@ -279,14 +307,35 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
     };
     const float bw = a.tt.wflag ? a.bias : 0.f, bg = a.tt.gflag ? a.bias : 0.f;
     const uint64_t ldc = a.C;
-    Ring<NQ> rq;
-    Ring<NV> rv;
+    uint8_t* ost = sm + LL::ost + warp * LL::OST;
+    Ring r(NS);
+    if (a.load_only) {  // diagnostics: the producer's feed rate alone
+        for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x)
+            for (uint32_t k = 0; k < heads * (nch + nvs); ++k, r.next()) {
+                dev::mbar_wait(&full[r.slot], r.phase);
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
+            }
+        return;
+    }
     for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
         const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
         const uint32_t a0 = qb * kQBlock;
         const uint32_t nqh = min(uint32_t(kQBlock), a.nq - a0);
         const uint32_t R = a.tt.kv_count[qb];
         const uint8_t* gm = a.tt.gmult + size_t(qb) * kKvMax;
+        int ngc[KC];  // global tokens on this lane's columns (the same for every query of the block)
+#pragma unroll
+        for (int k = 0; k < KC; ++k) ngc[k] = lane + 32 * k < int(R) ? gm[lane + 32 * k] : 0;
+        // window column ranges of this warp's softmax rows warp + kConsumerWarps * i, read
+        // once per item (their latency hides under the S phase)
+        constexpr int kRows = kQBlock / kConsumerWarps;
+        uint32_t wl[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const uint32_t rr = warp + kConsumerWarps * i;
+            wl[i] = rr < nqh ? uint32_t(a.tt.wlo[a0 + rr]) | uint32_t(a.tt.whi[a0 + rr]) << 8 : 0u;
+        }
         for (uint32_t h = 0; h < heads; ++h) {
             // ---------------- S = Q K^T ----------------
             // warp: m tile mt (16 queries) x n8 tiles wq, wq + kWQ, ... of the RP key columns
@@ -295,9 +344,9 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
             for (int j = 0; j < NJ; ++j)
 #pragma unroll
                 for (int x = 0; x < NA; ++x) acc[j][x][0] = acc[j][x][1] = acc[j][x][2] = acc[j][x][3] = 0.f;
-            for (uint32_t ch = 0; ch < nch; ++ch, rq.next()) {
-                dev::mbar_wait(&qfull[rq.slot], rq.phase);
-                const uint32_t st = sbase + rq.slot * LL::QKST;
+            for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
+                dev::mbar_wait(&full[r.slot], r.phase);
+                const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                 const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
 #pragma unroll
                 for (int kk = 0; kk < kDC / 16; ++kk) {
@@ -322,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&qempty[rq.slot]);
+                if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
             }
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
@@ -341,51 +390,69 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
             // Column c of the block's K/V list carries query qa's window token iff
             // wlo <= c <= whi, and gmult[c] global tokens; p_c = [window] e^(l_w - m) +
             // gmult[c] e^(l_g - m), summed one token at a time. A warp owns whole rows.
-            for (uint32_t r = warp; r < nqh; r += kConsumerWarps) {
-                const float* row = sp + r * SP;
-                const uint32_t qa = a0 + r;
-                const int lo = a.tt.wlo[qa], hi = a.tt.whi[qa];
-                float sv[KC], pv[KC];
-                bool inw[KC];
-                int ng[KC];
-                float m = -INFINITY;
+            // two rows per pass (independent shuffle chains); the block's global-token
+            // multiplicities per column were read once per item (ngc)
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    const int c = lane + 32 * k;
-                    const bool ok = c < int(R);
-                    sv[k] = ok ? a.scale * row[c] : 0.f;
-                    inw[k] = ok && c >= lo && c <= hi;
-                    ng[k] = ok ? gm[c] : 0;
-                    if (inw[k]) m = fmaxf(m, sv[k] + bw);
-                    if (ng[k]) m = fmaxf(m, sv[k] + bg);
-                }
+            for (int i0 = 0; i0 < kRows; i0 += 2) {
+                const uint32_t r0 = warp + kConsumerWarps * i0, r1 = r0 + kConsumerWarps;
+                if (r0 >= nqh) break;
+                const bool two = r1 < nqh;
+                float sv[2][KC], pv[2][KC], m[2] = {-INFINITY, -INFINITY}, z[2] = {0.f, 0.f};
+                bool inw[2][KC];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                float z = 0.f;
+                for (int w = 0; w < 2; ++w) {
+                    const uint32_t rr = w ? (two ? r1 : r0) : r0;
+                    const float* row = sp + rr * SP;
+                    const uint32_t wlh = wl[w ? (two ? i0 + 1 : i0) : i0];
+                    const int lo = int(wlh & 0xFFu), hi = int(wlh >> 8);
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    float e = inw[k] ? expf(sv[k] + bw - m) : 0.f;
-                    if (ng[k]) {
-                        const float eg = expf(sv[k] + bg - m);
-                        for (int t = 0; t < ng[k]; ++t) e += eg;
+                    for (int k = 0; k < KC; ++k) {
+                        const int c = lane + 32 * k;
+                        const bool ok = c < int(R);
+                        sv[w][k] = ok ? a.scale * row[c] : 0.f;
+                        inw[w][k] = ok && c >= lo && c <= hi;
+                        if (inw[w][k]) m[w] = fmaxf(m[w], sv[w][k] + bw);
+                        if (ngc[k]) m[w] = fmaxf(m[w], sv[w][k] + bg);
                     }
-                    pv[k] = e;
-                    z += e;
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-                const float zi = 1.0f / z;
+                for (int o = 16; o > 0; o >>= 1) {
+                    m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
+                    m[1] = fmaxf(m[1], __shfl_xor_sync(0xffffffffu, m[1], o));
+                }
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    const uint32_t c = lane + 32 * k;
-                    if (c < RP) {
-                        const uint32_t off = LL::pb + (c >> 6) * (kQBlock * 128) + swz(r, (c & 63) >> 3) + (c & 7) * 2;
-                        const float v = pv[k] * zi;
-                        const __nv_bfloat16 vh = __float2bfloat16_rn(v);
-                        *reinterpret_cast<__nv_bfloat16*>(sm + off) = vh;
-                        if (SPLIT)
-                            *reinterpret_cast<__nv_bfloat16*>(sm + off + LL::PB) =
-                                __float2bfloat16_rn(v - __bfloat162float(vh));
+                for (int w = 0; w < 2; ++w)
+#pragma unroll
+                    for (int k = 0; k < KC; ++k) {
+                        float e = inw[w][k] ? (SPLIT ? expf(sv[w][k] + bw - m[w]) : __expf(sv[w][k] + bw - m[w])) : 0.f;
+                        if (ngc[k])  // the column's ngc global tokens, each e^(l_g - m)
+                            e += float(ngc[k]) * (SPLIT ? expf(sv[w][k] + bg - m[w]) : __expf(sv[w][k] + bg - m[w]));
+                        pv[w][k] = e;
+                        z[w] += e;
+                    }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    z[0] += __shfl_xor_sync(0xffffffffu, z[0], o);
+                    z[1] += __shfl_xor_sync(0xffffffffu, z[1], o);
+                }
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    if (w == 1 && !two) break;
+                    const uint32_t rr = w ? r1 : r0;
+                    const float zi = 1.0f / z[w];
+#pragma unroll
+                    for (int k = 0; k < KC; ++k) {
+                        const uint32_t c = lane + 32 * k;
+                        if (c < RP) {
+                            const uint32_t off =
+                                LL::pb + (c >> 6) * (kQBlock * 128) + swz(rr, (c & 63) >> 3) + (c & 7) * 2;
+                            const float v = pv[w][k] * zi;
+                            const __nv_bfloat16 vh = __float2bfloat16_rn(v);
+                            *reinterpret_cast<__nv_bfloat16*>(sm + off) = vh;
+                            if (SPLIT)
+                                *reinterpret_cast<__nv_bfloat16*>(sm + off + LL::PB) =
+                                    __float2bfloat16_rn(v - __bfloat162float(vh));
+                        }
                     }
                 }
             }
@@ -401,87 +468,88 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
                     if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pal[LL::PREG && SPLIT ? kq : 0]);
                 }
             }
-            uint8_t* ost = sm + LL::ost + warp * LL::OST;
-            for (uint32_t ch = 0; ch < nch; ++ch, rv.next()) {
-                dev::mbar_wait(&vfull[rv.slot], rv.phase);
-                const uint32_t st = sbase + LL::vring + rv.slot * LL::VST;
-                const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
-                const uint32_t c0w = uint32_t(wq) * kON * 8;  // this warp's first column in the chunk
-                const bool live = c0w < vw;
-                float o[kON][4];
+            for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
+                dev::mbar_wait(&full[r.slot], r.phase);
+                const uint32_t n = min(VPS, nch - vs * VPS);
+                for (uint32_t i = 0; i < n; ++i) {
+                    const uint32_t ch = vs * VPS + i;
+                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST + i * LL::PL * LL::KT;
+                    const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
+                    const uint32_t c0w = uint32_t(wq) * kON * 8;  // this warp's first column in the chunk
+                    const bool live = c0w < vw;
+                    float o[kON][4];
 #pragma unroll
-                for (int n = 0; n < kON; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-                if (live) {
+                    for (int nn = 0; nn < kON; ++nn) o[nn][0] = o[nn][1] = o[nn][2] = o[nn][3] = 0.f;
+                    if (live) {
 #pragma unroll
-                    for (int kq = 0; kq < NTL / 2; ++kq) {
-                        uint32_t pf[4], pfl[4];
-                        if (LL::PREG) {
+                        for (int kq = 0; kq < NTL / 2; ++kq) {
+                            uint32_t pf[4], pfl[4];
+                            if (LL::PREG) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) pf[k] = pa[LL::PREG ? kq : 0][k];
-                            if (SPLIT)
+                                for (int k = 0; k < 4; ++k) pf[k] = pa[LL::PREG ? kq : 0][k];
+                                if (SPLIT)
 #pragma unroll
-                                for (int k = 0; k < 4; ++k) pfl[k] = pal[LL::PREG && SPLIT ? kq : 0][k];
-                        } else {
-                            ldsm_x4(p_addr(kq), pf);
-                            if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pfl);
-                        }
+                                    for (int k = 0; k < 4; ++k) pfl[k] = pal[LL::PREG && SPLIT ? kq : 0][k];
+                            } else {
+                                ldsm_x4(p_addr(kq), pf);
+                                if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pfl);
+                            }
 #pragma unroll
-                        for (int i2 = 0; i2 < kON / 2; ++i2) {
-                            uint32_t b[4];
-                            ldsm_x4_t(st + v_off[i2] + kq * 2048, b);
-                            mma_bf16(o[2 * i2], pf, b[0], b[1]);
-                            mma_bf16(o[2 * i2 + 1], pf, b[2], b[3]);
-                            if (SPLIT) {
-                                uint32_t bl[4];
-                                ldsm_x4_t(st + LL::KT + v_off[i2] + kq * 2048, bl);
-                                mma_bf16(o[2 * i2], pf, bl[0], bl[1]);
-                                mma_bf16(o[2 * i2 + 1], pf, bl[2], bl[3]);
-                                mma_bf16(o[2 * i2], pfl, b[0], b[1]);
-                                mma_bf16(o[2 * i2 + 1], pfl, b[2], b[3]);
+                            for (int i2 = 0; i2 < kON / 2; ++i2) {
+                                uint32_t b[4];
+                                ldsm_x4_t(st + v_off[i2] + kq * 2048, b);
+                                mma_bf16(o[2 * i2], pf, b[0], b[1]);
+                                mma_bf16(o[2 * i2 + 1], pf, b[2], b[3]);
+                                if (SPLIT) {
+                                    uint32_t bl[4];
+                                    ldsm_x4_t(st + LL::KT + v_off[i2] + kq * 2048, bl);
+                                    mma_bf16(o[2 * i2], pf, bl[0], bl[1]);
+                                    mma_bf16(o[2 * i2 + 1], pf, bl[2], bl[3]);
+                                    mma_bf16(o[2 * i2], pfl, b[0], b[1]);
+                                    mma_bf16(o[2 * i2 + 1], pfl, b[2], b[3]);
+                                }
                             }
                         }
+                        // accumulators -> staging [16 rows][kON*8 cols] (bf16; lo plane after it)
+#pragma unroll
+                        for (int nn = 0; nn < kON; ++nn) {
+                            const uint32_t o0 = uint32_t(g) * kOPitch + (nn * 8 + t4 * 2) * 2, o1 = o0 + 8 * kOPitch;
+                            if (SPLIT) {
+                                uint32_t h0, l0, h1, l1;
+                                split2(o[nn][0], o[nn][1], h0, l0);
+                                split2(o[nn][2], o[nn][3], h1, l1);
+                                *reinterpret_cast<uint32_t*>(ost + o0) = h0;
+                                *reinterpret_cast<uint32_t*>(ost + o1) = h1;
+                                *reinterpret_cast<uint32_t*>(ost + 16 * kOPitch + o0) = l0;
+                                *reinterpret_cast<uint32_t*>(ost + 16 * kOPitch + o1) = l1;
+                            } else {
+                                *reinterpret_cast<uint32_t*>(ost + o0) = pack_bf16(o[nn][0], o[nn][1]);
+                                *reinterpret_cast<uint32_t*>(ost + o1) = pack_bf16(o[nn][2], o[nn][3]);
+                            }
+                        }
+                        __syncwarp();
+                        // 16 rows x kON 16-byte pieces: row rr -> query a0 + 16 mt + rr
+                        constexpr int kPieces = 16 * kON;
+#pragma unroll
+                        for (int i2 = 0; i2 < (kPieces + 31) / 32; ++i2) {
+                            const uint32_t pc = lane + 32 * i2;
+                            const uint32_t rr = pc / kON, part = pc % kON;
+                            const uint32_t q = mt * 16 + rr, col = c0w + part * 8;
+                            if (pc < uint32_t(kPieces) && q < nqh && col < vw) {
+                                __nv_bfloat16* dst =
+                                    a.ctx + (uint64_t(a0 + q) * a.HW + p) * ldc + h * a.d + ch * kDC + col;
+                                *reinterpret_cast<uint4*>(dst) =
+                                    *reinterpret_cast<const uint4*>(ost + rr * kOPitch + part * 16);
+                                if (SPLIT)
+                                    *reinterpret_cast<uint4*>(dst + a.ctx_lo) =
+                                        *reinterpret_cast<const uint4*>(ost + 16 * kOPitch + rr * kOPitch + part * 16);
+                            }
+                        }
+                        __syncwarp();  // staging is rewritten by the next chunk
                     }
                 }
                 __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&vempty[rv.slot]);
-                if (live) {
-                    // accumulators -> staging [16 rows][kON*8 cols] (bf16; lo plane after it)
-#pragma unroll
-                    for (int n = 0; n < kON; ++n) {
-                        const uint32_t o0 = uint32_t(g) * kOPitch + (n * 8 + t4 * 2) * 2, o1 = o0 + 8 * kOPitch;
-                        if (SPLIT) {
-                            uint32_t h0, l0, h1, l1;
-                            split2(o[n][0], o[n][1], h0, l0);
-                            split2(o[n][2], o[n][3], h1, l1);
-                            *reinterpret_cast<uint32_t*>(ost + o0) = h0;
-                            *reinterpret_cast<uint32_t*>(ost + o1) = h1;
-                            *reinterpret_cast<uint32_t*>(ost + 16 * kOPitch + o0) = l0;
-                            *reinterpret_cast<uint32_t*>(ost + 16 * kOPitch + o1) = l1;
-                        } else {
-                            *reinterpret_cast<uint32_t*>(ost + o0) = pack_bf16(o[n][0], o[n][1]);
-                            *reinterpret_cast<uint32_t*>(ost + o1) = pack_bf16(o[n][2], o[n][3]);
-                        }
-                    }
-                    __syncwarp();
-                    // 16 rows x kON 16-byte pieces: row r -> query a0 + 16 mt + r
-                    constexpr int kPieces = 16 * kON;
-#pragma unroll
-                    for (int i2 = 0; i2 < (kPieces + 31) / 32; ++i2) {
-                        const uint32_t pc = lane + 32 * i2;
-                        const uint32_t r = pc / kON, part = pc % kON;
-                        const uint32_t q = mt * 16 + r, col = c0w + part * 8;
-                        if (pc < uint32_t(kPieces) && q < nqh && col < vw) {
-                            __nv_bfloat16* dst =
-                                a.ctx + (uint64_t(a0 + q) * a.HW + p) * ldc + h * a.d + ch * kDC + col;
-                            *reinterpret_cast<uint4*>(dst) =
-                                *reinterpret_cast<const uint4*>(ost + r * kOPitch + part * 16);
-                            if (SPLIT)
-                                *reinterpret_cast<uint4*>(dst + a.ctx_lo) =
-                                    *reinterpret_cast<const uint4*>(ost + 16 * kOPitch + r * kOPitch + part * 16);
-                        }
-                    }
-                    __syncwarp();  // staging is rewritten by the next chunk
-                }
+                if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
             }
         }
     }
@@ -493,7 +561,7 @@ int g_sms = 0;
 // {64 head-dim elements, 1 head, 1 position, 32 >> kind frames}, 128-byte swizzle; head-dim
 // elements past d read as zero.
 int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames, uint32_t HW, uint32_t C,
-              uint32_t heads) {
+              uint32_t heads, int layout) {
     auto fn = get_encode_fn();
     if (!fn) return int(cudaErrorNotSupported);
     const uint32_t d = C / heads;
@@ -504,30 +572,54 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
                 m.box[pl][k] = m.box[0][k];
                 continue;
             }
-            cuuint64_t gdim[4] = {d, 3ull * heads, HW, frames};
-            // frame-major [frames][HW][3C] rows (position stride 3C, frame stride HW 3C), or
-            // position-major [HW][frames][3C] (diagnostics: g_attn_pos_major)
+            // frame-major [frames][HW][3C] rows (position stride 3C, frame stride HW 3C),
+            // position-major [HW][frames][3C], or chunked [HW][3C/64][frames][64]
             const uint64_t row = uint64_t(C) * 3 * 2;
-            cuuint64_t gstride[3] = {uint64_t(d) * 2, g_attn_pos_major ? row * frames : row,
-                                     g_attn_pos_major ? row : row * HW};
+            const bool chunked = layout == 2;
+            cuuint64_t gdim[4] = {d, 3ull * heads, HW, frames};
+            cuuint64_t gstride[3] = {uint64_t(d) * 2, layout ? row * frames : row, layout ? row : row * HW};
             cuuint32_t box[4] = {uint32_t(kDC), 1, 1, 32u >> k};
+            if (chunked) {
+                gdim[0] = kDC;
+                gdim[1] = frames;
+                gdim[2] = 3ull * C / kDC;
+                gdim[3] = HW;
+                gstride[0] = kDC * 2;
+                gstride[1] = uint64_t(frames) * kDC * 2;
+                gstride[2] = (3ull * C / kDC) * frames * kDC * 2;
+                box[1] = 32u >> k;
+                box[3] = 1;
+            }
             cuuint32_t estride[4] = {1, 1, 1, 1};
             const CUresult r = fn(&m.box[pl][k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim,
                                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
         }
+        if (!base) {
+            m.g4[pl] = m.g4[0];
+            continue;
+        }
+        cuuint64_t gdim[2] = {layout == 2 ? uint64_t(kDC) : 3ull * C, layout == 2 ? 3ull * C / kDC * HW * frames
+                                                                                 : uint64_t(HW) * frames};
+        cuuint64_t gstride[1] = {layout == 2 ? uint64_t(kDC) * 2 : uint64_t(C) * 3 * 2};
+        cuuint32_t box[2] = {uint32_t(kDC), 1};
+        cuuint32_t estride[2] = {1, 1};
+        const CUresult r = fn(&m.g4[pl], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
+                              box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
     }
     return 0;
 }
 
 template <int NTL, bool SPLIT>
-int launch_core(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
+int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     using LL = CoreLay<NTL, SPLIT>;
     static bool attr = false;
     if (!attr) {
         const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, SPLIT>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(LL::total));
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return int(e);
         attr = true;
     }
@@ -537,9 +629,17 @@ int launch_core(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
         cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dv);
         if (g_sms <= 0) g_sms = 148;
     }
-    const uint32_t slots = uint32_t(g_sms) * LL::ctas;
+    // CTAs per SM (VINF_ATTN_CTAS, diagnostics) and the ring depth that fits them
+    static const int env_ctas = [] {
+        const char* e = getenv("VINF_ATTN_CTAS");
+        return e ? atoi(e) : 0;
+    }();
+    const int ctas = env_ctas >= 1 && env_ctas <= 4 ? env_ctas : LL::ctas;
+    args.ns = uint32_t(LL::stages(ctas));
+    const uint32_t slots = uint32_t(g_sms) * uint32_t(ctas);
     const uint32_t grid = args.items < slots ? args.items : slots;
-    return int(launch_pdl(attention_core_kernel<NTL, SPLIT>, dim3(grid), dim3(kThreads), LL::total, s, maps, args));
+    return int(launch_pdl(attention_core_kernel<NTL, SPLIT>, dim3(grid), dim3(kThreads), LL::total(int(args.ns)), s,
+                          maps, args));
 }
 
 template <bool SPLIT>
@@ -571,7 +671,8 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     if (reinterpret_cast<uintptr_t>(qkv) % 16 || reinterpret_cast<uintptr_t>(qkv_lo) % 16)
         return int(cudaErrorInvalidValue);
     AttnMaps maps;
-    const int rc = make_maps(maps, qkv, qkv_lo, qkv_frames, HW, C, heads);
+    if (g_attn_pos_major == 2 && (C % kDC || (C / heads) % kDC)) return int(cudaErrorInvalidValue);
+    const int rc = make_maps(maps, qkv, qkv_lo, qkv_frames, HW, C, heads, g_attn_pos_major);
     if (rc) return rc;
     AttnArgs args;
     args.HW = HW;
@@ -583,6 +684,10 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     args.nqb = (nq + kQBlock - 1) / kQBlock;
     args.q_frame0 = q_frame0;
     args.items = HW * args.nqb;
+    args.frames = qkv_frames;
+    args.pos_major = uint32_t(g_attn_pos_major);
+    static const uint32_t load_only = getenv("VINF_ATTN_LOAD_ONLY") ? 1u : 0u;
+    args.load_only = load_only;
     args.scale = scale;
     args.bias = bias;
     args.ctx = static_cast<__nv_bfloat16*>(ctx);

@@ -53,6 +53,7 @@ int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint3
         cudaStream_t s = nullptr;
         cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
         tok.upload(L.tok[1], s);
+        {  // the buffers are freed (stream-ordered) before the stream is destroyed
         const uint64_t plane = uint64_t(L.af) * L.hw * 3 * channels;
         const uint64_t ctxn = uint64_t(L.f_clip) * L.hw * channels;
         TmpBuf qkv(plane * 2 * (f32 ? 2 : 1), s), ctx(ctxn * 2 * (f32 ? 2 : 1), s);
@@ -78,6 +79,7 @@ int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint3
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         g_attn_pos_major = 0;
+        }
         cuda_check(cudaStreamSynchronize(s), "sync");
         tok.release();
         cudaStreamDestroy(s);

@@ -91,8 +91,9 @@ struct HostTokens {
         count[a] = k + 1;
         if (!global) nwin[a] = k + 1;
     }
-    // Builds the per-block K/V lists; call after all push()es.
-    void finalize();
+    // Builds the per-block K/V lists; call after all push()es. gather4: the attention core
+    // may fetch runs of single frames four at a time (head dim a multiple of 64).
+    void finalize(bool gather4 = false);
     // One device blob: rows | biased | col | count | kv_frames | kv_count.
     size_t blob_bytes() const;
     void pack(uint8_t* dst) const;

@@ -290,7 +290,7 @@ void attention_generic(const void* src, vinf_dtype dt, uint32_t frames, uint32_t
     e1.out_bf16 = !f32;
     gemm(A.op, {0}, p->wqkv, {0}, int64_t(rows), 3 * C, e1, f32, s);
     HostTokens tk = tok;
-    tk.finalize();
+    tk.finalize((C / p->heads) % 64 == 0);
     if (!tk.kv_ok) config_error("a query block touches more than 192 distinct frames");
     if ((C / p->heads) % 8 != 0) config_error("attention head dim (C / heads) must be a multiple of 8");
     DevTokens dt_tok;

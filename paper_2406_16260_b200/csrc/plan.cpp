@@ -86,7 +86,7 @@ void predict_groupnorm_traffic(uint32_t frames, uint32_t workers, uint32_t group
 // ---------------------------------------------------------------------------
 // Token tables
 
-void HostTokens::finalize() {
+void HostTokens::finalize(bool gather4) {
     kv_ok = true;
     wflag = gflag = -1;
     for (uint32_t qb = 0; qb < nqb; ++qb) {
@@ -144,18 +144,36 @@ void HostTokens::finalize() {
         const uint16_t* fr = &kv_frames[size_t(qb) * kKvMax];
         const uint32_t R = kv_count[qb];
         uint32_t nb = 0, rows = 0;
+        auto put = [&](uint32_t word) {
+            if (nb >= uint32_t(kKvMax)) config_error("attention K/V load program too long");
+            kv_box[size_t(qb) * kKvMax + nb++] = word;
+        };
         for (uint32_t c0 = 0; c0 < R;) {
             uint32_t len = 1;
             while (c0 + len < R && fr[c0 + len] == fr[c0] + len) ++len;
+            if (gather4 && len == 1) {
+                // a run of isolated frames (sampled globals outside the window band):
+                // four per row-gather while four remain, as 3 words
+                uint32_t n1 = 1;
+                while (c0 + n1 < R && (c0 + n1 + 1 >= R || fr[c0 + n1 + 1] != fr[c0 + n1] + 1)) ++n1;
+                while (n1 >= 4) {
+                    put(uint32_t(fr[c0]) | c0 << 16 | uint32_t(kBoxGather4) << 24);
+                    put(uint32_t(fr[c0 + 1]) | uint32_t(fr[c0 + 2]) << 16);
+                    put(uint32_t(fr[c0 + 3]));
+                    rows += 4;
+                    c0 += 4;
+                    n1 -= 4;
+                }
+                if (n1 == 0) continue;
+                len = 1;
+            }
             uint32_t at = 0;
             while (at < len) {
                 const uint32_t left = len - at;
                 int kind = 0;
                 while ((32u >> kind) > left) ++kind;
                 const uint32_t h = 32u >> kind;
-                if (nb >= uint32_t(kKvMax)) config_error("attention K/V load program too long");
-                kv_box[size_t(qb) * kKvMax + nb++] =
-                    uint32_t(fr[c0 + at]) | (c0 + at) << 16 | uint32_t(kind) << 24;
+                put(uint32_t(fr[c0 + at]) | (c0 + at) << 16 | uint32_t(kind) << 24);
                 rows += h;
                 at += h;
             }
@@ -310,7 +328,7 @@ Layout::Layout(const vinf_engine_desc& desc) : d(desc) {
             for (uint32_t j = 0; j < d.n_global; ++j)
                 tok[b].push(a, b >= 2 ? null_frame : g_frame[j], (b & 1) == 1, true);
         }
-        tok[b].finalize();
+        tok[b].finalize((d.channels / d.heads) % 64 == 0);
         if (!tok[b].kv_ok) config_error("a query block touches more than 192 distinct frames");
     }
 
