@@ -356,6 +356,9 @@ int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint3
                          uint32_t n_local, uint32_t n_global, int f32, int pos_major, int iters, float* avg_ms);
 /* Streaming 16-byte loads over `bytes` of device memory. */
 int vinf_read_bw_bench(uint64_t bytes, int iters, float* avg_ms);
+/* 1-D bulk copies (TMA) of `chunk` bytes into an mbarrier ring of `stages` slots per CTA,
+ * `ctas` CTAs per SM (the attention core's feed without its compute). */
+int vinf_bulk_bw_bench(uint64_t bytes, uint32_t chunk, uint32_t stages, uint32_t ctas, int iters, float* avg_ms);
 
 #ifdef __cplusplus
 }

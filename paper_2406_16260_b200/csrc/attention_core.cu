@@ -50,7 +50,7 @@ constexpr uint32_t kOPitch = kON * 16 + 16;  // ctx staging row pitch (bytes, co
 constexpr uint32_t kQT = kQBlock * 128;  // one plane of a Q chunk (32 rows x 128 B)
 
 struct AttnMaps {
-    CUtensorMap box[2][kBoxKinds];  // [plane][kind]: boxes {64, 1, 1, 32 >> kind}
+    CUtensorMap box[2][kBoxKinds];  // [plane][kind]: boxes of kind + 1 frames x 64 head-dim elements
     CUtensorMap g4[2];              // [plane]: 2-D rows x 3C view, box {64, 1}, for row gathers
 };
 
@@ -210,10 +210,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
     if (warp == kConsumerWarps) {
         // ---------------- producer: one thread issues every TMA load ----------------
         if (lane != 0) return;
-        for (int pl = 0; pl < int(LL::PL); ++pl) {
-            for (int k = 0; k < kBoxKinds; ++k) dev::tma_prefetch_desc(&maps.box[pl][k]);
-            dev::tma_prefetch_desc(&maps.g4[pl]);
-        }
+        for (int pl = 0; pl < int(LL::PL); ++pl) dev::tma_prefetch_desc(&maps.g4[pl]);
         Ring r(NS);
         for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
             const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
@@ -264,13 +261,9 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
                     uint64_t* bar = &full[r.slot];
                     dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
-                    // the block's query rows exactly: boxes of 16, 8, ... rows (32 = one box)
-                    for (uint32_t k = 0, q = 0; k < uint32_t(kBoxKinds); ++k)
-                        if (nqh & (32u >> k)) {
-                            for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                                box4(st + pl * kQT + q * 128u, &maps.box[pl][k], bar, 0, h, ch, uint32_t(qf) + q);
-                            q += 32u >> k;
-                        }
+                    // the block's query rows exactly, one box
+                    for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                        box4(st + pl * kQT, &maps.box[pl][nqh - 1], bar, 0, h, ch, uint32_t(qf));
                     load_kv(st + LL::PL * kQT, bar, 1, h, ch);
                 }
                 for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {  // PV phase: VPS V chunks
@@ -558,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
 int g_sms = 0;
 
 // 4-D view of the [frames][HW][3 x heads][d] Q/K/V buffer (one bf16 plane): boxes of
-// {64 head-dim elements, 1 head, 1 position, 32 >> kind frames}, 128-byte swizzle; head-dim
+// {64 head-dim elements, 1 head, 1 position, kind + 1 frames}, 128-byte swizzle; head-dim
 // elements past d read as zero.
 int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames, uint32_t HW, uint32_t C,
               uint32_t heads, int layout) {
@@ -578,7 +571,7 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
             const bool chunked = layout == 2;
             cuuint64_t gdim[4] = {d, 3ull * heads, HW, frames};
             cuuint64_t gstride[3] = {uint64_t(d) * 2, layout ? row * frames : row, layout ? row : row * HW};
-            cuuint32_t box[4] = {uint32_t(kDC), 1, 1, 32u >> k};
+            cuuint32_t box[4] = {uint32_t(kDC), 1, 1, uint32_t(k) + 1};
             if (chunked) {
                 gdim[0] = kDC;
                 gdim[1] = frames;
@@ -587,7 +580,7 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
                 gstride[0] = kDC * 2;
                 gstride[1] = uint64_t(frames) * kDC * 2;
                 gstride[2] = (3ull * C / kDC) * frames * kDC * 2;
-                box[1] = 32u >> k;
+                box[1] = uint32_t(k) + 1;
                 box[3] = 1;
             }
             cuuint32_t estride[4] = {1, 1, 1, 1};
@@ -670,10 +663,44 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     if (!attention_core_supported(C, heads, tt)) return int(cudaErrorInvalidValue);
     if (reinterpret_cast<uintptr_t>(qkv) % 16 || reinterpret_cast<uintptr_t>(qkv_lo) % 16)
         return int(cudaErrorInvalidValue);
-    AttnMaps maps;
     if (g_attn_pos_major == 2 && (C % kDC || (C / heads) % kDC)) return int(cudaErrorInvalidValue);
-    const int rc = make_maps(maps, qkv, qkv_lo, qkv_frames, HW, C, heads, g_attn_pos_major);
-    if (rc) return rc;
+    // 66 tensor maps per buffer: encoded once per (buffer, shape, layout), then reused
+    struct Cached {
+        const void *q = nullptr, *ql = nullptr;
+        uint32_t frames = 0, HW = 0, C = 0, heads = 0;
+        int layout = -1;
+        AttnMaps maps;
+    };
+    static std::mutex mu;
+    static Cached cache[8];
+    static int cache_next = 0;
+    AttnMaps maps;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        int hit = -1;
+        for (int i = 0; i < 8; ++i) {
+            const Cached& c = cache[i];
+            if (c.q == qkv && c.ql == qkv_lo && c.frames == qkv_frames && c.HW == HW && c.C == C && c.heads == heads &&
+                c.layout == g_attn_pos_major)
+                hit = i;
+        }
+        if (hit < 0) {
+            Cached& c = cache[cache_next];
+            c.layout = -1;
+            const int rc = make_maps(c.maps, qkv, qkv_lo, qkv_frames, HW, C, heads, g_attn_pos_major);
+            if (rc) return rc;
+            c.q = qkv;
+            c.ql = qkv_lo;
+            c.frames = qkv_frames;
+            c.HW = HW;
+            c.C = C;
+            c.heads = heads;
+            c.layout = g_attn_pos_major;
+            hit = cache_next;
+            cache_next = (cache_next + 1) % 8;
+        }
+        maps = cache[hit].maps;
+    }
     AttnArgs args;
     args.HW = HW;
     args.C = C;
@@ -706,7 +733,66 @@ __global__ void read_bw_kernel(const uint4* __restrict__ p, uint64_t n, uint32_t
     }
     if (acc == 0x12345678u) *sink = acc;
 }
+// 1-D bulk copies of `chunk` bytes into a ring of `stages` smem slots, one issuing thread
+// per CTA, the CTA's 4 other warps release the slots (the shape of the attention core's feed).
+__global__ void __launch_bounds__(160) bulk_bw_kernel(const uint8_t* __restrict__ p, uint64_t bytes, uint32_t chunk,
+                                                        uint32_t stages) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + stages * chunk);
+    uint64_t* empty = full + stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < stages; ++s) {
+            dev::mbar_init(&full[s], 1);
+            dev::mbar_init(&empty[s], 4);
+        }
+        dev::fence_barrier_init();
+    }
+    __syncthreads();
+    const uint64_t n = bytes / chunk;
+    Ring r(stages);
+    if (warp == 4) {
+        if (lane) return;
+        for (uint64_t i = blockIdx.x; i < n; i += gridDim.x, r.next()) {
+            dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
+            dev::mbar_arrive_expect_tx(&full[r.slot], chunk);
+            dev::bulk_g2s(dev::smem_u32(sm + r.slot * chunk), p + i * chunk, chunk, &full[r.slot]);
+        }
+        return;
+    }
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x, r.next()) {
+        dev::mbar_wait(&full[r.slot], r.phase);
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
+    }
+}
 }  // namespace
+
+// Diagnostics: the feed above over `bytes` with ctas CTAs per SM (average ms).
+int bulk_bw_bench(uint64_t bytes, uint32_t chunk, uint32_t stages, uint32_t ctas, int iters, float* ms) {
+    void* buf = nullptr;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) return int(cudaErrorMemoryAllocation);
+    cudaMemset(buf, 1, bytes);
+    if (g_sms == 0) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
+    const uint32_t smem = stages * chunk + stages * 16 + 64;
+    cudaFuncSetAttribute(bulk_bw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    bulk_bw_kernel<<<g_sms * ctas, 160, smem>>>(static_cast<const uint8_t*>(buf), bytes, chunk, stages);
+    cudaEventRecord(a);
+    for (int i = 0; i < iters; ++i)
+        bulk_bw_kernel<<<g_sms * ctas, 160, smem>>>(static_cast<const uint8_t*>(buf), bytes, chunk, stages);
+    cudaEventRecord(b);
+    const cudaError_t e = cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    *ms = t / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    return int(e);
+}
 
 // Diagnostics: streaming 16-byte loads over `bytes` (average ms over iters).
 int read_bw_bench(uint64_t bytes, int iters, float* ms) {

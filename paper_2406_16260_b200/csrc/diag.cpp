@@ -12,6 +12,7 @@
 namespace vinf {
 int guarded_call(const std::function<void()>& f);
 int read_bw_bench(uint64_t bytes, int iters, float* ms);
+int bulk_bw_bench(uint64_t bytes, uint32_t chunk, uint32_t stages, uint32_t ctas, int iters, float* ms);
 }  // namespace vinf
 
 using namespace vinf;
@@ -22,6 +23,13 @@ int vinf_read_bw_bench(uint64_t bytes, int iters, float* ms) {
     return guarded_call([&] {
         if (!ms || iters <= 0 || bytes < 16) shape_error("bad arguments");
         cuda_check(read_bw_bench(bytes, iters, ms), "read bandwidth probe");
+    });
+}
+
+int vinf_bulk_bw_bench(uint64_t bytes, uint32_t chunk, uint32_t stages, uint32_t ctas, int iters, float* ms) {
+    return guarded_call([&] {
+        if (!ms || iters <= 0 || chunk % 16 || !stages) shape_error("bad arguments");
+        cuda_check(bulk_bw_bench(bytes, chunk, stages, ctas, iters, ms), "bulk bandwidth probe");
     });
 }
 

@@ -85,7 +85,7 @@ struct TokenTable {
     int kv_ok;                  // every block's K/V list fits kKvMax
     int max_kv;                 // largest K/V list over the blocks
     // TMA load program of each block's K/V list: the sorted distinct frames split into
-    // contiguous runs, each run into boxes of 32/16/8/4/2/1 frame rows (kind 0..5), box i
+    // contiguous runs, each run into boxes of <= 32 frame rows (kind = rows - 1), box i
     // packed as frame | smem row << 16 | kind << 24 in kv_box[qb][i] (kv_nbox words); runs of
     // single frames may come as row gathers (kBoxGather4, 3 words). kv_load_rows = the rows
     // those boxes write (= kv_count: the transaction bytes of a K or V stage / 128 B).
@@ -93,9 +93,9 @@ struct TokenTable {
     const uint16_t* kv_nbox;    // [nqb]
     const uint16_t* kv_load_rows;  // [nqb]
 };
-constexpr int kBoxKinds = 6;     // box heights 32 >> kind
-constexpr int kBoxGather4 = 6;   // entry kind: four single frames by one row gather (3 words:
-                                 // f0 | row << 16 | kind << 24, f1 | f2 << 16, f3)
+constexpr int kBoxKinds = 32;       // box heights kind + 1 (one TMA op per run of <= 32 frames)
+constexpr int kBoxGather4 = 0xFE;   // entry kind: four single frames by one row gather (3 words:
+                                    // f0 | row << 16 | kind << 24, f1 | f2 << 16, f3)
 
 // Whether the core runs this configuration: head dim d = C / heads with d % 8 == 0 and
 // every query block's distinct K/V frames <= kKvMax. There is no other attention kernel:

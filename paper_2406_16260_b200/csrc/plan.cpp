@@ -138,8 +138,9 @@ void HostTokens::finalize(bool gather4) {
     }
     if (wflag < 0) wflag = 0;
     if (gflag < 0) gflag = 0;
-    // TMA box program: runs of consecutive frames, each covered exactly by boxes of 32,
-    // 16, ... 1 rows (no box reads a frame the block does not use: every byte is traffic)
+    // TMA box program: runs of consecutive frames, each covered exactly by boxes of <= 32
+    // rows (one TMA op per run: the copy engine's per-op cost, not bytes, bounds small boxes;
+    // no box reads a frame the block does not use)
     for (uint32_t qb = 0; qb < nqb && kv_ok; ++qb) {
         const uint16_t* fr = &kv_frames[size_t(qb) * kKvMax];
         const uint32_t R = kv_count[qb];
@@ -169,11 +170,8 @@ void HostTokens::finalize(bool gather4) {
             }
             uint32_t at = 0;
             while (at < len) {
-                const uint32_t left = len - at;
-                int kind = 0;
-                while ((32u >> kind) > left) ++kind;
-                const uint32_t h = 32u >> kind;
-                put(uint32_t(fr[c0 + at]) | (c0 + at) << 16 | uint32_t(kind) << 24);
+                const uint32_t h = std::min<uint32_t>(len - at, uint32_t(kBoxKinds));
+                put(uint32_t(fr[c0 + at]) | (c0 + at) << 16 | (h - 1) << 24);
                 rows += h;
                 at += h;
             }
