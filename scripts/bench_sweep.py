@@ -4,7 +4,8 @@ roofline fraction, at the configs[1] block shape (40x64 latent, C=640, bf16, 1 G
     python scripts/bench_sweep.py [--steps K] [--out gpurun_out/cfg5_sweep.json]
 
 n_global <= F and n_local / 2 <= F: at the 24-frame clip n_global runs 4..16; the 64-frame
-rows extend it to 32 and 64. Each point: frames/s of the whole block (device-resident, CUDA
+rows extend it to 32 and 64, the 288-frame rows (one GPU's clip of 2,304 frames over 8) run
+4..64 at long-clip block shapes. Each point: frames/s of the whole block (device-resident, CUDA
 events), the attention core's time and its HBM roofline fraction (Q, K, V read once + ctx
 written), and the block's fraction of the sustained tensor peak."""
 import argparse
@@ -32,6 +33,9 @@ def main():
     hbm, _, tf_sus, src = peaks()
     points = [(24, g, l) for g in (4, 8, 16) for l in (2, 4, 8, 16, 32)]
     points += [(64, g, l) for g in (32, 64) for l in (2, 8, 16, 32)]
+    # one GPU's clip of the 2,304-frame video over 8 GPUs: long clips, where the window band
+    # and the sampled globals make 32-query blocks with up to 95 distinct K/V frames
+    points += [(288, g, l) for g in (4, 16, 64) for l in (2, 16, 32)]
     rows = []
     for F, ng, nl in points:
         d = en.make_desc(F, 1, 0, H, W, C, 3, 32, 1, nl, ng, 10.0, 800.0, 1e-5, 0.0, 1, torch.bfloat16)
