@@ -354,6 +354,10 @@ int vinf_gemm_bench(uint32_t M, uint32_t N, uint32_t K, uint32_t nseg, int flags
  * over a synthetic Q/K/V buffer; pos_major = 1 views it as [HW][frames][3C]. */
 int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint32_t channels, uint32_t heads,
                          uint32_t n_local, uint32_t n_global, int f32, int pos_major, int iters, float* avg_ms);
+/* The attention core's feed for later launches: 0 = by configuration (TMA ring for bf16
+ * blocks of <= 32 distinct K/V frames, cp.async ring otherwise), 1 = TMA ring, 2 = cp.async
+ * ring. Returns the previous setting. */
+int vinf_debug_attention_impl(int impl);
 /* Streaming 16-byte loads over `bytes` of device memory. */
 int vinf_read_bw_bench(uint64_t bytes, int iters, float* avg_ms);
 /* 1-D bulk copies (TMA) of `chunk` bytes into an mbarrier ring of `stages` slots per CTA,

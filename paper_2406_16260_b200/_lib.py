@@ -162,6 +162,7 @@ _SIGS = {
                                            _u64p, C.c_uint32, _u32p]),
     "vinf_attention_bench": (C.c_int, [C.c_uint32] * 7 + [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "vinf_read_bw_bench": (C.c_int, [C.c_uint64, C.c_int, C.POINTER(C.c_float)]),
+    "vinf_debug_attention_impl": (C.c_int, [C.c_int]),
     "vinf_bulk_bw_bench": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(C.c_float)]),
     # clip-parallel executor (communicators)
     "vinf_comm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),

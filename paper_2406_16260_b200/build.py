@@ -20,7 +20,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libvinf_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["gemm_tc.cu", "elementwise.cu", "groupnorm.cu", "attention_core.cu", "plan.cpp", "ops.cpp",
+SOURCES = ["gemm_tc.cu", "elementwise.cu", "groupnorm.cu", "attention_core.cu", "attention_cpasync.cu", "plan.cpp", "ops.cpp",
            "engine.cpp", "comm.cpp", "capi.cpp", "runapi.cpp", "diag.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "--expt-relaxed-constexpr",

@@ -1,27 +1,29 @@
-// Dual-scope attention core (attend_tokens, ops.cpp:209-241, applied per spatial position
-// as in dual_scope_reference ops.cpp:318-336 and attention_parallel clip_parallel.cpp:311-334).
-// The Q/K/V projections run before it as tcgen05 GEMMs; this kernel does only the banded +
-// global token mixing, ~1.5% of the block's flops, bound by reading Q/K/V once and writing
-// ctx once. One kernel serves every configuration:
+// Dual-scope attention core, TMA ring (attend_tokens, ops.cpp:209-241, applied per spatial
+// position as in dual_scope_reference ops.cpp:318-336 and attention_parallel
+// clip_parallel.cpp:311-334). The Q/K/V projections run before it as tcgen05 GEMMs; the core
+// does only the banded + global token mixing, ~1.5% of the block's flops, bound by reading
+// Q/K/V once and writing ctx once. launch_attention_core feeds narrow bf16 tiles
+// (<= 32 distinct K/V frames per 32-query block: the 24-frame VideoCrafter2 clip, the
+// headline) through this TMA ring and everything else through attention_cpasync.cu:
 //
 //   * work item = (spatial position p, block of 32 query frames); R = the distinct K/V
-//     frames the block's queries touch (window band + sampled globals, <= kKvMax = 192);
-//   * persistent CTAs, warp-specialised: warp 8 issues TMA loads (4-D tensor maps over the
-//     [frames][HW][3 x heads][d] Q/K/V buffer, 128-byte swizzle, 64-wide head-dim chunks,
-//     zero-filled past the head dim) into an mbarrier ring; the K/V frames of a block come
-//     as a host-built program of boxes of 32/16/8/4/2/1 consecutive frames; warps 0-7
-//     consume: S = Q K^T per head over the chunks, the reference's explicit token softmax
-//     (window tokens then globals, duplicates kept, +bias on the flagged side) in column
-//     form, ctx = P V chunk by chunk, stored straight from the accumulators;
+//     frames the block's queries touch (window band + sampled globals);
+//   * persistent CTAs, warp-specialised: one producer warp issues TMA loads (4-D tensor maps
+//     over the [frames][HW][3 x heads][d] Q/K/V buffer, 128-byte swizzle, 64-wide head-dim
+//     chunks, zero-filled past the head dim) into one mbarrier FIFO ring per CTA: a block's
+//     query rows are one box, its K/V frames a host-built program of one box per run of
+//     consecutive frames (<= 32 rows) or one row gather per four isolated frames; four
+//     consumer warps: S = Q K^T per head over the chunks, the reference's explicit token
+//     softmax (window tokens then globals, duplicates kept, +bias on the flagged side) in
+//     column form, ctx = P V chunk by chunk through per-warp staging to 16-byte stores;
 //   * mma.sync m16n8k16 bf16 -> fp32 (tcgen05 needs M >= 64; a block has <= 32 queries, 24 at
 //     the VideoCrafter2 clip);
 //   * bf16 mode: Q/K/V and ctx are bf16; split mode (the fp32 engine mode): each is two bf16
 //     planes hi = RN(x), lo = RN(x - hi) and every product runs as hi*hi + hi*lo + lo*hi (S
 //     and PV), the same bf16x3 arithmetic as the fp32-mode GEMMs.
 //
-// The ring keeps loading the next item's chunks while the consumers run a softmax or finish
-// the last PV chunks, so HBM stays busy across items; no __syncthreads in the steady state
-// (two named barriers of the consumer warps per head around the softmax).
+// The FIFO keeps a fixed prefetch distance across phases and items: V chunks load during the
+// softmax, the next item's Q/K chunks during the PV phase.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -30,6 +32,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -38,15 +41,23 @@ namespace vinf {
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn();
 int g_attn_pos_major = 0;
+int g_attn_impl = []() {  // 0 = by configuration, 1 = TMA ring, 2 = cp.async ring (diagnostics)
+    const char* e = getenv("VINF_ATTN_IMPL");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "tma" ? 1 : v == "cpasync" ? 2 : 0;
+}();
 
 namespace {
 
 constexpr int kDC = 64;  // head-dim chunk (one 128-byte swizzle row of bf16)
-constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + the producer warp
-constexpr int kWQ = kConsumerWarps / 2;  // warps per 16-query m tile
-constexpr int kON = 8 / kWQ;              // PV: n8 output tiles per warp in a 64-wide chunk
-constexpr uint32_t kOPitch = kON * 16 + 16;  // ctx staging row pitch (bytes, conflict-free)
+// CW consumer warps per CTA (4 or 8) + one producer warp; derived tile constants:
+#define VINF_ATTN_WARP_CONSTANTS(CW)                                                         \
+    static constexpr int kConsumerWarps = CW;                                                  \
+    static constexpr int kThreads = (kConsumerWarps + 1) * 32; /* + the producer warp */      \
+    static constexpr int kWQ = kConsumerWarps / 2;             /* warps per 16-query m tile */ \
+    static constexpr int kON = 8 / kWQ;  /* PV: n8 output tiles per warp in a 64-wide chunk */ \
+    static constexpr uint32_t kOPitch = kON * 16 + 16; /* ctx staging row pitch, conflict-free */
 constexpr uint32_t kQT = kQBlock * 128;  // one plane of a Q chunk (32 rows x 128 B)
 
 struct AttnMaps {
@@ -121,8 +132,9 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
 // One FIFO keeps a fixed prefetch distance across phases and items: V chunks load during the
 // softmax, the next item's Q/K chunks during the PV phase. Several CTAs per SM interleave
 // their phases, so the memory pipe never drains.
-template <int NTL, bool SPLIT>
+template <int NTL, bool SPLIT, int CW>
 struct CoreLay {
+    VINF_ATTN_WARP_CONSTANTS(CW)
     static constexpr uint32_t RP = NTL * 8;
     static constexpr uint32_t SP = RP + 4;
     static constexpr uint32_t PL = SPLIT ? 2 : 1;
@@ -135,7 +147,7 @@ struct CoreLay {
     static constexpr uint32_t scratch = (kQBlock * SP * 4 + PL * PB + kConsumerWarps * OST + 127) / 128 * 128;
     // as many CTAs per SM (up to 4) as leave a ring of >= 4 stages each
     static constexpr int pick_ctas() {
-        for (int c = 4; c > 1; --c)
+        for (int c = CW == 8 ? 2 : 4; c > 1; --c)  // 8 consumer warps: registers allow 2
             if (c * (scratch + 4 * ST + 2048) <= 226u * 1024u) return c;
         return 1;
     }
@@ -170,10 +182,12 @@ struct Ring {
     }
 };
 
-template <int NTL, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
+template <int NTL, bool SPLIT, int CW>
+__global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     attention_core_kernel(const __grid_constant__ AttnMaps maps, const AttnArgs a) {
-    using LL = CoreLay<NTL, SPLIT>;
+    using LL = CoreLay<NTL, SPLIT, CW>;
+    constexpr int kConsumerWarps = LL::kConsumerWarps, kThreads = LL::kThreads, kWQ = LL::kWQ, kON = LL::kON;
+    constexpr uint32_t kOPitch = LL::kOPitch;
     constexpr uint32_t RP = LL::RP;
     constexpr int SP = int(LL::SP);
     const uint32_t NS = a.ns;
@@ -396,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, SPLIT>::ctas)
                 for (int w = 0; w < 2; ++w) {
                     const uint32_t rr = w ? (two ? r1 : r0) : r0;
                     const float* row = sp + rr * SP;
-                    const uint32_t wlh = wl[w ? (two ? i0 + 1 : i0) : i0];
+                    const uint32_t wlh = (w && two) ? wl[(i0 + 1) % kRows] : wl[i0];
                     const int lo = int(wlh & 0xFFu), hi = int(wlh >> 8);
 #pragma unroll
                     for (int k = 0; k < KC; ++k) {
@@ -606,12 +620,12 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
     return 0;
 }
 
-template <int NTL, bool SPLIT>
+template <int NTL, bool SPLIT, int CW>
 int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
-    using LL = CoreLay<NTL, SPLIT>;
+    using LL = CoreLay<NTL, SPLIT, CW>;
     static bool attr = false;
     if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, SPLIT>,
+        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, SPLIT, CW>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return int(e);
         attr = true;
@@ -631,15 +645,27 @@ int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     args.ns = uint32_t(LL::stages(ctas));
     const uint32_t slots = uint32_t(g_sms) * uint32_t(ctas);
     const uint32_t grid = args.items < slots ? args.items : slots;
-    return int(launch_pdl(attention_core_kernel<NTL, SPLIT>, dim3(grid), dim3(kThreads), LL::total(int(args.ns)), s,
-                          maps, args));
+    return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW>, dim3(grid), dim3(LL::kThreads),
+                          LL::total(int(args.ns)), s, maps, args));
+}
+
+// consumer warps per CTA: 4 (VINF_ATTN_WARPS=8 selects 8: measured no faster, at 2 CTAs per
+// SM, on the cfg2 and 288-frame shapes: profiles/r02_attn/warps_ctas.txt)
+template <int NTL, bool SPLIT>
+int launch_ntl(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
+    static const int env_w = [] {
+        const char* e = getenv("VINF_ATTN_WARPS");
+        return e ? atoi(e) : 0;
+    }();
+    const int cw = env_w == 8 ? 8 : 4;
+    return cw == 8 ? launch_core<NTL, SPLIT, 8>(maps, args, s) : launch_core<NTL, SPLIT, 4>(maps, args, s);
 }
 
 template <bool SPLIT>
 int launch_mode(uint32_t RP, const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
 #define CORE(NTL) \
     case NTL * 8: \
-        return launch_core<NTL, SPLIT>(maps, args, s)
+        return launch_ntl<NTL, SPLIT>(maps, args, s)
     switch (RP) {
         CORE(2); CORE(4); CORE(6); CORE(8); CORE(10); CORE(12);
         CORE(14); CORE(16); CORE(18); CORE(20); CORE(22); CORE(24);
@@ -663,6 +689,15 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     if (!attention_core_supported(C, heads, tt)) return int(cudaErrorInvalidValue);
     if (reinterpret_cast<uintptr_t>(qkv) % 16 || reinterpret_cast<uintptr_t>(qkv_lo) % 16)
         return int(cudaErrorInvalidValue);
+    // Which ring feeds the core (same arithmetic and token rules; measured on one B200,
+    // profiles/r02_attn/impl_ab.txt): the TMA ring for bf16 blocks of <= 32 distinct K/V frames
+    // (the 24-frame VideoCrafter2 clip: 72.7 vs 77.1 us), the cp.async ring of one position per
+    // CTA everywhere else (wide tiles of long clips: 581 vs 784 us at F = 288, C = 320; the
+    // split mode: 144 vs 154 us), where thread-issued copies of many CTAs keep more in flight.
+    const uint32_t RPw = (uint32_t(tt.max_kv) + 15) & ~15u;
+    const int impl = g_attn_impl ? g_attn_impl : (!qkv_lo && RPw <= 32 ? 1 : 2);
+    if (impl == 2)
+        return launch_attention_core_cpasync(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s);
     if (g_attn_pos_major == 2 && (C % kDC || (C / heads) % kDC)) return int(cudaErrorInvalidValue);
     // 66 tensor maps per buffer: encoded once per (buffer, shape, layout), then reused
     struct Cached {

@@ -2,7 +2,9 @@
 // single-worker engine layout's token table, and a streaming-read bandwidth probe.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <functional>
+#include <string>
 #include <vector>
 
 #include "host.hpp"
@@ -31,6 +33,14 @@ int vinf_bulk_bw_bench(uint64_t bytes, uint32_t chunk, uint32_t stages, uint32_t
         if (!ms || iters <= 0 || chunk % 16 || !stages) shape_error("bad arguments");
         cuda_check(bulk_bw_bench(bytes, chunk, stages, ctas, iters, ms), "bulk bandwidth probe");
     });
+}
+
+// Selects the attention core implementation for later launches (0 = by configuration,
+// 1 = TMA ring, 2 = cp.async ring); returns the previous setting.
+int vinf_debug_attention_impl(int impl) {
+    const int old = g_attn_impl;
+    if (impl >= 0 && impl <= 2) g_attn_impl = impl;
+    return old;
 }
 
 // The attention core alone over the Q/K/V buffer of a single-worker engine layout

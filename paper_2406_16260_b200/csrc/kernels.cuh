@@ -107,6 +107,13 @@ bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
 // ctx: [nq * HW, C] bf16.
 // Split (fp32) mode: qkv_lo / ctx_lo non-null are the lo planes (same layout) of the
 // bf16x3 operands; every product runs as hi*hi + hi*lo + lo*hi.
+// The same core as a cp.async ring over one position per CTA (attention_cpasync.cu).
+int launch_attention_core_cpasync(const void* qkv, const void* qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
+                                  uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias,
+                                  void* ctx, void* ctx_lo, cudaStream_t s);
+// Which implementation launch_attention_core uses: 0 = by configuration, 1 = the TMA ring,
+// 2 = the cp.async ring (VINF_ATTN_IMPL=tma|cpasync, vinf_debug_attention_impl).
+extern int g_attn_impl;
 // Diagnostics knob: 1 = the qkv buffer is position-major [HW][frames][3C].
 extern int g_attn_pos_major;
 // qkv_frames: frames of the qkv buffer (the TMA tensor maps' outer extent).
