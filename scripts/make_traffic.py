@@ -10,7 +10,7 @@ GROUPS = {
     "group_fold_kernel": "gn_fold",
     "group_apply_bf16_kernel": "gn_apply",
     ", 1, 0, 0, 1>": "qkv_gemm",
-    "attention_core_lean_kernel": "attn_core",
+    "attention_core_kernel": "attn_core",
     ", 1, 1, 0, 1>": "o_gemm",
     "stub_bf16_kernel": "stub",
 }

@@ -18,7 +18,8 @@ def full(rep):
     want = {"time_us": "gpu__time_duration.sum", "dram_read_MB": "dram__bytes_read.sum",
             "dram_write_MB": "dram__bytes_write.sum",
             "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-            "tensor_pipe_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+            "lts_hit_pct": "lts__t_sector_hit_rate.pct",
+            "issue_active_pct": "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
             "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
             "regs": "launch__registers_per_thread", "smem_KB": "launch__shared_mem_per_block_dynamic"}
