@@ -67,7 +67,8 @@ struct AttnMaps {
 
 struct AttnArgs {
     uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items, ns, frames, pos_major;
-    uint32_t load_only;  // diagnostics: consumers only wait for and release the stages
+    uint32_t load_only;  // diagnostics: consumers only wait for and release the stages (2: bulk feed)
+    const uint8_t* diag_src;
     float scale, bias;
     __nv_bfloat16* ctx;
     int64_t ctx_lo;  // elements from ctx to its lo plane (split mode)
@@ -275,6 +276,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                     uint64_t* bar = &full[r.slot];
                     dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    if (a.load_only == 2) {  // diagnostics: the same bytes as one contiguous bulk copy
+                        dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + ch) % 40000) * 8192u, kvb + nqh * 128u * LL::PL,
+                                      bar);
+                        continue;
+                    }
                     // the block's query rows exactly, one box
                     for (uint32_t pl = 0; pl < LL::PL; ++pl)
                         box4(st + pl * kQT, &maps.box[pl][nqh - 1], bar, 0, h, ch, uint32_t(qf));
@@ -286,6 +292,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                     uint64_t* bar = &full[r.slot];
                     dev::mbar_arrive_expect_tx(bar, kvb * n);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    if (a.load_only == 2) {
+                        dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + 16 + vs) % 40000) * 8192u, kvb * n, bar);
+                        continue;
+                    }
                     for (uint32_t i = 0; i < n; ++i) load_kv(st + i * LL::PL * LL::KT, bar, 2, h, vs * VPS + i);
                 }
             }
@@ -748,8 +758,9 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     args.items = HW * args.nqb;
     args.frames = qkv_frames;
     args.pos_major = uint32_t(g_attn_pos_major);
-    static const uint32_t load_only = getenv("VINF_ATTN_LOAD_ONLY") ? 1u : 0u;
+    static const uint32_t load_only = getenv("VINF_ATTN_LOAD_ONLY") ? uint32_t(atoi(getenv("VINF_ATTN_LOAD_ONLY"))) : 0u;
     args.load_only = load_only;
+    args.diag_src = static_cast<const uint8_t*>(qkv);  // load-only 2: reads within the first 320 MB
     args.scale = scale;
     args.bias = bias;
     args.ctx = static_cast<__nv_bfloat16*>(ctx);
