@@ -198,7 +198,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     constexpr int NA = NJ <= 2 ? 2 : 1;         // S accumulators per tile (shorter MMA chains)
     static_assert(NTL % 2 == 0 && RP <= uint32_t(kKvMax), "K/V rows padded to a multiple of 16");
     extern __shared__ uint8_t sm_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB aligned, offset from the __shared__ array itself so every access stays a shared-space
+    // access (a pointer rebuilt from an integer would make them generic loads / stores)
+    uint8_t* sm = sm_raw + ((1024u - (dev::smem_u32(sm_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = dev::smem_u32(sm);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + LL::bars(int(NS)));
@@ -274,8 +276,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                 for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {  // S phase: Q + K chunk
                     dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
                     uint64_t* bar = &full[r.slot];
-                    dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
+                    if (a.load_only != 3) dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    if (a.load_only == 3) {  // diagnostics: no loads at all (the consumers alone)
+                        dev::mbar_arrive(bar);
+                        continue;
+                    }
                     if (a.load_only == 2) {  // diagnostics: the same bytes as one contiguous bulk copy
                         dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + ch) % 40000) * 8192u, kvb + nqh * 128u * LL::PL,
                                       bar);
@@ -290,6 +296,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                     const uint32_t n = min(VPS, nch - vs * VPS);
                     dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
                     uint64_t* bar = &full[r.slot];
+                    if (a.load_only == 3) {
+                        dev::mbar_arrive(bar);
+                        continue;
+                    }
                     dev::mbar_arrive_expect_tx(bar, kvb * n);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (a.load_only == 2) {
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     const uint64_t ldc = a.C;
     uint8_t* ost = sm + LL::ost + warp * LL::OST;
     Ring r(NS);
-    if (a.load_only) {  // diagnostics: the producer's feed rate alone
+    if (a.load_only == 1 || a.load_only == 2) {  // diagnostics: the producer's feed rate alone
         for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x)
             for (uint32_t k = 0; k < heads * (nch + nvs); ++k, r.next()) {
                 dev::mbar_wait(&full[r.slot], r.phase);
