@@ -183,7 +183,9 @@ struct Ring {
     }
 };
 
-template <int NTL, bool SPLIT, int CW>
+// D > 0: the head dim fixed at compile time with heads == 1 (d == C; the chunk loops unroll and
+// every chunk is full when D % 64 == 0), D == 0: any configuration
+template <int NTL, bool SPLIT, int CW, int D>
 __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     attention_core_kernel(const __grid_constant__ AttnMaps maps, const AttnArgs a) {
     using LL = CoreLay<NTL, SPLIT, CW>;
@@ -223,7 +225,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     dev::pdl_wait();
     dev::pdl_trigger();
 
-    const uint32_t heads = a.heads, nch = a.nch, nvs = (nch + VPS - 1) / VPS;
+    constexpr bool kFixed = D > 0;
+    const uint32_t heads = kFixed ? 1u : a.heads, nch = kFixed ? uint32_t((D + kDC - 1) / kDC) : a.nch;
+    const uint32_t nvs = (nch + VPS - 1) / VPS;
+    const uint32_t dd = kFixed ? uint32_t(D) : a.d, CC = kFixed ? uint32_t(D) : a.C;
     if (warp == kConsumerWarps) {
         // ---------------- producer: one thread issues every TMA load ----------------
         if (lane != 0) return;
@@ -240,11 +245,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
             // 1 = position-major rows [HW][frames][3C], 2 = chunked [HW][3C/64][frames][64]
             // (the 64-channel chunk of a position's frames contiguous). box: `rows` frames from
             // f0 of 64-wide chunk ch of (which, head h); gathers: 2-D row of frame f.
-            const uint32_t nchk = 3 * a.C / kDC;
+            const uint32_t nchk = 3 * CC / kDC;
             auto box4 = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, uint32_t which, uint32_t h,
                             uint32_t ch, uint32_t f0) {
                 if (a.pos_major == 2)
-                    tma_load_4d(dst, map, bar, 0, int32_t(f0), int32_t((which * a.C + h * a.d) / kDC + ch), int32_t(p));
+                    tma_load_4d(dst, map, bar, 0, int32_t(f0), int32_t((which * CC + h * dd) / kDC + ch), int32_t(p));
                 else
                     tma_load_4d(dst, map, bar, int32_t(ch * kDC), int32_t(which * heads + h), int32_t(p), int32_t(f0));
             };
@@ -260,8 +265,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                     if (kind == uint32_t(kBoxGather4)) {
                         const uint32_t e1 = prog[b + 1], e2 = prog[b + 2];
                         b += 2;
-                        const uint32_t chunk = (which * a.C + h * a.d) / kDC + ch;
-                        const int32_t col = a.pos_major == 2 ? 0 : int32_t(which * a.C + h * a.d + ch * kDC);
+                        const uint32_t chunk = (which * CC + h * dd) / kDC + ch;
+                        const int32_t col = a.pos_major == 2 ? 0 : int32_t(which * CC + h * dd + ch * kDC);
                         for (uint32_t pl = 0; pl < LL::PL; ++pl)
                             dev::tma_gather4(dst + pl * LL::KT + row * 128u, &maps.g4[pl], bar, col,
                                              grow(chunk, e & 0xFFFFu), grow(chunk, e1 & 0xFFFFu),
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                ((((kq & 3) * 2 + hb) ^ r7) << 4);
     };
     const float bw = a.tt.wflag ? a.bias : 0.f, bg = a.tt.gflag ? a.bias : 0.f;
-    const uint64_t ldc = a.C;
+    const uint64_t ldc = CC;
     uint8_t* ost = sm + LL::ost + warp * LL::OST;
     Ring r(NS);
     if (a.load_only == 1 || a.load_only == 2) {  // diagnostics: the producer's feed rate alone
@@ -356,6 +361,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
         for (int k = 0; k < KC; ++k) ngc[k] = lane + 32 * k < int(R) ? gm[lane + 32 * k] : 0;
         // window column ranges of this warp's softmax rows warp + kConsumerWarps * i, read
         // once per item (their latency hides under the S phase)
+        // narrow tiles (quad softmax): this thread's row tid / 4 and its eight columns
+        int qlo = 0, qhi = -1, qng[8];
+        if constexpr (RP <= 32 && kConsumerWarps == 4) {
+            const uint32_t rr = uint32_t(tid) >> 2, quarter = uint32_t(lane) & 3u;
+            if (rr < nqh) {
+                qlo = a.tt.wlo[a0 + rr];
+                qhi = a.tt.whi[a0 + rr];
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t c = quarter * 8 + uint32_t(k);
+                qng[k] = c < R ? gm[c] : 0;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) qng[k] = 0;
+        }
         constexpr int kRows = kQBlock / kConsumerWarps;
         uint32_t wl[kRows];
 #pragma unroll
@@ -374,7 +396,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
             for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
                 dev::mbar_wait(&full[r.slot], r.phase);
                 const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
-                const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
+                const uint32_t vw = min(uint32_t(kDC), dd - ch * kDC);
 #pragma unroll
                 for (int kk = 0; kk < kDC / 16; ++kk) {
                     if (kk * 16 >= int(vw)) break;  // zero-filled past the head dim
@@ -417,6 +439,60 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
             // Column c of the block's K/V list carries query qa's window token iff
             // wlo <= c <= whi, and gmult[c] global tokens; p_c = [window] e^(l_w - m) +
             // gmult[c] e^(l_g - m), summed one token at a time. A warp owns whole rows.
+            if constexpr (RP <= 32 && kConsumerWarps == 4) {
+                // narrow tiles: all 32 rows in one pass, four threads per row (eight columns
+                // each, two quad shuffles per reduction), P written as one 16-byte piece per thread
+                const uint32_t rr = uint32_t(tid) >> 2, quarter = uint32_t(lane) & 3u;
+                if (rr < nqh) {
+                    const float* row = sp + rr * SP + quarter * 8;
+                    const bool have = quarter * 8 < RP;  // columns past RP were never stored
+                    const float4 s0 = have ? *reinterpret_cast<const float4*>(row) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float4 s1 = have ? *reinterpret_cast<const float4*>(row + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float sr[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                    float sv[8], m = -INFINITY;
+                    bool inw[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int c = int(quarter) * 8 + k;
+                        const bool ok = c < int(R);
+                        sv[k] = ok ? a.scale * sr[k] : 0.f;
+                        inw[k] = ok && c >= qlo && c <= qhi;
+                        if (inw[k]) m = fmaxf(m, sv[k] + bw);
+                        if (qng[k]) m = fmaxf(m, sv[k] + bg);
+                    }
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+                    float e[8], z = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        e[k] = inw[k] ? (SPLIT ? expf(sv[k] + bw - m) : __expf(sv[k] + bw - m)) : 0.f;
+                        if (qng[k]) e[k] += float(qng[k]) * (SPLIT ? expf(sv[k] + bg - m) : __expf(sv[k] + bg - m));
+                        z += e[k];
+                    }
+                    z += __shfl_xor_sync(0xffffffffu, z, 1);
+                    z += __shfl_xor_sync(0xffffffffu, z, 2);
+                    const float zi = 1.0f / z;
+                    uint32_t ph[4], pl[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (SPLIT)
+                            split2(e[2 * k] * zi, e[2 * k + 1] * zi, ph[k], pl[k]);
+                        else
+                            ph[k] = pack_bf16(e[2 * k] * zi, e[2 * k + 1] * zi);
+                    }
+                    *reinterpret_cast<uint4*>(sm + LL::pb + swz(rr, quarter)) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+                    if (SPLIT)
+                        *reinterpret_cast<uint4*>(sm + LL::pb + LL::PB + swz(rr, quarter)) =
+                            make_uint4(pl[0], pl[1], pl[2], pl[3]);
+                } else {
+                    // keep the quad's shuffles converged (rows past the block contribute nothing)
+                    float m = 0.f;
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+                    m += __shfl_xor_sync(0xffffffffu, m, 1);
+                    m += __shfl_xor_sync(0xffffffffu, m, 2);
+                }
+            } else
             // two rows per pass (independent shuffle chains); the block's global-token
             // multiplicities per column were read once per item (ngc)
 #pragma unroll
@@ -501,7 +577,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                 for (uint32_t i = 0; i < n; ++i) {
                     const uint32_t ch = vs * VPS + i;
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST + i * LL::PL * LL::KT;
-                    const uint32_t vw = min(uint32_t(kDC), a.d - ch * kDC);
+                    const uint32_t vw = min(uint32_t(kDC), dd - ch * kDC);
                     const uint32_t c0w = uint32_t(wq) * kON * 8;  // this warp's first column in the chunk
                     const bool live = c0w < vw;
                     float o[kON][4];
@@ -564,7 +640,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                             const uint32_t q = mt * 16 + rr, col = c0w + part * 8;
                             if (pc < uint32_t(kPieces) && q < nqh && col < vw) {
                                 __nv_bfloat16* dst =
-                                    a.ctx + (uint64_t(a0 + q) * a.HW + p) * ldc + h * a.d + ch * kDC + col;
+                                    a.ctx + (uint64_t(a0 + q) * a.HW + p) * ldc + h * dd + ch * kDC + col;
                                 *reinterpret_cast<uint4*>(dst) =
                                     *reinterpret_cast<const uint4*>(ost + rr * kOPitch + part * 16);
                                 if (SPLIT)
@@ -640,12 +716,12 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
     return 0;
 }
 
-template <int NTL, bool SPLIT, int CW>
+template <int NTL, bool SPLIT, int CW, int D>
 int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     using LL = CoreLay<NTL, SPLIT, CW>;
     static bool attr = false;
     if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, SPLIT, CW>,
+        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, SPLIT, CW, D>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return int(e);
         attr = true;
@@ -665,7 +741,7 @@ int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     args.ns = uint32_t(LL::stages(ctas));
     const uint32_t slots = uint32_t(g_sms) * uint32_t(ctas);
     const uint32_t grid = args.items < slots ? args.items : slots;
-    return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW>, dim3(grid), dim3(LL::kThreads),
+    return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW, D>, dim3(grid), dim3(LL::kThreads),
                           LL::total(int(args.ns)), s, maps, args));
 }
 
@@ -678,7 +754,19 @@ int launch_ntl(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
         return e ? atoi(e) : 0;
     }();
     const int cw = env_w == 8 ? 8 : 4;
-    return cw == 8 ? launch_core<NTL, SPLIT, 8>(maps, args, s) : launch_core<NTL, SPLIT, 4>(maps, args, s);
+    // one head with the head dim of a VideoCrafter2 level: compile-time chunk loops
+    if constexpr (NTL <= 4 && !SPLIT) {
+        if (args.heads == 1) switch (args.d) {
+                case 320: return cw == 8 ? launch_core<NTL, SPLIT, 8, 320>(maps, args, s)
+                                         : launch_core<NTL, SPLIT, 4, 320>(maps, args, s);
+                case 640: return cw == 8 ? launch_core<NTL, SPLIT, 8, 640>(maps, args, s)
+                                         : launch_core<NTL, SPLIT, 4, 640>(maps, args, s);
+                case 1280: return cw == 8 ? launch_core<NTL, SPLIT, 8, 1280>(maps, args, s)
+                                          : launch_core<NTL, SPLIT, 4, 1280>(maps, args, s);
+                default: break;
+            }
+    }
+    return cw == 8 ? launch_core<NTL, SPLIT, 8, 0>(maps, args, s) : launch_core<NTL, SPLIT, 4, 0>(maps, args, s);
 }
 
 template <bool SPLIT>
