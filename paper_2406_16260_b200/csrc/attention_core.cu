@@ -12,7 +12,9 @@
 //     over the [frames][HW][3 x heads][d] Q/K/V buffer, 128-byte swizzle, 64-wide head-dim
 //     chunks, zero-filled past the head dim) into one mbarrier FIFO ring per CTA: a block's
 //     query rows are one box, its K/V frames a host-built program of one box per run of
-//     consecutive frames (<= 32 rows) or one row gather per four isolated frames; four
+//     consecutive frames (<= 32 rows) or one row gather per four isolated frames (instances
+//     with a compile-time head dim add a copy warp that moves the query rows with cp.async
+//     instead: the TMA engine's per-row cost bounds the feed, the LSU path runs beside it); four
 //     consumer warps: S = Q K^T per head over the chunks, the reference's explicit token
 //     softmax (window tokens then globals, duplicates kept, +bias on the flagged side) in
 //     column form, ctx = P V chunk by chunk through per-warp staging to 16-byte stores;
@@ -68,6 +70,9 @@ struct AttnMaps {
 struct AttnArgs {
     uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items, ns, frames, pos_major;
     uint32_t load_only;  // diagnostics: consumers only wait for and release the stages (2: bulk feed)
+    uint32_t qfeed;      // D > 0 instances: 1 = Q rows by the copy warp (cp.async), 2 = + V chunks 1..
+    const __nv_bfloat16* q;     // the Q/K/V buffer (and its lo plane) for the copy warp
+    const __nv_bfloat16* q_lo;
     const uint8_t* diag_src;
     float scale, bias;
     __nv_bfloat16* ctx;
@@ -87,6 +92,16 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(dev::smem_u32(bar))
         : "memory");
+}
+
+// 16 bytes global -> shared through the LSU path, zero-filled when !valid
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+// arrives on the mbarrier once this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(dev::smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -185,11 +200,14 @@ struct Ring {
 
 // D > 0: the head dim fixed at compile time with heads == 1 (d == C; the chunk loops unroll and
 // every chunk is full when D % 64 == 0), D == 0: any configuration
+// D > 0 instances also carry a copy warp (warp CW + 1) that loads the Q rows with cp.async
+// (a.qfeed): the TMA engine's per-row cost bounds the feed, and the LSU path runs beside it.
 template <int NTL, bool SPLIT, int CW, int D>
-__global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
+__global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     attention_core_kernel(const __grid_constant__ AttnMaps maps, const AttnArgs a) {
     using LL = CoreLay<NTL, SPLIT, CW>;
-    constexpr int kConsumerWarps = LL::kConsumerWarps, kThreads = LL::kThreads, kWQ = LL::kWQ, kON = LL::kON;
+    constexpr int kConsumerWarps = LL::kConsumerWarps, kThreads = LL::kThreads + (D > 0 ? 32 : 0), kWQ = LL::kWQ,
+                  kON = LL::kON;
     constexpr uint32_t kOPitch = LL::kOPitch;
     constexpr uint32_t RP = LL::RP;
     constexpr int SP = int(LL::SP);
@@ -199,6 +217,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     constexpr int NJ = (NTL + kWQ - 1) / kWQ;  // S n8 tiles per warp
     constexpr int NA = NJ <= 2 ? 2 : 1;         // S accumulators per tile (shorter MMA chains)
     static_assert(NTL % 2 == 0 && RP <= uint32_t(kKvMax), "K/V rows padded to a multiple of 16");
+    static_assert(D == 0 || RP <= 32, "the copy warp holds at most 8 K/V rows per lane");
     extern __shared__ uint8_t sm_raw[];
     // 1 KB aligned, offset from the __shared__ array itself so every access stays a shared-space
     // access (a pointer rebuilt from an integer would make them generic loads / stores)
@@ -215,7 +234,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
         *reinterpret_cast<uint4*>(sm + i) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         for (uint32_t s = 0; s < NS; ++s) {
-            dev::mbar_init(&full[s], 1);
+            dev::mbar_init(&full[s], 1 + (D > 0 && a.qfeed ? 32 : 0));
             dev::mbar_init(&empty[s], kConsumerWarps);
         }
         dev::fence_barrier_init();
@@ -229,6 +248,86 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
     const uint32_t heads = kFixed ? 1u : a.heads, nch = kFixed ? uint32_t((D + kDC - 1) / kDC) : a.nch;
     const uint32_t nvs = (nch + VPS - 1) / VPS;
     const uint32_t dd = kFixed ? uint32_t(D) : a.d, CC = kFixed ? uint32_t(D) : a.C;
+    if (D > 0 && warp == kConsumerWarps + 1) {
+        // ------ copy warp: the Q rows of every S-phase stage, V chunks 1.. of every PV stage ------
+        // lane: 16-byte piece lane & 7 of rows lane >> 3, +4, ...; destination in the TMA
+        // 128B-swizzle order the consumers read; one arrival per lane per stage. The TMA
+        // producer keeps the K chunks and the first V chunk of a stage (half the rows each).
+        if (!a.qfeed) return;
+        Ring r(NS);
+        const uint32_t piece = uint32_t(lane) & 7u, r0 = uint32_t(lane) >> 3;
+        const uint64_t rowlen = a.pos_major == 2 ? uint64_t(kDC) : 3ull * CC;
+        for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+            const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
+            const uint32_t nqh = min(uint32_t(kQBlock), a.nq - qb * kQBlock);
+            const uint32_t qf = a.q_frame0 + qb * kQBlock;
+            // this lane's K/V frames (rows r0, r0 + 4, ... < R <= 32), read once per item
+            const uint32_t R = a.tt.kv_count[qb];
+            uint32_t vfr[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t row = r0 + 4u * uint32_t(k);
+                vfr[k] = a.qfeed >= 2 && row < R ? a.tt.kv_frames[size_t(qb) * kKvMax + row] : 0u;
+            }
+            for (uint32_t h = 0; h < heads; ++h) {
+                for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
+                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
+                    uint64_t* bar = &full[r.slot];
+                    if (a.load_only >= 2) {
+                        dev::mbar_arrive(bar);
+                        continue;
+                    }
+                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    const uint32_t col = ch * kDC + piece * 8;
+                    const bool valid = col < dd;
+                    const uint32_t chunk = (h * dd) / kDC + ch;
+                    for (uint32_t row = r0; row < nqh; row += 4) {
+                        const uint32_t f = qf + row;
+                        const uint64_t grow = a.pos_major == 2 ? (uint64_t(p) * (3 * CC / kDC) + chunk) * a.frames + f
+                                              : a.pos_major   ? uint64_t(p) * a.frames + f
+                                                              : uint64_t(f) * a.HW + p;
+                        const uint64_t off = grow * rowlen + (a.pos_major == 2 ? piece * 8 : h * dd + (valid ? col : 0));
+                        const uint32_t dst = st + swz(row, piece);
+                        cp_async16(dst, a.q + off, valid);
+                        if (SPLIT) cp_async16(dst + kQT, a.q_lo + off, valid);
+                    }
+                    cp_async_arrive(bar);
+                }
+                for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
+                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
+                    uint64_t* bar = &full[r.slot];
+                    if (a.load_only >= 2) {
+                        dev::mbar_arrive(bar);
+                        continue;
+                    }
+                    const uint32_t n = min(VPS, nch - vs * VPS);
+                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    for (uint32_t i = 1; i < (a.qfeed >= 2 ? n : 1u); ++i) {
+                        const uint32_t ch = vs * VPS + i;
+                        const uint32_t col = ch * kDC + piece * 8;
+                        const bool valid = col < dd;
+                        const uint32_t chunk = (2 * CC + h * dd) / kDC + ch;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t row = r0 + 4u * uint32_t(k);
+                            if (row >= R) break;
+                            const uint32_t f = vfr[k];
+                            const uint64_t grow = a.pos_major == 2 ? (uint64_t(p) * (3 * CC / kDC) + chunk) * a.frames + f
+                                                  : a.pos_major   ? uint64_t(p) * a.frames + f
+                                                                  : uint64_t(f) * a.HW + p;
+                            const uint64_t off =
+                                grow * rowlen + (a.pos_major == 2 ? piece * 8 : 2 * CC + h * dd + (valid ? col : 0));
+                            const uint32_t dst = st + i * LL::PL * LL::KT + swz(row, piece);
+                            cp_async16(dst, a.q + off, valid);
+                            if (SPLIT) cp_async16(dst + LL::KT, a.q_lo + off, valid);
+                        }
+                    }
+                    cp_async_arrive(bar);
+                }
+            }
+        }
+        return;
+    }
     if (warp == kConsumerWarps) {
         // ---------------- producer: one thread issues every TMA load ----------------
         if (lane != 0) return;
@@ -281,7 +380,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                 for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {  // S phase: Q + K chunk
                     dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
                     uint64_t* bar = &full[r.slot];
-                    if (a.load_only != 3) dev::mbar_arrive_expect_tx(bar, kvb + nqh * 128u * LL::PL);
+                    const bool qtma = !(D > 0 && a.qfeed) || a.load_only == 2;  // Q rows by TMA here
+                    if (a.load_only != 3) dev::mbar_arrive_expect_tx(bar, kvb + (qtma ? nqh * 128u * LL::PL : 0u));
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (a.load_only == 3) {  // diagnostics: no loads at all (the consumers alone)
                         dev::mbar_arrive(bar);
@@ -292,9 +392,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                                       bar);
                         continue;
                     }
-                    // the block's query rows exactly, one box
-                    for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                        box4(st + pl * kQT, &maps.box[pl][nqh - 1], bar, 0, h, ch, uint32_t(qf));
+                    // the block's query rows exactly, one box (unless the copy warp loads them)
+                    if (qtma)
+                        for (uint32_t pl = 0; pl < LL::PL; ++pl)
+                            box4(st + pl * kQT, &maps.box[pl][nqh - 1], bar, 0, h, ch, uint32_t(qf));
                     load_kv(st + LL::PL * kQT, bar, 1, h, ch);
                 }
                 for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {  // PV phase: VPS V chunks
@@ -305,13 +406,14 @@ __global__ void __launch_bounds__((CW + 1) * 32, CoreLay<NTL, SPLIT, CW>::ctas)
                         dev::mbar_arrive(bar);
                         continue;
                     }
-                    dev::mbar_arrive_expect_tx(bar, kvb * n);
+                    const uint32_t nt = (D > 0 && a.qfeed >= 2 && a.load_only != 2) ? 1u : n;  // chunks by TMA
+                    dev::mbar_arrive_expect_tx(bar, kvb * nt);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (a.load_only == 2) {
                         dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + 16 + vs) % 40000) * 8192u, kvb * n, bar);
                         continue;
                     }
-                    for (uint32_t i = 0; i < n; ++i) load_kv(st + i * LL::PL * LL::KT, bar, 2, h, vs * VPS + i);
+                    for (uint32_t i = 0; i < nt; ++i) load_kv(st + i * LL::PL * LL::KT, bar, 2, h, vs * VPS + i);
                 }
             }
         }
@@ -741,7 +843,12 @@ int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     args.ns = uint32_t(LL::stages(ctas));
     const uint32_t slots = uint32_t(g_sms) * uint32_t(ctas);
     const uint32_t grid = args.items < slots ? args.items : slots;
-    return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW, D>, dim3(grid), dim3(LL::kThreads),
+    static const uint32_t qfeed = [] {
+        const char* e = getenv("VINF_ATTN_QFEED");
+        return e ? uint32_t(atoi(e)) : 1u;  // 0 = all by TMA, 1 = Q rows, 2 = Q rows + V chunks 1..
+    }();
+    args.qfeed = D > 0 ? qfeed : 0u;
+    return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW, D>, dim3(grid), dim3(LL::kThreads + (D > 0 ? 32 : 0)),
                           LL::total(int(args.ns)), s, maps, args));
 }
 
@@ -859,6 +966,8 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     static const uint32_t load_only = getenv("VINF_ATTN_LOAD_ONLY") ? uint32_t(atoi(getenv("VINF_ATTN_LOAD_ONLY"))) : 0u;
     args.load_only = load_only;
     args.diag_src = static_cast<const uint8_t*>(qkv);  // load-only 2: reads within the first 320 MB
+    args.q = static_cast<const __nv_bfloat16*>(qkv);
+    args.q_lo = static_cast<const __nv_bfloat16*>(qkv_lo);
     args.scale = scale;
     args.bias = bias;
     args.ctx = static_cast<__nv_bfloat16*>(ctx);
