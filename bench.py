@@ -94,7 +94,8 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
-def kernel_floor_us(frames: int, h: int, w: int, c: int, es: int, hbm_gbs: float, tf: float) -> dict:
+def kernel_floor_us(frames: int, h: int, w: int, c: int, es: int, hbm_gbs: float, tf: float,
+                    fused_o: bool = False) -> dict:
     """Roofline floor of one block step, kernel by kernel (bf16 GroupNorm-folded pipeline):
     each kernel takes at least max(its tensor work / peak, its algorithmic HBM bytes / peak),
     with T = frames*H*W*C*s the bytes of one clip-sized tensor:
@@ -103,12 +104,18 @@ def kernel_floor_us(frames: int, h: int, w: int, c: int, es: int, hbm_gbs: float
       QKV   2*H*W*3C^2 flop per frame; in, Q/K/V out   4 T
       attn  Q/K/V in, ctx out                          4 T              (HBM)
       O     2*H*W*C^2 flop per frame; ctx, residual, out 3 T
-    GroupNorm statistics and folding are not counted (latency-bound, a few us per step)."""
+    GroupNorm statistics and folding are not counted (latency-bound, a few us per step).
+    fused_o (one head): no O GEMM; the attention core reads Q/K/V and the residual and writes
+    the block output (5 T); W_vo = W_o W_v is 2 C^3 flop."""
     t = frames * h * w * c * es
     m = frames * h * w
     parts = {"stub": (0.0, 2 * t), "conv_gemm": (6.0 * m * c * c, 3 * t),
              "qkv_gemm": (6.0 * m * c * c, 4 * t), "attn_core": (0.0, 4 * t),
              "o_gemm": (2.0 * m * c * c, 3 * t)}
+    if fused_o:
+        del parts["o_gemm"]
+        parts["attn_core"] = (0.0, 5 * t)
+        parts["wvo_gemm"] = (2.0 * c * c * c, 0.0)
     out = {}
     for k, (fl, by) in parts.items():
         out[k] = max(fl / (tf * 1e12), by / (hbm_gbs * 1e9)) * 1e6
@@ -288,11 +295,15 @@ class ClockSampler:
 
 # ---- our arm --------------------------------------------------------------------
 
-def kernel_work(f_clip: int, dtype_bytes: int, split: bool = False, h: int = H, w: int = W, c: int = C):
+def kernel_work(f_clip: int, dtype_bytes: int, split: bool = False, h: int = H, w: int = W, c: int = C,
+                fused_o: bool = False):
     """Algorithmic work per launch for each kernel group: GEMM flops 2*M*N*K
     (x3 in the fp32 mode: every product runs as bf16 hi*hi + hi*lo + lo*hi on the tensor
     pipe, so that is the tensor work against the bf16 peak); bandwidth kernels their
-    compulsory bytes (fp32 mode: Q/K/V and ctx as two bf16 planes = 4 B per element)."""
+    compulsory bytes (fp32 mode: Q/K/V and ctx as two bf16 planes = 4 B per element).
+    fused_o (one head, engine.cpp fuse_o): the O projection is absorbed into V (W_vo = W_o W_v,
+    a C^3 GEMM per step) and the attention core reads the residual and writes the block
+    output instead of ctx (Q/K/V + residual in, y out)."""
     hw = h * w
     M = f_clip * hw
     E = hw * c
@@ -308,6 +319,18 @@ def kernel_work(f_clip: int, dtype_bytes: int, split: bool = False, h: int = H, 
         "gn_apply": (f_clip * E * (s + 2 * s), "hbm") if split else (f_clip * E * (s + s), "hbm"),
         "gn_fold": (3 * c * c * (2 + 2) + 3 * c * 4, "hbm"),  # W read, W' + b' written
         "attn_core": (f_clip * E * s * 4, "hbm"),  # Q, K, V once + ctx write
+        "wvo_gemm": (k * 2.0 * c * c * c, "tensor"),
+    } if not fused_o else {
+        "conv_gemm": (k * 2.0 * M * c * TAPS * c, "tensor"),
+        "qkv_gemm": (k * 2.0 * M * 3 * c * c, "tensor"),
+        "wvo_gemm": (k * 2.0 * c * c * c, "tensor"),
+        "kv_gemm_ctx": (None, "tensor"),
+        "stub": (f_clip * E * (s + (2 * s if split else s)), "hbm"),
+        "gn_stats": (((M + 31) // 32) * 2 * c * 4, "hbm"),
+        "gn_apply": (f_clip * E * (s + 2 * s), "hbm") if split else (f_clip * E * (s + s), "hbm"),
+        "gn_fold": (3 * c * c * (2 + 2) + 3 * c * 4, "hbm"),
+        # Q, K, V once + residual (bf16 raw u; fp32 GN output) + y (bf16; fp32)
+        "attn_core": (f_clip * E * (s * 3 + (4 if split else s) * 2), "hbm"),
     }
 
 
@@ -517,7 +540,8 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (peaks chosen by the clocks of the region) ------
     hbm, tf_burst, tf_sus, src = peaks()
     tf, which, both = tensor_peak(clocks)
-    work = kernel_work(fc, es, split=dtype == torch.float32)
+    fused_o = "o_gemm" not in stats  # engine.cpp fuse_o: the O projection absorbed into V
+    work = kernel_work(fc, es, split=dtype == torch.float32, fused_o=fused_o)
     per_kernel = roofline_of(work, stats, tf, hbm, args.steps)
     dom = max(stats, key=lambda k: stats[k][0]) if stats else None
     roof = None
@@ -541,9 +565,13 @@ def run_ours(args):
                 roof["traffic_source"] = tr["source"]
         except (OSError, ValueError):
             pass
-    flops_step = sum(work[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm"))
-    floor = kernel_floor_us(fc, H, W, C, es, hbm, tf)
-    block_roof = {"flops_per_step": flops_step,
+    # tensor work executed per step (fused: W_vo in place of the O GEMM); the reference's own
+    # count (conv + Q/K/V + O projections) beside it
+    flops_step = sum(work[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm", "wvo_gemm") if k in work)
+    ref_flops = sum(kernel_work(fc, es)[k][0] for k in ("conv_gemm", "qkv_gemm", "o_gemm"))
+    floor = kernel_floor_us(fc, H, W, C, es, hbm, tf, fused_o=fused_o)
+    block_roof = {"flops_per_step": flops_step, "reference_flops_per_step": ref_flops,
+                  "o_projection": "absorbed into V (W_vo = W_o W_v each step)" if fused_o else "GEMM",
                   "achieved_tflops": flops_step / (ms_per_step / 1000.0) / 1e12,
                   "frac_of_tensor_peak": flops_step / (ms_per_step / 1000.0) / 1e12 / tf,
                   "tensor_peak": {"value": tf, "which": which, **both},
@@ -568,7 +596,7 @@ def run_ours(args):
         ms32, clk32 = timer.run(step32, k32)
         st32, _ = _profile(e32, step32, k32, timer)
         tf32, which32, _ = tensor_peak(clk32)
-        w32 = kernel_work(fc, 4, split=True)
+        w32 = kernel_work(fc, 4, split=True, fused_o="o_gemm" not in st32)
         pk32 = roofline_of(w32, st32, tf32, hbm, k32)
         f32_rec = {"value": n * fc * k32 / (ms32 / 1000.0), "unit": "frames/s",
                    "ms_per_step": ms32 / k32, "steps": k32,
@@ -677,8 +705,12 @@ def measure_vc2(en, ops, n, rank, dtype, dev, group, timer, frames, steps, warmu
     es = 2 if dtype == torch.bfloat16 else 4
     k = 1.0 if dtype == torch.bfloat16 else 3.0
     fcs = [e.layout.f_clip for e in engines]
-    flops = [k * 14.0 * fc * h * w * c * c for fc, (c, h, w) in zip(fcs, VC2_LEVELS)]
-    floors = [sum(kernel_floor_us(fc, h, w, c, es, hbm, tf).values()) for fc, (c, h, w) in zip(fcs, VC2_LEVELS)]
+    # the engine absorbs the O projection into V for one head (engine.cpp fuse_o)
+    fused = HEADS == 1 and os.environ.get("VINF_NO_FUSE_O", "0") in ("", "0")
+    flops = [k * ((12.0 * fc * h * w * c * c + 2.0 * c ** 3) if fused else 14.0 * fc * h * w * c * c)
+             for fc, (c, h, w) in zip(fcs, VC2_LEVELS)]
+    floors = [sum(kernel_floor_us(fc, h, w, c, es, hbm, tf, fused_o=fused).values())
+              for fc, (c, h, w) in zip(fcs, VC2_LEVELS)]
     levels = [{"channels": c, "height": h, "width": w, "frames_per_gpu": fc, "ms": m,
                "achieved_tflops": fl / (m / 1000.0) / 1e12, "frac_of_tensor_peak": fl / (m / 1000.0) / 1e12 / tf,
                "kernel_floor_ms": fu / 1000.0, "frac_of_kernel_floor": fu / 1000.0 / m}

@@ -77,6 +77,8 @@ struct AttnArgs {
     float scale, bias;
     __nv_bfloat16* ctx;
     int64_t ctx_lo;  // elements from ctx to its lo plane (split mode)
+    FuseO fo;        // fo.y: the block output (O projection absorbed into V) instead of ctx
+    uint32_t fo_tab;  // fused output with GroupNorm folding: s, t copied to shared memory (2C floats)
     TokenTable tt;
 };
 
@@ -178,9 +180,9 @@ struct CoreLay {
     static constexpr uint32_t bars(int ns) { return ring + uint32_t(ns) * ST; }
     static constexpr uint32_t total(int ns) { return bars(ns) + 2u * uint32_t(ns) * 8u + 1024u; }
     // the deepest ring (<= 16 stages) that lets `c` CTAs share an SM
-    static constexpr int stages(int c) {
+    static constexpr int stages(int c, uint32_t extra = 0) {
         int ns = 16;
-        while (ns > 2 && uint32_t(c) * total(ns) > 227u * 1024u) --ns;
+        while (ns > 2 && uint32_t(c) * (total(ns) + extra) > 227u * 1024u) --ns;
         return ns;
     }
     static_assert(total(2) <= 227 * 1024, "attention core shared memory");
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     constexpr uint32_t RP = LL::RP;
     constexpr int SP = int(LL::SP);
     const uint32_t NS = a.ns;
-    constexpr uint32_t VPS = LL::VPS;
+    constexpr uint32_t kVPS = LL::VPS;
     constexpr int KC = (int(RP) + 31) / 32;     // softmax columns per lane
     constexpr int NJ = (NTL + kWQ - 1) / kWQ;  // S n8 tiles per warp
     constexpr int NA = NJ <= 2 ? 2 : 1;         // S accumulators per tile (shorter MMA chains)
@@ -243,9 +245,23 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     __syncthreads();
     dev::pdl_wait();
     dev::pdl_trigger();
+    // fused output: the residual's per-channel scale and shift, after the ring's barriers
+    float* stab = reinterpret_cast<float*>(sm + LL::bars(int(NS)) + 2 * NS * 8);
+    if (a.fo_tab) {
+        for (uint32_t i = tid; i < a.C; i += kThreads) {
+            stab[i] = a.fo.s[i];
+            stab[a.C + i] = a.fo.t[i];
+        }
+        __syncthreads();
+    }
 
     constexpr bool kFixed = D > 0;
     const uint32_t heads = kFixed ? 1u : a.heads, nch = kFixed ? uint32_t((D + kDC - 1) / kDC) : a.nch;
+    // fused output through the ring (copy-warp instances): each PV stage carries one V chunk
+    // (K slot) and the matching residual chunk of the block's queries (Q slot), the residual
+    // loaded by the copy warp; the consumers add it from shared memory
+    const bool fr = D > 0 && !SPLIT && a.qfeed == 1 && a.fo.y != nullptr && a.fo.res_bf16 && a.load_only != 2;
+    const uint32_t VPS = fr ? 1u : kVPS;
     const uint32_t nvs = (nch + VPS - 1) / VPS;
     const uint32_t dd = kFixed ? uint32_t(D) : a.d, CC = kFixed ? uint32_t(D) : a.C;
     if (D > 0 && warp == kConsumerWarps + 1) {
@@ -302,6 +318,15 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     }
                     const uint32_t n = min(VPS, nch - vs * VPS);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    if (fr) {  // residual chunk vs (bf16) of the block's query rows -> the Q slot
+                        const uint32_t a0 = qb * kQBlock;
+                        const bool valid = vs * kDC + piece * 8 < dd;
+                        for (uint32_t row = r0; row < nqh; row += 4)
+                            cp_async16(st + swz(row, piece),
+                                       static_cast<const __nv_bfloat16*>(a.fo.res) +
+                                           (uint64_t(a0 + row) * a.HW + p) * CC + (valid ? vs * kDC + piece * 8 : 0),
+                                       valid);
+                    }
                     for (uint32_t i = 1; i < (a.qfeed >= 2 ? n : 1u); ++i) {
                         const uint32_t ch = vs * VPS + i;
                         const uint32_t col = ch * kDC + piece * 8;
@@ -392,6 +417,15 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                                       bar);
                         continue;
                     }
+                    if (a.fo.y && !fr && h == 0 && ch == 0) {  // fused output: the item's residual rows into L2
+                        const uint32_t rb = CC * (a.fo.res_bf16 ? 2u : 4u);
+                        const uint8_t* res = static_cast<const uint8_t*>(a.fo.res);
+                        for (uint32_t q = 0; q < nqh; ++q)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                             res + (uint64_t(qb * kQBlock + q) * a.HW + p) * rb),
+                                         "r"(rb)
+                                         : "memory");
+                    }
                     // the block's query rows exactly, one box (unless the copy warp loads them)
                     if (qtma)
                         for (uint32_t pl = 0; pl < LL::PL; ++pl)
@@ -409,6 +443,10 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     const uint32_t nt = (D > 0 && a.qfeed >= 2 && a.load_only != 2) ? 1u : n;  // chunks by TMA
                     dev::mbar_arrive_expect_tx(bar, kvb * nt);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
+                    if (fr) {  // the V chunk into the K slot (the copy warp fills the Q slot)
+                        load_kv(st + LL::PL * kQT, bar, 2, h, vs);
+                        continue;
+                    }
                     if (a.load_only == 2) {
                         dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + 16 + vs) % 40000) * 8192u, kvb * n, bar);
                         continue;
@@ -673,12 +711,32 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     if (SPLIT) ldsm_x4(p_addr(kq) + LL::PB, pal[LL::PREG && SPLIT ? kq : 0]);
                 }
             }
+            constexpr int kPc = (16 * kON + 31) / 32;  // output pieces per lane per chunk
             for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
                 dev::mbar_wait(&full[r.slot], r.phase);
                 const uint32_t n = min(VPS, nch - vs * VPS);
-                for (uint32_t i = 0; i < n; ++i) {
+                // fused output, bf16 residual: this stage's residual pieces requested up front, so
+                // their latency (L2: the producer prefetched the item's rows) hides under the PV math
+                uint4 rpre[SPLIT ? 1 : kVPS][kPc];
+                if (!SPLIT && a.fo.y && a.fo.res_bf16 && !fr) {
+#pragma unroll
+                    for (int i = 0; i < int(kVPS); ++i)
+#pragma unroll
+                        for (int i2 = 0; i2 < kPc; ++i2) {
+                            const uint32_t pc = lane + 32 * i2, ch = vs * VPS + uint32_t(i);
+                            const uint32_t q = mt * 16 + pc / kON, col = uint32_t(wq) * kON * 8 + (pc % kON) * 8;
+                            if (uint32_t(i) < n && pc < uint32_t(16 * kON) && q < nqh && ch * kDC + col < dd)
+                                rpre[SPLIT ? 0 : i][i2] = __ldg(reinterpret_cast<const uint4*>(
+                                    static_cast<const __nv_bfloat16*>(a.fo.res) +
+                                    (uint64_t(a0 + q) * a.HW + p) * ldc + ch * kDC + col));
+                        }
+                }
+#pragma unroll
+                for (uint32_t i = 0; i < kVPS; ++i) {
+                    if (i >= n) break;
                     const uint32_t ch = vs * VPS + i;
-                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST + i * LL::PL * LL::KT;
+                    const uint32_t slot = LL::ring + r.slot * LL::ST;  // fr: the residual chunk at its start
+                    const uint32_t st = sbase + slot + (fr ? LL::PL * kQT : i * LL::PL * LL::KT);
                     const uint32_t vw = min(uint32_t(kDC), dd - ch * kDC);
                     const uint32_t c0w = uint32_t(wq) * kON * 8;  // this warp's first column in the chunk
                     const bool live = c0w < vw;
@@ -741,13 +799,49 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                             const uint32_t rr = pc / kON, part = pc % kON;
                             const uint32_t q = mt * 16 + rr, col = c0w + part * 8;
                             if (pc < uint32_t(kPieces) && q < nqh && col < vw) {
-                                __nv_bfloat16* dst =
-                                    a.ctx + (uint64_t(a0 + q) * a.HW + p) * ldc + h * dd + ch * kDC + col;
-                                *reinterpret_cast<uint4*>(dst) =
-                                    *reinterpret_cast<const uint4*>(ost + rr * kOPitch + part * 16);
-                                if (SPLIT)
-                                    *reinterpret_cast<uint4*>(dst + a.ctx_lo) =
-                                        *reinterpret_cast<const uint4*>(ost + 16 * kOPitch + rr * kOPitch + part * 16);
+                                const uint64_t o = (uint64_t(a0 + q) * a.HW + p) * ldc + h * dd + ch * kDC + col;
+                                const uint4 hv = *reinterpret_cast<const uint4*>(ost + rr * kOPitch + part * 16);
+                                if (a.fo.y) {  // y = ctx' + residual (one head: ldc = d)
+                                    float v[8];
+                                    unpack8(hv, v);
+                                    if (SPLIT) {
+                                        unpack8_add(*reinterpret_cast<const uint4*>(ost + 16 * kOPitch + rr * kOPitch +
+                                                                                     part * 16),
+                                                    v);
+                                        fuse_o_store(a.fo, o, ch * kDC + col, v);
+                                    } else if (fr) {  // the residual piece from the stage's Q slot
+                                        const uint4 u = *reinterpret_cast<const uint4*>(sm + slot + swz(q, col >> 3));
+                                        if (a.fo_tab) {
+                                            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                                            const float* sc = stab + ch * kDC + col;
+                                            const float4 s0 = *reinterpret_cast<const float4*>(sc);
+                                            const float4 s1 = *reinterpret_cast<const float4*>(sc + 4);
+                                            const float4 t0 = *reinterpret_cast<const float4*>(sc + CC);
+                                            const float4 t1 = *reinterpret_cast<const float4*>(sc + CC + 4);
+                                            const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                                            const float tt8[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+                                            for (int k = 0; k < 4; ++k) {
+                                                const float2 x = __bfloat1622float2(u2[k]);
+                                                v[2 * k] += x.x * ss[2 * k] + tt8[2 * k];
+                                                v[2 * k + 1] += x.y * ss[2 * k + 1] + tt8[2 * k + 1];
+                                            }
+                                        } else {
+                                            fuse_o_add_bf16(a.fo, u, ch * kDC + col, v);
+                                        }
+                                        fuse_o_write(a.fo, o, v);
+                                    } else if (a.fo.res_bf16) {
+                                        fuse_o_add_bf16(a.fo, rpre[SPLIT ? 0 : i][i2], ch * kDC + col, v);
+                                        fuse_o_write(a.fo, o, v);
+                                    } else {
+                                        fuse_o_store(a.fo, o, ch * kDC + col, v);
+                                    }
+                                } else {
+                                    *reinterpret_cast<uint4*>(a.ctx + o) = hv;
+                                    if (SPLIT)
+                                        *reinterpret_cast<uint4*>(a.ctx + o + a.ctx_lo) = *reinterpret_cast<const uint4*>(
+                                            ost + 16 * kOPitch + rr * kOPitch + part * 16);
+                                }
                             }
                         }
                         __syncwarp();  // staging is rewritten by the next chunk
@@ -840,7 +934,10 @@ int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
         return e ? atoi(e) : 0;
     }();
     const int ctas = env_ctas >= 1 && env_ctas <= 4 ? env_ctas : LL::ctas;
-    args.ns = uint32_t(LL::stages(ctas));
+    // fused output with GroupNorm folding (copy-warp instances): s, t in shared memory
+    args.fo_tab = D > 0 && args.fo.y && args.fo.s ? 1u : 0u;
+    const uint32_t tab = args.fo_tab ? (2 * args.C * 4 + 127) / 128 * 128 : 0u;
+    args.ns = uint32_t(LL::stages(ctas, tab));
     const uint32_t slots = uint32_t(g_sms) * uint32_t(ctas);
     const uint32_t grid = args.items < slots ? args.items : slots;
     static const uint32_t qfeed = [] {
@@ -849,7 +946,7 @@ int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     }();
     args.qfeed = D > 0 ? qfeed : 0u;
     return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW, D>, dim3(grid), dim3(LL::kThreads + (D > 0 ? 32 : 0)),
-                          LL::total(int(args.ns)), s, maps, args));
+                          LL::total(int(args.ns)) + tab, s, maps, args));
 }
 
 // consumer warps per CTA: 4 (VINF_ATTN_WARPS=8 selects 8: measured no faster, at 2 CTAs per
@@ -898,8 +995,10 @@ bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt) 
 
 int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_frames, uint32_t HW, uint32_t C,
                           uint32_t heads, uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale,
-                          float bias, void* ctx, void* ctx_lo, cudaStream_t s) {
+                          float bias, void* ctx, void* ctx_lo, cudaStream_t s, const FuseO* fo) {
     if (HW == 0 || !qkv || !ctx || (qkv_lo == nullptr) != (ctx_lo == nullptr)) return int(cudaErrorInvalidValue);
+    if (fo && fo->y && (heads != 1 || !fo->res || (fo->s == nullptr) != (fo->t == nullptr)))
+        return int(cudaErrorInvalidValue);
     if (nq == 0) return 0;
     if (!attention_core_supported(C, heads, tt)) return int(cudaErrorInvalidValue);
     if (reinterpret_cast<uintptr_t>(qkv) % 16 || reinterpret_cast<uintptr_t>(qkv_lo) % 16)
@@ -912,7 +1011,8 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     const uint32_t RPw = (uint32_t(tt.max_kv) + 15) & ~15u;
     const int impl = g_attn_impl ? g_attn_impl : (!qkv_lo && RPw <= 32 ? 1 : 2);
     if (impl == 2)
-        return launch_attention_core_cpasync(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s);
+        return launch_attention_core_cpasync(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s,
+                                             fo);
     if (g_attn_pos_major == 2 && (C % kDC || (C / heads) % kDC)) return int(cudaErrorInvalidValue);
     // 66 tensor maps per buffer: encoded once per (buffer, shape, layout), then reused
     struct Cached {
@@ -973,6 +1073,7 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     args.ctx = static_cast<__nv_bfloat16*>(ctx);
     args.ctx_lo = ctx_lo ? static_cast<__nv_bfloat16*>(ctx_lo) - static_cast<__nv_bfloat16*>(ctx) : 0;
     args.tt = tt;
+    if (fo) args.fo = *fo;
     const uint32_t RP = (uint32_t(tt.max_kv) + 15) & ~15u;
     return qkv_lo ? launch_mode<true>(RP, maps, args, s) : launch_mode<false>(RP, maps, args, s);
 }

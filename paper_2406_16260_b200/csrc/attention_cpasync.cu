@@ -117,7 +117,7 @@ template <int NTL, int NS, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
     attention_core_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_lo, uint32_t HW, uint32_t C,
                           uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale,
-                          float bias, __nv_bfloat16* __restrict__ ctx, int64_t ctx_lo) {
+                          float bias, __nv_bfloat16* __restrict__ ctx, int64_t ctx_lo, const FuseO fo) {
     dev::pdl_wait();
     dev::pdl_trigger();
     using LL = CoreLay<NTL, NS, SPLIT>;
@@ -217,10 +217,18 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
             if (c * 8 < vw) {
                 const uint8_t* ost = sm + LL::ost + buf * (LL::PL * LL::QT);
                 const uint64_t o = (uint64_t(a0 + r) * HW + p) * C + c0 + c * 8;
-                *reinterpret_cast<uint4*>(ctx + o) = *reinterpret_cast<const uint4*>(ost + swz(r, c));
-                if (SPLIT)
-                    *reinterpret_cast<uint4*>(ctx + ctx_lo + o) =
-                        *reinterpret_cast<const uint4*>(ost + LL::QT + swz(r, c));
+                const uint4 hv = *reinterpret_cast<const uint4*>(ost + swz(r, c));
+                if (fo.y) {  // y = ctx' + residual (one head)
+                    float v[8];
+                    unpack8(hv, v);
+                    if (SPLIT) unpack8_add(*reinterpret_cast<const uint4*>(ost + LL::QT + swz(r, c)), v);
+                    fuse_o_store(fo, o, c0 + c * 8, v);
+                } else {
+                    *reinterpret_cast<uint4*>(ctx + o) = hv;
+                    if (SPLIT)
+                        *reinterpret_cast<uint4*>(ctx + ctx_lo + o) =
+                            *reinterpret_cast<const uint4*>(ost + LL::QT + swz(r, c));
+                }
             }
         }
     };
@@ -425,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
 template <int NTL, int NS, bool SPLIT>
 int launch_core(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
                 uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
-                cudaStream_t s) {
+                cudaStream_t s, const FuseO& fo) {
     using LL = CoreLay<NTL, NS, SPLIT>;
     static_assert(LL::total <= 227 * 1024, "attention core shared memory");
     static bool attr = false;
@@ -438,7 +446,7 @@ int launch_core(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32
     dim3 grid(HW * ((nq + kQBlock - 1) / kQBlock));
     return int(launch_pdl(attention_core_kernel<NTL, NS, SPLIT>, grid, dim3(kThreads), LL::total, s,
                           static_cast<const __nv_bfloat16*>(qkv), qkv_lo, HW, C, heads, nq, q_frame0, tt,
-                          scale, bias, static_cast<__nv_bfloat16*>(ctx), ctx_lo));
+                          scale, bias, static_cast<__nv_bfloat16*>(ctx), ctx_lo, fo));
 }
 
 // ring depth per (K/V width, mode): deep rings for the narrow tiles (4 CTAs/SM at cfg2),
@@ -446,18 +454,18 @@ int launch_core(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32
 template <int NTL, bool SPLIT>
 int launch_ntl(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
                uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
-               cudaStream_t s) {
+               cudaStream_t s, const FuseO& fo) {
     constexpr int NS = NTL <= 4 ? 5 : (NTL <= 8 ? 4 : (SPLIT ? 2 : 3));
-    return launch_core<NTL, NS, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s);
+    return launch_core<NTL, NS, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
 }
 
 template <bool SPLIT>
 int launch_mode(uint32_t RP, const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
                 uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx,
-                int64_t ctx_lo, cudaStream_t s) {
+                int64_t ctx_lo, cudaStream_t s, const FuseO& fo) {
 #define CORE(NTL) \
     case NTL * 8: \
-        return launch_ntl<NTL, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s)
+        return launch_ntl<NTL, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo)
     switch (RP) {
         CORE(2); CORE(4); CORE(6); CORE(8); CORE(10); CORE(12);
         CORE(14); CORE(16); CORE(18); CORE(20); CORE(22); CORE(24);
@@ -470,9 +478,12 @@ int launch_mode(uint32_t RP, const void* qkv, int64_t qkv_lo, uint32_t HW, uint3
 
 int launch_attention_core_cpasync(const void* qkv, const void* qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
                           uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias,
-                          void* ctx, void* ctx_lo, cudaStream_t s) {
+                          void* ctx, void* ctx_lo, cudaStream_t s, const FuseO* fo) {
     if (HW == 0 || !qkv || !ctx || (qkv_lo == nullptr) != (ctx_lo == nullptr))
         return int(cudaErrorInvalidValue);
+    if (fo && fo->y && (heads != 1 || !fo->res || (fo->s == nullptr) != (fo->t == nullptr)))
+        return int(cudaErrorInvalidValue);
+    const FuseO f = fo ? *fo : FuseO{};
     if (nq == 0) return 0;
     if (!(heads > 0 && C % heads == 0 && (C / heads) % 8 == 0 && tt.kv_ok && tt.max_kv > 0 && tt.max_kv <= kKvMax))
         return int(cudaErrorInvalidValue);
@@ -481,9 +492,9 @@ int launch_attention_core_cpasync(const void* qkv, const void* qkv_lo, uint32_t 
     if (qkv_lo) {
         const int64_t ql = static_cast<const bf*>(qkv_lo) - static_cast<const bf*>(qkv);
         const int64_t cl = static_cast<bf*>(ctx_lo) - static_cast<bf*>(ctx);
-        return launch_mode<true>(RP, qkv, ql, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, cl, s);
+        return launch_mode<true>(RP, qkv, ql, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, cl, s, f);
     }
-    return launch_mode<false>(RP, qkv, 0, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, 0, s);
+    return launch_mode<false>(RP, qkv, 0, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, 0, s, f);
 }
 
 }  // namespace vinf

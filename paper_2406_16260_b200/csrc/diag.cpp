@@ -76,12 +76,29 @@ int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint3
         const uint64_t ctxn = uint64_t(L.f_clip) * L.hw * channels;
         TmpBuf qkv(plane * 2 * (f32 ? 2 : 1), s), ctx(ctxn * 2 * (f32 ? 2 : 1), s);
         cuda_check(cudaMemsetAsync(qkv.p, 0x3c, plane * 2 * (f32 ? 2 : 1), s), "fill");
+        // VINF_DIAG_FUSE=1 (one head): the fused output (block output = ctx' + res * s + t)
+        const bool fuse = getenv("VINF_DIAG_FUSE") && heads == 1;
+        TmpBuf res(fuse ? ctxn * (f32 ? 4 : 2) : 16, s), aff(fuse ? 2ull * channels * 4 : 16, s),
+            yb(fuse ? ctxn * (f32 ? 4 : 2) : 16, s);
+        FuseO fo;
+        if (fuse) {
+            cuda_check(cudaMemsetAsync(res.p, 0x3c, ctxn * (f32 ? 4 : 2), s), "fill");
+            cuda_check(cudaMemsetAsync(aff.p, 0, 2ull * channels * 4, s), "fill");
+            fo.res = res.p;
+            fo.res_bf16 = !f32;
+            if (!f32) {
+                fo.s = static_cast<const float*>(aff.p);
+                fo.t = static_cast<const float*>(aff.p) + channels;
+            }
+            fo.y = yb.p;
+            fo.y_bf16 = !f32;
+        }
         auto* q = static_cast<__nv_bfloat16*>(qkv.p);
         auto* c = static_cast<__nv_bfloat16*>(ctx.p);
         g_attn_pos_major = pos_major;
         auto launch = [&] {
             cuda_check(launch_attention_core(q, f32 ? q + plane : nullptr, L.af, L.hw, channels, heads, L.f_clip,
-                                             L.ha, tok.tt, L.scale, d.bias, c, f32 ? c + ctxn : nullptr, s),
+                                             L.ha, tok.tt, L.scale, d.bias, c, f32 ? c + ctxn : nullptr, s, &fo),
                        "attention core");
         };
         launch();

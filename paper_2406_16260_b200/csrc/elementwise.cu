@@ -190,7 +190,29 @@ __global__ void euler_kernel(void* __restrict__ x, const void* __restrict__ eps,
     }
 }
 
+// out[c][r] = in[r][c] through a 32 x 33 tile (weight layout change, once per set_block)
+__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out, uint32_t rows,
+                                 uint32_t cols) {
+    __shared__ float t[32][33];
+    const uint32_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (uint32_t i = threadIdx.y; i < 32; i += blockDim.y) {
+        const uint32_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) t[i][threadIdx.x] = in[uint64_t(r) * cols + c];
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.y; i < 32; i += blockDim.y) {
+        const uint32_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[uint64_t(c) * rows + r] = t[threadIdx.x][i];
+    }
+}
+
 }  // namespace
+
+int launch_transpose_f32(const float* in, float* out, uint32_t rows, uint32_t cols, cudaStream_t s) {
+    if (!rows || !cols) return 0;
+    transpose_kernel<<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(in, out, rows, cols);
+    return int(cudaGetLastError());
+}
 
 int launch_euler(void* x, const void* eps, bool bf16, uint64_t n, double lambda, cudaStream_t s) {
     if (n == 0) return 0;

@@ -40,8 +40,9 @@ struct EngineBlock {
     float* beta() const { return f32 + 4 * C; }
     uint32_t C = 0;
     DevMat conv;  // [taps*C, C]
-    DevMat wqkv;  // [3C, C]
+    DevMat wqkv;  // [3C, C]; with one head its V rows hold W_o W_v, re-formed every step
     DevMat wo;    // [C, C]
+    DevMat wvT;   // [C, C]: W_v transposed, the B operand of W_o W_v
 };
 
 struct vinf_engine {
@@ -148,6 +149,9 @@ struct vinf_engine {
     void stub_frames(uint32_t b, uint32_t f0, uint32_t nf, cudaStream_t s);  // own frames [f0, f0+nf)
     void stage_conv(uint32_t b, cudaStream_t s);
     void stage_gn_apply(uint32_t b, cudaStream_t s);
+    // W_vo = W_o W_v for block b (fuse_o), ahead of the GroupNorm fold that reads it (a fork
+    // onto a second stream beside the stub measured the same step time: it stays inline)
+    void launch_wvo(uint32_t b, cudaStream_t s);
     void stage_attention(uint32_t b, double t, cudaStream_t s);
     void stage_qkv(uint32_t b, cudaStream_t s);
     void project_qkv(uint32_t b, uint32_t frame0, uint32_t nframes, bool with_q, cudaStream_t s);
@@ -165,6 +169,15 @@ struct vinf_engine {
     bool fold() const {
         return !f32() && fold_env && (ablate == VINF_ABLATE_NONE || ablate == VINF_ABLATE_CONV);
     }
+    // One head: ctx W_o^T = P (X W_v^T) W_o^T = P (X (W_o W_v)^T), so the O projection is
+    // absorbed into V (W_vo = W_o W_v, formed each step by a C^3 GEMM ahead of the GroupNorm
+    // fold) and the attention core writes the block output (residual added in its epilogue).
+    // VINF_NO_FUSE_O=1 keeps the separate O GEMM.
+    bool fuse_o_env = [] {
+        const char* v = getenv("VINF_NO_FUSE_O");
+        return !v || !*v || *v == '0';
+    }();
+    bool fuse_o() const { return L.d.heads == 1 && fuse_o_env; }
     DevMat wfold_view() const {  // the folded Q/K/V weights (workspace), hi plane only
         DevMat m;
         m.rows = 3 * L.d.channels;
@@ -238,6 +251,26 @@ void vinf_engine::stage_conv(uint32_t b, cudaStream_t s) {
     launches += 1;
 }
 
+void vinf_engine::launch_wvo(uint32_t b, cudaStream_t s) {
+    // V rows of W_qkv = W_o W_v (A = W_o [C x C], B = W_v^T)
+    const EngineBlock& B = blocks.at(b);
+    const uint32_t C = L.d.channels;
+    Operand A;
+    A.hi = B.wo.hi;
+    A.lo = f32() ? B.wo.lo : nullptr;
+    A.rows = C;
+    A.cols = C;
+    A.ld = C;
+    Epilogue ep;
+    ep.out = B.wqkv.hi + uint64_t(2) * C * C;
+    ep.out_lo = f32() ? B.wqkv.lo + uint64_t(2) * C * C : nullptr;
+    ep.out_ld = C;
+    ep.out_bf16 = !f32();
+    Span wspan(this, "wvo_gemm", s);
+    gemm(A, {0}, B.wvT, {0}, C, C, ep, f32(), s);
+    launches += 1;
+}
+
 void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     const EngineBlock& B = blocks.at(b);
     double* sums = at<double>(L.off_sums);
@@ -248,6 +281,7 @@ void vinf_engine::stage_gn_apply(uint32_t b, cudaStream_t s) {
     // formed by the apply kernel itself from the (all-reduced) sums
     (void)stats;
     auto* u2 = at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E;
+    if (fuse_o()) launch_wvo(b, s);
     if (fold()) {
         const uint32_t C = L.d.channels;
         float* aff = gn_aff();
@@ -335,12 +369,24 @@ void vinf_engine::stage_attention(uint32_t b, double t, cudaStream_t s) {
         }
         Span span(this, "attn_core", s);
         const uint64_t plane = uint64_t(L.af) * hw * 3 * C;
+        FuseO fo;
+        if (fuse_o()) {  // the block output straight from the core: ctx' + GN(u) (O GEMM epilogue below)
+            fo.res = f32() ? at(L.off_u2f) : static_cast<void*>(at<__nv_bfloat16>(L.off_u2) + uint64_t(L.ha) * L.E);
+            fo.res_bf16 = !f32();
+            if (fold()) {
+                fo.s = gn_aff();
+                fo.t = gn_aff() + C;
+            }
+            fo.y = y_of(b);
+            fo.y_bf16 = !f32();
+        }
         cuda_check(launch_attention_core(qkv, f32() ? qkv + plane : nullptr, L.af, L.hw, C, L.d.heads, L.f_clip, L.ha,
                                          tt[(abl ? 2 : 0) + (bias_global ? 1 : 0)], L.scale, L.d.bias, ctx,
-                                         ctxlo, s),
+                                         ctxlo, s, &fo),
                    "attention core");
         ++launches;
     }
+    if (fuse_o()) return;
     Operand O;
     O.hi = ctx;
     O.lo = ctxlo;
@@ -539,6 +585,7 @@ int vinf_engine_create(const vinf_layout* l, void* workspace, void* stream, vinf
             B.conv.alloc(L.d.taps * C, C);
             B.wqkv.alloc(3 * C, C);
             B.wo.alloc(C, C);
+            B.wvT.alloc(C, C);
         }
         cuda_check(cudaStreamSynchronize(s), "engine create sync");
         *out = e;
@@ -558,6 +605,7 @@ void vinf_engine_destroy(vinf_engine* e) {
         B.conv.release();
         B.wqkv.release();
         B.wo.release();
+        B.wvT.release();
     }
     delete e;
 }
@@ -588,6 +636,8 @@ int vinf_engine_set_block(vinf_engine* e, uint32_t block, const float* stub_a,
         cuda_check(cudaMemcpyAsync(tmp + mat, wk, mat * 4, cudaMemcpyDeviceToDevice, s), "wk");
         cuda_check(cudaMemcpyAsync(tmp + 2 * mat, wv, mat * 4, cudaMemcpyDeviceToDevice, s), "wv");
         B.wqkv.from_f32(tmp, s);
+        cuda_check(launch_transpose_f32(wv, tmp, C, C, s), "transpose W_v");
+        B.wvT.from_f32(tmp, s);
         cuda_check(cudaFreeAsync(tmp, s), "tmp");
         B.wo.from_f32(wo, s);
     });

@@ -107,18 +107,104 @@ bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt);
 // ctx: [nq * HW, C] bf16.
 // Split (fp32) mode: qkv_lo / ctx_lo non-null are the lo planes (same layout) of the
 // bf16x3 operands; every product runs as hi*hi + hi*lo + lo*hi.
+// Fused output (one head, engine.cpp stage_attention): the O projection is absorbed into V
+// (the projection emits V' = X (W_o W_v)^T), so ctx' = P V' is already ctx W_o^T and the core
+// writes the block output y = ctx' + residual in place of ctx. residual = res * s + t per
+// channel (bf16 res, GroupNorm folded: s, t non-null), res (bf16) or res (fp32); y is bf16 or
+// fp32 (split mode: from ctx' hi + lo). res and y use ctx's [nq * HW, C] offsets.
+struct FuseO {
+    const void* res = nullptr;
+    const float* s = nullptr;
+    const float* t = nullptr;
+    void* y = nullptr;  // null: no fusion, ctx is written
+    int res_bf16 = 1;
+    int y_bf16 = 1;
+};
+#ifdef __CUDACC__
+// v += residual for 8 consecutive channels from `col`, given the raw bf16 residual piece u
+__device__ __forceinline__ void fuse_o_add_bf16(const FuseO& f, const uint4& u, uint32_t col, float (&v)[8]) {
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 x = __bfloat1622float2(u2[k]);
+        r[2 * k] = x.x;
+        r[2 * k + 1] = x.y;
+    }
+    if (f.s) {
+        const float4 s0 = __ldg(reinterpret_cast<const float4*>(f.s + col));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(f.s + col) + 1);
+        const float4 t0 = __ldg(reinterpret_cast<const float4*>(f.t + col));
+        const float4 t1 = __ldg(reinterpret_cast<const float4*>(f.t + col) + 1);
+        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        const float tc[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = r[k] * sc[k] + tc[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += r[k];
+}
+__device__ __forceinline__ void fuse_o_write(const FuseO& f, uint64_t o, const float (&v)[8]) {
+    if (f.y_bf16) {
+        uint4 w;
+        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+            wp[k] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(f.y) + o) = w;
+    } else {
+        float* yf = static_cast<float*>(f.y) + o;
+        reinterpret_cast<float4*>(yf)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(yf)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+}
+// y for 8 consecutive channels from `col` at element offset o, v = ctx' (fp32)
+__device__ __forceinline__ void fuse_o_store(const FuseO& f, uint64_t o, uint32_t col, float (&v)[8]) {
+    if (f.res_bf16) {
+        fuse_o_add_bf16(f, __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(f.res) + o)), col, v);
+    } else {
+        const float* rf = static_cast<const float*>(f.res) + o;
+        const float4 r0 = __ldg(reinterpret_cast<const float4*>(rf));
+        const float4 r1 = __ldg(reinterpret_cast<const float4*>(rf) + 1);
+        v[0] += r0.x; v[1] += r0.y; v[2] += r0.z; v[3] += r0.w;
+        v[4] += r1.x; v[5] += r1.y; v[6] += r1.z; v[7] += r1.w;
+    }
+    fuse_o_write(f, o, v);
+}
+// v[8] from one staged 16-byte piece of bf16 (and its lo plane in split mode)
+__device__ __forceinline__ void unpack8(const uint4& h, float (&v)[8]) {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&h);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 x = __bfloat1622float2(b[k]);
+        v[2 * k] = x.x;
+        v[2 * k + 1] = x.y;
+    }
+}
+__device__ __forceinline__ void unpack8_add(const uint4& l, float (&v)[8]) {
+    float w[8];
+    unpack8(l, w);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += w[k];
+}
+#endif
 // The same core as a cp.async ring over one position per CTA (attention_cpasync.cu).
 int launch_attention_core_cpasync(const void* qkv, const void* qkv_lo, uint32_t HW, uint32_t C, uint32_t heads,
                                   uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale, float bias,
-                                  void* ctx, void* ctx_lo, cudaStream_t s);
+                                  void* ctx, void* ctx_lo, cudaStream_t s, const FuseO* fo = nullptr);
 // Which implementation launch_attention_core uses: 0 = by configuration, 1 = the TMA ring,
 // 2 = the cp.async ring (VINF_ATTN_IMPL=tma|cpasync, vinf_debug_attention_impl).
 extern int g_attn_impl;
 // Diagnostics knob: 1 = the qkv buffer is position-major [HW][frames][3C].
 extern int g_attn_pos_major;
-// qkv_frames: frames of the qkv buffer (the TMA tensor maps' outer extent).
+// qkv_frames: frames of the qkv buffer (the TMA tensor maps' outer extent). fo: fused output
+// (null or fo->y null: ctx is written).
 int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_frames, uint32_t HW, uint32_t C,
                           uint32_t heads, uint32_t nq, uint32_t q_frame0, const TokenTable& tt, float scale,
-                          float bias, void* ctx, void* ctx_lo, cudaStream_t s);
+                          float bias, void* ctx, void* ctx_lo, cudaStream_t s, const FuseO* fo = nullptr);
+// out[c][r] = in[r][c] (fp32, rows x cols)
+int launch_transpose_f32(const float* in, float* out, uint32_t rows, uint32_t cols, cudaStream_t s);
 
 }  // namespace vinf
