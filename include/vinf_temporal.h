@@ -195,8 +195,10 @@ enum {
     VINF_BUF_CONV_IN = 2,/* conv operand, frames [hc | f_clip | hc] (bf16 plane / hi plane) */
     VINF_BUF_ATTN_IN = 3,/* attention operand, frames [ha | f_clip | ha | remote globals] */
     VINF_BUF_GN_SUMS = 4,/* f64 [2][groups] */
-    VINF_BUF_QKV = 5,    /* [attn frames * H*W, 3C] engine dtype (Q | K | V per row) */
-    VINF_BUF_CTX = 6     /* [f_clip * H*W, C] attention context (bf16 / hi plane) */
+    VINF_BUF_QKV = 5,    /* [attn frames * H*W, 3C] engine dtype (Q | K | V per row); with one
+                            head the V columns hold V' = X (W_o W_v)^T (the O projection absorbed) */
+    VINF_BUF_CTX = 6     /* [f_clip * H*W, C] attention context (bf16 / hi plane); not written with
+                            one head, where the core writes the block output (VINF_NO_FUSE_O=1: it is) */
 };
 int vinf_layout_region(const vinf_layout* l, int which, uint64_t* offset, uint64_t* bytes,
                        uint64_t* frame_bytes);
