@@ -718,7 +718,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                 // fused output, bf16 residual: this stage's residual pieces requested up front, so
                 // their latency (L2: the producer prefetched the item's rows) hides under the PV math
                 uint4 rpre[SPLIT ? 1 : kVPS][kPc];
-                if (!SPLIT && a.fo.y && a.fo.res_bf16 && !fr) {
+                if (D == 0 && !SPLIT && a.fo.y && a.fo.res_bf16) {
 #pragma unroll
                     for (int i = 0; i < int(kVPS); ++i)
 #pragma unroll
@@ -793,6 +793,20 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                         __syncwarp();
                         // 16 rows x kON 16-byte pieces: row rr -> query a0 + 16 mt + rr
                         constexpr int kPieces = 16 * kON;
+                        // fused output through the ring: this lane's columns are the same for all
+                        // of its pieces (kON divides 32), so s and t are read once per chunk
+                        float ssc[8], tsc[8];
+                        if (fr && a.fo_tab) {
+                            const float* sc = stab + ch * kDC + c0w + (uint32_t(lane) % kON) * 8;
+                            const float4 s0 = *reinterpret_cast<const float4*>(sc);
+                            const float4 s1 = *reinterpret_cast<const float4*>(sc + 4);
+                            const float4 t0 = *reinterpret_cast<const float4*>(sc + CC);
+                            const float4 t1 = *reinterpret_cast<const float4*>(sc + CC + 4);
+                            ssc[0] = s0.x; ssc[1] = s0.y; ssc[2] = s0.z; ssc[3] = s0.w;
+                            ssc[4] = s1.x; ssc[5] = s1.y; ssc[6] = s1.z; ssc[7] = s1.w;
+                            tsc[0] = t0.x; tsc[1] = t0.y; tsc[2] = t0.z; tsc[3] = t0.w;
+                            tsc[4] = t1.x; tsc[5] = t1.y; tsc[6] = t1.z; tsc[7] = t1.w;
+                        }
 #pragma unroll
                         for (int i2 = 0; i2 < (kPieces + 31) / 32; ++i2) {
                             const uint32_t pc = lane + 32 * i2;
@@ -813,24 +827,17 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                                         const uint4 u = *reinterpret_cast<const uint4*>(sm + slot + swz(q, col >> 3));
                                         if (a.fo_tab) {
                                             const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-                                            const float* sc = stab + ch * kDC + col;
-                                            const float4 s0 = *reinterpret_cast<const float4*>(sc);
-                                            const float4 s1 = *reinterpret_cast<const float4*>(sc + 4);
-                                            const float4 t0 = *reinterpret_cast<const float4*>(sc + CC);
-                                            const float4 t1 = *reinterpret_cast<const float4*>(sc + CC + 4);
-                                            const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-                                            const float tt8[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
                                             for (int k = 0; k < 4; ++k) {
                                                 const float2 x = __bfloat1622float2(u2[k]);
-                                                v[2 * k] += x.x * ss[2 * k] + tt8[2 * k];
-                                                v[2 * k + 1] += x.y * ss[2 * k + 1] + tt8[2 * k + 1];
+                                                v[2 * k] += x.x * ssc[2 * k] + tsc[2 * k];
+                                                v[2 * k + 1] += x.y * ssc[2 * k + 1] + tsc[2 * k + 1];
                                             }
                                         } else {
                                             fuse_o_add_bf16(a.fo, u, ch * kDC + col, v);
                                         }
                                         fuse_o_write(a.fo, o, v);
-                                    } else if (a.fo.res_bf16) {
+                                    } else if (D == 0 && a.fo.res_bf16) {
                                         fuse_o_add_bf16(a.fo, rpre[SPLIT ? 0 : i][i2], ch * kDC + col, v);
                                         fuse_o_write(a.fo, o, v);
                                     } else {
@@ -959,8 +966,15 @@ int launch_ntl(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
     }();
     const int cw = env_w == 8 ? 8 : 4;
     // one head with the head dim of a VideoCrafter2 level: compile-time chunk loops
+    // (a fused output goes through the ring only with the Q copy warp: otherwise the generic
+    // instance, whose consumers load the residual themselves)
+    static const bool ring_fuse = [] {
+        const char* q = getenv("VINF_ATTN_QFEED");
+        const char* l = getenv("VINF_ATTN_LOAD_ONLY");
+        return (!q || atoi(q) == 1) && (!l || atoi(l) != 2);
+    }();
     if constexpr (NTL <= 4 && !SPLIT) {
-        if (args.heads == 1) switch (args.d) {
+        if (args.heads == 1 && (!args.fo.y || (ring_fuse && args.fo.res_bf16))) switch (args.d) {
                 case 320: return cw == 8 ? launch_core<NTL, SPLIT, 8, 320>(maps, args, s)
                                          : launch_core<NTL, SPLIT, 4, 320>(maps, args, s);
                 case 640: return cw == 8 ? launch_core<NTL, SPLIT, 8, 640>(maps, args, s)
