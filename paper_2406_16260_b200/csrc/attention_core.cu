@@ -179,10 +179,12 @@ struct CoreLay {
     static constexpr uint32_t ring = (ost + kConsumerWarps * OST + 1023) / 1024 * 1024;
     static constexpr uint32_t bars(int ns) { return ring + uint32_t(ns) * ST; }
     static constexpr uint32_t total(int ns) { return bars(ns) + 2u * uint32_t(ns) * 8u + 1024u; }
-    // the deepest ring (<= 16 stages) that lets `c` CTAs share an SM
+    // the deepest ring (<= 16 stages) that lets `c` CTAs share an SM (228 KB per SM, of which
+    // the driver reserves 1 KB per CTA: sized against 227 KB / c, a ring could leave room for
+    // one CTA fewer, as it did for the F = 96, 20 x 32 case: 187 -> 124 us)
     static constexpr int stages(int c, uint32_t extra = 0) {
         int ns = 16;
-        while (ns > 2 && uint32_t(c) * (total(ns) + extra) > 227u * 1024u) --ns;
+        while (ns > 2 && uint32_t(c) * (total(ns) + extra + 1024u) > 228u * 1024u) --ns;
         return ns;
     }
     static_assert(total(2) <= 227 * 1024, "attention core shared memory");

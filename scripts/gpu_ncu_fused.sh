@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+CMD="python scripts/attn_micro.py 24 40 64 640 1 16 16 0"
+VINF_DIAG_FUSE=1 timeout 120 $CMD > gpurun_out/plain5.log 2>&1 && \
+VINF_DIAG_FUSE=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attention_core -s 1 -c 1 -o gpurun_out/prof_attn_fused $CMD > gpurun_out/ncu5.log 2>&1; echo "ncu rc=$?"; cat gpurun_out/plain5.log
