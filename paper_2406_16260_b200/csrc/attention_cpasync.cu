@@ -175,6 +175,23 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
             if (qk && q_ok) {
                 cp_async16(st + swz(lr, lp), q_src + col, bytes);
                 if (SPLIT) cp_async16(st + LL::QT + swz(lr, lp), q_src + qkv_lo + col, bytes);
+            } else if (!qk && q_ok && fo.y) {
+                // fused output: the chunk's residual rows into the idle Q slot of the PV stage
+                // (bf16: one piece per thread; fp32: 16 pieces of 4 floats a row, columns 0-31
+                // in the hi plane's slot, 32-63 in the lo plane's)
+                const uint64_t ro = (uint64_t(a0 + lr) * HW + p) * C + col;
+                if (fo.res_bf16) {
+                    cp_async16(st + swz(lr, lp), static_cast<const __nv_bfloat16*>(fo.res) + ro + (bytes ? lp * 8 : 0),
+                               bytes);
+                } else {
+#pragma unroll
+                    for (uint32_t k = 0; k < 2; ++k) {
+                        const uint32_t pc = lp + 8 * k;
+                        const uint32_t rb = pc * 4 < d - ch * kDC ? 16u : 0u;
+                        cp_async16(st + k * LL::QT + swz(lr, lp),
+                                   static_cast<const float*>(fo.res) + ro + (rb ? pc * 4 : 0), rb);
+                    }
+                }
             }
             const uint32_t kc = (qk ? C : 2 * C) + col;
 #pragma unroll
@@ -211,7 +228,9 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
         return sbase + LL::pb + uint32_t(kq >> 2) * (kQBlock * 128) + (mt * 16 + r7 + b1 * 8) * 128 +
                ((((kq & 3) * 2 + hb) ^ r7) << 4);
     };
-    auto store_ctx = [&](uint32_t buf, uint32_t c0, uint32_t vw) {  // staged chunk -> ctx rows
+    // staged chunk -> ctx rows; rslot: the ring slot of the chunk's PV stage (fused output: its
+    // residual rows sit in the slot's Q area)
+    auto store_ctx = [&](uint32_t buf, uint32_t c0, uint32_t vw, uint32_t rslot) {
         if (tid < int(nqh) * 8) {
             const uint32_t r = tid >> 3, c = tid & 7;
             if (c * 8 < vw) {
@@ -222,7 +241,17 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
                     float v[8];
                     unpack8(hv, v);
                     if (SPLIT) unpack8_add(*reinterpret_cast<const uint4*>(ost + LL::QT + swz(r, c)), v);
-                    fuse_o_store(fo, o, c0 + c * 8, v);
+                    const uint8_t* rs = sm + rslot * LL::stage;
+                    if (fo.res_bf16) {
+                        fuse_o_add_bf16(fo, *reinterpret_cast<const uint4*>(rs + swz(r, c)), c0 + c * 8, v);
+                    } else {
+                        const uint32_t p0 = 2 * c, p1 = 2 * c + 1;
+                        const float4 r0 = *reinterpret_cast<const float4*>(rs + (p0 >> 3) * LL::QT + swz(r, p0 & 7));
+                        const float4 r1 = *reinterpret_cast<const float4*>(rs + (p1 >> 3) * LL::QT + swz(r, p1 & 7));
+                        v[0] += r0.x; v[1] += r0.y; v[2] += r0.z; v[3] += r0.w;
+                        v[4] += r1.x; v[5] += r1.y; v[6] += r1.z; v[7] += r1.w;
+                    }
+                    fuse_o_write(fo, o, v);
                 } else {
                     *reinterpret_cast<uint4*>(ctx + o) = hv;
                     if (SPLIT)
@@ -370,7 +399,9 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
         for (uint32_t ch = 0; ch < nch; ++ch, ++och) {
             cp_wait<NS - 2>();
             __syncthreads();
-            if (ch > 0) store_ctx((och - 1) & 1, h * d + (ch - 1) * kDC, min(uint32_t(kDC), d - (ch - 1) * kDC));
+            if (ch > 0)
+                store_ctx((och - 1) & 1, h * d + (ch - 1) * kDC, min(uint32_t(kDC), d - (ch - 1) * kDC),
+                          cslot == 0 ? NS - 1 : cslot - 1);
             issue();
             const uint32_t st = sbase + cslot * LL::stage;
             cslot = cslot + 1 == NS ? 0 : cslot + 1;
@@ -423,7 +454,8 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
             }
         }
         __syncthreads();
-        store_ctx((och - 1) & 1, h * d + (nch - 1) * kDC, min(uint32_t(kDC), d - (nch - 1) * kDC));
+        store_ctx((och - 1) & 1, h * d + (nch - 1) * kDC, min(uint32_t(kDC), d - (nch - 1) * kDC),
+                  cslot == 0 ? NS - 1 : cslot - 1);
         // the staging buffer and S / P scratch are rewritten only after the next head's
         // first S-phase barrier
     }
