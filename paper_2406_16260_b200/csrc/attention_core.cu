@@ -43,6 +43,12 @@ namespace vinf {
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn();
 int g_attn_pos_major = 0;
+// widest K/V list (rows) the copy-warp TMA instances take for one-block clips
+// (VINF_ATTN_CW_ROWS, diagnostics)
+static const uint32_t g_cw_rows = [] {
+    const char* e = getenv("VINF_ATTN_CW_ROWS");
+    return e ? uint32_t(atoi(e)) : 64u;
+}();
 int g_attn_impl = []() {  // 0 = by configuration, 1 = TMA ring, 2 = cp.async ring (diagnostics)
     const char* e = getenv("VINF_ATTN_IMPL");
     if (!e) return 0;
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     constexpr int NJ = (NTL + kWQ - 1) / kWQ;  // S n8 tiles per warp
     constexpr int NA = NJ <= 2 ? 2 : 1;         // S accumulators per tile (shorter MMA chains)
     static_assert(NTL % 2 == 0 && RP <= uint32_t(kKvMax), "K/V rows padded to a multiple of 16");
-    static_assert(D == 0 || RP <= 32, "the copy warp holds at most 8 K/V rows per lane");
+    static_assert(D == 0 || RP <= 64, "copy-warp instances: K/V tiles of up to 64 rows");
     extern __shared__ uint8_t sm_raw[];
     // 1 KB aligned, offset from the __shared__ array itself so every access stays a shared-space
     // access (a pointer rebuilt from an integer would make them generic loads / stores)
@@ -279,11 +285,12 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
             const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
             const uint32_t nqh = min(uint32_t(kQBlock), a.nq - qb * kQBlock);
             const uint32_t qf = a.q_frame0 + qb * kQBlock;
-            // this lane's K/V frames (rows r0, r0 + 4, ... < R <= 32), read once per item
+            // this lane's K/V frames (rows r0, r0 + 4, ... < R <= RP), read once per item
             const uint32_t R = a.tt.kv_count[qb];
-            uint32_t vfr[8];
+            constexpr int kVF = int(RP) / 4;
+            uint32_t vfr[kVF];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < kVF; ++k) {
                 const uint32_t row = r0 + 4u * uint32_t(k);
                 vfr[k] = a.qfeed >= 2 && row < R ? a.tt.kv_frames[size_t(qb) * kKvMax + row] : 0u;
             }
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                         const bool valid = col < dd;
                         const uint32_t chunk = (2 * CC + h * dd) / kDC + ch;
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
+                        for (int k = 0; k < kVF; ++k) {
                             const uint32_t row = r0 + 4u * uint32_t(k);
                             if (row >= R) break;
                             const uint32_t f = vfr[k];
@@ -975,7 +982,7 @@ int launch_ntl(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
         const char* l = getenv("VINF_ATTN_LOAD_ONLY");
         return (!q || atoi(q) == 1) && (!l || atoi(l) != 2);
     }();
-    if constexpr (NTL <= 4 && !SPLIT) {
+    if constexpr (NTL <= 8 && !SPLIT) {
         if (args.heads == 1 && (!args.fo.y || (ring_fuse && args.fo.res_bf16))) switch (args.d) {
                 case 320: return cw == 8 ? launch_core<NTL, SPLIT, 8, 320>(maps, args, s)
                                          : launch_core<NTL, SPLIT, 4, 320>(maps, args, s);
@@ -1025,7 +1032,13 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     // CTA everywhere else (wide tiles of long clips: 581 vs 784 us at F = 288, C = 320; the
     // split mode: 144 vs 154 us), where thread-issued copies of many CTAs keep more in flight.
     const uint32_t RPw = (uint32_t(tt.max_kv) + 15) & ~15u;
-    const int impl = g_attn_impl ? g_attn_impl : (!qkv_lo && RPw <= 32 ? 1 : 2);
+    // Single-head VideoCrafter2 head dims on a one-block clip (nq <= 32: a clip-parallel worker's
+    // 24 frames) run the copy-warp TMA instances up to 64 K/V rows (its halo + remote-global
+    // list: 124 vs 148 us for 2 workers, 139 vs 152 us for 8, profiles/r02_attn/worker_impl.txt);
+    // long clips (many blocks per position) keep the cp.async ring above 32 rows (626 vs 862 us
+    // at F = 288, C = 320).
+    const bool cw_inst = heads == 1 && (C == 320 || C == 640 || C == 1280) && nq <= uint32_t(kQBlock);
+    const int impl = g_attn_impl ? g_attn_impl : (!qkv_lo && (RPw <= 32 || (cw_inst && RPw <= g_cw_rows)) ? 1 : 2);
     if (impl == 2)
         return launch_attention_core_cpasync(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s,
                                              fo);

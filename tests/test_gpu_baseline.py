@@ -188,6 +188,20 @@ def test_cfg4_clip_parallel_2304(en, oracle, parity_log, dtype):
     check(parity_log, f"cfg4 {NAME[dtype]} F=2304 over 8 C=64 n_global=64", got, want, TOL[dtype])
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("workers,C", [(2, 640), (8, 320), (4, 1280)])
+def test_clip_parallel_worker_tiles(en, oracle, parity_log, dtype, workers, C):
+    # 24 frames per worker (configs[2]'s clip): one query block per position with a 40-56 row
+    # K/V list (own frames + halos + remote globals), the copy-warp TMA instances with the
+    # O projection absorbed (bf16) and the cp.async ring (fp32)
+    F, H, W = 24 * workers, 2, 4
+    x = oracle.tensor_from_seed((F, H, W, C), 8)
+    got = run_engines(en, x, dtype, 900.0, workers=workers)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 900.0, 32)
+    check(parity_log, f"workers {NAME[dtype]} {workers} x 24 frames 2x4 C={C}", got, want, TOL[dtype])
+
+
 # ---- GroupNorm with shifted inputs ------------------------------------------------------
 
 
