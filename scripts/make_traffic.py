@@ -9,7 +9,8 @@ GROUPS = {
     "colpart_fold": "gn_stats",
     "group_fold_kernel": "gn_fold",
     "group_apply_bf16_kernel": "gn_apply",
-    ", 1, 0, 0, 1>": "qkv_gemm",
+    "<240, 1, 0, 0, 1>": "qkv_gemm",
+    "<224, 1, 0, 0, 1>": "wvo_gemm",
     "attention_core_kernel": "attn_core",
     ", 1, 1, 0, 1>": "o_gemm",
     "stub_bf16_kernel": "stub",
