@@ -202,6 +202,21 @@ def test_clip_parallel_worker_tiles(en, oracle, parity_log, dtype, workers, C):
     check(parity_log, f"workers {NAME[dtype]} {workers} x 24 frames 2x4 C={C}", got, want, TOL[dtype])
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_o_projection_absorbed_vs_separate(en, oracle, parity_log, dtype, monkeypatch):
+    # one head: the engine absorbs W_o into V and the attention core writes the block output;
+    # VINF_NO_FUSE_O=1 (read per engine) keeps ctx and the O GEMM. Both against the oracle.
+    F, H, W, C = 24, 4, 8, 640
+    x = oracle.tensor_from_seed((F, H, W, C), 9)
+    bp = oracle.build_block(C, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 900.0, 32)
+    fused = run_engines(en, x, dtype, 900.0)
+    monkeypatch.setenv("VINF_NO_FUSE_O", "1")
+    separate = run_engines(en, x, dtype, 900.0)
+    check(parity_log, f"O absorbed {NAME[dtype]} F=24 4x8 C=640", fused, want, TOL[dtype])
+    check(parity_log, f"O separate {NAME[dtype]} F=24 4x8 C=640", separate, want, TOL[dtype])
+
+
 # ---- GroupNorm with shifted inputs ------------------------------------------------------
 
 
