@@ -53,7 +53,7 @@ int g_attn_impl = []() {  // 0 = by configuration, 1 = TMA ring, 2 = cp.async ri
     const char* e = getenv("VINF_ATTN_IMPL");
     if (!e) return 0;
     const std::string v(e);
-    return v == "tma" ? 1 : v == "cpasync" ? 2 : v == "tc5" ? 3 : 0;
+    return v == "tma" ? 1 : v == "cpasync" ? 2 : 0;
 }();
 
 namespace {
@@ -870,341 +870,6 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// tcgen05 core for one-block clips (the 24-frame VideoCrafter2 clip and a clip-parallel
-// worker's 24 frames: nq <= 32 queries, <= 32 distinct K/V frames per position, one head,
-// bf16). Item = 4 consecutive positions; their 4 x 32 query rows form one M = 128 tile
-// (row = 32 * position + query frame), so:
-//   * S: per position one tcgen05.mma M=128 N=32 per 16-wide k step against that position's
-//     K rows, into TMEM columns 32 * position (only the diagonal 32 x 32 blocks are used);
-//   * softmax: warp q (TMEM lane quadrant q = position q) reads its rows' 32 columns with one
-//     tcgen05.ld, one query row per thread, no shuffles; P (bf16, block-diagonal 128 x 128,
-//     the off-diagonal blocks stay zero) to shared memory;
-//   * PV: per 64-wide output chunk one M=128 N=64 K=128 accumulation with V as an MN-major
-//     operand (the TMA tile of K/V rows as loaded), into a double-buffered TMEM chunk;
-//   * epilogue: the same four warps drain each chunk (one row per thread, 64 columns), add
-//     the residual (fused output) and write 128-byte row pieces.
-// Roles: warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue (two per TMEM lane
-// quadrant, 32 columns of each output chunk each); warps 2-5 also run the softmax.
-constexpr int kT5Pos = 4;
-constexpr uint32_t kT5Tile = 128u * 128u;       // 128 rows x 128 B
-constexpr uint32_t kT5Stage = 2u * kT5Tile;     // S: Q tile + K tile; PV: two V chunks
-constexpr int kT5Stages = 5;
-constexpr int kT5Threads = 320;  // + 8 softmax / epilogue warps (two per TMEM lane quadrant)
-constexpr uint32_t kT5Ring = 0;
-constexpr uint32_t kT5P = kT5Ring + kT5Stages * kT5Stage;  // P: two 64-column blocks
-constexpr uint32_t kT5Tab = kT5P + 2 * kT5Tile;            // s, t (2C floats)
-__host__ __device__ constexpr uint32_t t5_bars(uint32_t C) { return kT5Tab + 2u * C * 4u; }
-__host__ __device__ constexpr uint32_t t5_total(uint32_t C) { return t5_bars(C) + 256u + 1024u; }
-
-struct T5Args {
-    uint32_t HW, nq, q_frame0, items;
-    float scale, bias;
-    TokenTable tt;
-    FuseO fo;
-    __nv_bfloat16* ctx;
-};
-
-// MN-major operand (V: rows = the K dimension, 64 N elements per 128-byte row), SW128
-__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
-    d |= static_cast<uint64_t>(kT5Tile >> 4) << 16;  // LBO: next 64-wide N block (unused at N = 64)
-    d |= static_cast<uint64_t>(1024u >> 4) << 32;    // SBO: next 8-row group along K
-    d |= 1ull << 46;
-    d |= 2ull << 61;
-    return d;
-}
-
-template <int D>
-__global__ void __launch_bounds__(kT5Threads, 1) attention_tc5_kernel(const __grid_constant__ AttnMaps maps,
-                                                                     const T5Args a) {
-    constexpr uint32_t nch = D / kDC;
-    constexpr uint32_t nvs = (nch + 1) / 2;
-    extern __shared__ uint8_t sm_raw[];
-    uint8_t* sm = sm_raw + ((1024u - (dev::smem_u32(sm_raw) & 1023u)) & 1023u);
-    const uint32_t sbase = dev::smem_u32(sm);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + t5_bars(D));
-    uint64_t* empty = full + kT5Stages;
-    uint64_t* sfull = empty + kT5Stages;   // S accumulated (MMA commit)
-    uint64_t* pfull = sfull + 1;           // P written (4 softmax warps)
-    uint64_t* ofull = pfull + 1;           // [2] output chunk accumulated
-    uint64_t* oempty = ofull + 2;          // [2] output chunk drained (4 warps)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(oempty + 2);
-    float* stab = reinterpret_cast<float*>(sm + kT5Tab);
-
-    // zero the ring and P once (pad rows and P's off-diagonal blocks stay finite / zero)
-    for (uint32_t i = tid * 16; i < kT5Tab; i += kT5Threads * 16)
-        *reinterpret_cast<uint4*>(sm + i) = make_uint4(0, 0, 0, 0);
-    if (tid == 0) {
-        for (int s = 0; s < kT5Stages; ++s) {
-            dev::mbar_init(&full[s], 1);
-            dev::mbar_init(&empty[s], 1);
-        }
-        dev::mbar_init(sfull, 1);
-        dev::mbar_init(pfull, 4);
-        for (int b = 0; b < 2; ++b) {
-            dev::mbar_init(&ofull[b], 1);
-            dev::mbar_init(&oempty[b], 8);
-        }
-        dev::fence_barrier_init();
-    }
-    if (warp == 1) dev::tmem_alloc(tmem_holder, 256);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    dev::tc_fence_before();
-    __syncthreads();
-    dev::tc_fence_after();
-    const uint32_t tmem = *tmem_holder;
-    dev::pdl_wait();
-    dev::pdl_trigger();
-    const bool tab = a.fo.y && a.fo.s;
-    if (tab) {
-        for (uint32_t i = tid; i < uint32_t(D); i += kT5Threads) {
-            stab[i] = a.fo.s[i];
-            stab[D + i] = a.fo.t[i];
-        }
-    }
-    __syncthreads();
-
-    const uint32_t R = a.tt.kv_count[0];
-    const uint32_t kvb = uint32_t(a.tt.kv_load_rows[0]) * 128u;  // one position's K or V chunk
-    if (warp == 0) {
-        // ---------------- producer ----------------
-        if (lane == 0) {
-            const uint32_t nb = a.tt.kv_nbox[0];
-            const uint32_t* prog = a.tt.kv_box;
-            auto box4 = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, uint32_t p, uint32_t which,
-                            uint32_t ch, uint32_t f0) {
-                tma_load_4d(dst, map, bar, int32_t(ch * kDC), int32_t(which), int32_t(p), int32_t(f0));
-            };
-            auto load_kv = [&](uint32_t dst, uint64_t* bar, uint32_t p, uint32_t which, uint32_t ch) {
-                for (uint32_t b = 0; b < nb; ++b) {
-                    const uint32_t e = prog[b];
-                    const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
-                    if (kind == uint32_t(kBoxGather4)) {
-                        const uint32_t e1 = prog[b + 1], e2 = prog[b + 2];
-                        b += 2;
-                        auto gr = [&](uint32_t f) { return int32_t(f * a.HW + p); };
-                        dev::tma_gather4(dst + row * 128u, &maps.g4[0], bar, int32_t(which * D + ch * kDC),
-                                         gr(e & 0xFFFFu), gr(e1 & 0xFFFFu), gr(e1 >> 16), gr(e2 & 0xFFFFu));
-                        continue;
-                    }
-                    box4(dst + row * 128u, &maps.box[0][kind], bar, p, which, ch, e & 0xFFFFu);
-                }
-            };
-            Ring r(kT5Stages);
-            for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
-                const uint32_t p0 = item * kT5Pos;
-                const uint32_t np = min(uint32_t(kT5Pos), a.HW - p0);
-                if (a.fo.y) {  // the item's residual rows into L2 (the epilogue reads them directly)
-                    for (uint32_t q = 0; q < np; ++q)
-                        for (uint32_t f = 0; f < a.nq; ++f)
-                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                             static_cast<const __nv_bfloat16*>(a.fo.res) +
-                                             (uint64_t(f) * a.HW + p0 + q) * D),
-                                         "r"(uint32_t(D * 2))
-                                         : "memory");
-                }
-                for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
-                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
-                    uint64_t* bar = &full[r.slot];
-                    const uint32_t st = sbase + kT5Ring + r.slot * kT5Stage;
-                    dev::mbar_arrive_expect_tx(bar, np * (a.nq * 128u + kvb));
-                    for (uint32_t q = 0; q < np; ++q) {
-                        box4(st + q * 4096u, &maps.box[0][a.nq - 1], bar, p0 + q, 0, ch, a.q_frame0);
-                        load_kv(st + kT5Tile + q * 4096u, bar, p0 + q, 1, ch);
-                    }
-                }
-                for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
-                    const uint32_t n = min(2u, nch - vs * 2);
-                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
-                    uint64_t* bar = &full[r.slot];
-                    const uint32_t st = sbase + kT5Ring + r.slot * kT5Stage;
-                    dev::mbar_arrive_expect_tx(bar, n * np * kvb);
-                    for (uint32_t i = 0; i < n; ++i)
-                        for (uint32_t q = 0; q < np; ++q) load_kv(st + i * kT5Tile + q * 4096u, bar, p0 + q, 2, vs * 2 + i);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
-        constexpr uint32_t idS = dev::idesc_bf16_f32(128, 32);
-        constexpr uint32_t idPV = dev::idesc_bf16_f32(128, 64) | (1u << 16);  // B (V) MN-major
-        const uint32_t tS = tmem, tO = tmem + 128;
-        Ring r(kT5Stages);
-        uint32_t oc_count = 0, li = 0;
-        for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x, ++li) {
-            for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
-                dev::mbar_wait(&full[r.slot], r.phase);
-                dev::tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t st = sbase + kT5Ring + r.slot * kT5Stage;
-                    const uint64_t qd = dev::sw128_kmajor_desc(st);
-#pragma unroll
-                    for (uint32_t q = 0; q < uint32_t(kT5Pos); ++q) {
-                        const uint64_t kd = dev::sw128_kmajor_desc(st + kT5Tile + q * 4096u);
-#pragma unroll
-                        for (uint32_t kk = 0; kk < 4; ++kk)
-                            dev::umma_bf16(tS + q * 32, qd + 2 * kk, kd + 2 * kk, idS, (ch > 0 || kk > 0) ? 1u : 0u);
-                    }
-                    dev::umma_commit(&empty[r.slot]);
-                    if (ch == nch - 1) dev::umma_commit(sfull);
-                }
-                __syncwarp();
-            }
-            dev::mbar_wait(pfull, li & 1u);  // softmax done: P in shared memory, S read
-            dev::tc_fence_after();
-            for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
-                const uint32_t n = min(2u, nch - vs * 2);
-                dev::mbar_wait(&full[r.slot], r.phase);
-                dev::tc_fence_after();
-                const uint32_t st = sbase + kT5Ring + r.slot * kT5Stage;
-                for (uint32_t i = 0; i < n; ++i, ++oc_count) {
-                    const uint32_t b = oc_count & 1u;
-                    dev::mbar_wait(&oempty[b], ((oc_count >> 1) & 1u) ^ 1u);
-                    dev::tc_fence_after();
-                    if (lane == 0) {
-                        const uint64_t vd = sw128_mnmajor_desc(st + i * kT5Tile);
-#pragma unroll
-                        for (uint32_t kk = 0; kk < 8; ++kk) {
-                            const uint64_t pd = dev::sw128_kmajor_desc(sbase + kT5P + (kk >> 2) * kT5Tile) + 2 * (kk & 3);
-                            dev::umma_bf16(tO + b * 64, pd, vd + (kk * 2048u >> 4), idPV, kk > 0 ? 1u : 0u);
-                        }
-                        dev::umma_commit(&ofull[b]);
-                    }
-                    __syncwarp();
-                }
-                if (lane == 0) dev::umma_commit(&empty[r.slot]);
-                __syncwarp();
-            }
-        }
-    } else {
-        // ---------------- softmax + epilogue: warp quadrant q = position q ----------------
-        const uint32_t q = uint32_t(warp) & 3u;
-        const uint32_t half = uint32_t(warp - 2) >> 2;  // which 32 columns of an output chunk
-        const bool smx = half == 0;                        // warps 2-5 run the softmax
-        const uint32_t f = uint32_t(lane);  // this thread's query frame (row 32 q + f)
-        const bool qok = f < a.nq;
-        const int wlo = qok ? a.tt.wlo[f] : 0, whi = qok ? a.tt.whi[f] : -1;
-        const float bw = a.tt.wflag ? a.bias : 0.f, bg = a.tt.gflag ? a.bias : 0.f;
-        uint32_t gm[8];  // gmult[0..31], four per word
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            uint32_t w = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t c = uint32_t(4 * k + j);
-                w |= (c < R ? uint32_t(a.tt.gmult[c]) : 0u) << (8 * j);
-            }
-            gm[k] = w;
-        }
-        const uint32_t row = 32u * q + f;
-        const uint32_t lane_base = (32u * q) << 16;
-        uint32_t oc_count = 0, li = 0;
-        for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x, ++li) {
-            const uint32_t p = item * kT5Pos + q;
-            const bool live = qok && p < a.HW;
-            if (smx) {
-                dev::mbar_wait(sfull, li & 1u);
-                dev::tc_fence_after();
-                uint32_t sr[32];
-                dev::tmem_ld_32x32b_x32(tmem + lane_base + q * 32, sr);
-                dev::tmem_wait_ld();
-                // token softmax (column form): window tokens c in [wlo, whi], gmult[c] global tokens
-                float e[32], m = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float sv = a.scale * __uint_as_float(sr[c]);
-                    const uint32_t g = (gm[c >> 2] >> (8 * (c & 3))) & 0xFFu;
-                    const bool inw = uint32_t(c) < R && c >= wlo && c <= whi;
-                    e[c] = sv;
-                    if (inw) m = fmaxf(m, sv + bw);
-                    if (g) m = fmaxf(m, sv + bg);
-                }
-                float z = 0.f;
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const uint32_t g = (gm[c >> 2] >> (8 * (c & 3))) & 0xFFu;
-                    const bool inw = uint32_t(c) < R && c >= wlo && c <= whi;
-                    float v = inw ? __expf(e[c] + bw - m) : 0.f;
-                    if (g) v += float(g) * __expf(e[c] + bg - m);
-                    e[c] = v;
-                    z += v;
-                }
-                const float zi = live ? 1.0f / z : 0.f;
-                // P row: 32 bf16 at columns 32 q .. 32 q + 31 (block q / 2, 16-byte chunks 4 (q & 1) + j)
-                uint8_t* pr = sm + kT5P + (q >> 1) * kT5Tile;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        w[k] = live ? pack_bf16(e[8 * j + 2 * k] * zi, e[8 * j + 2 * k + 1] * zi) : 0u;
-                    *reinterpret_cast<uint4*>(pr + swz(row, 4u * (q & 1u) + uint32_t(j))) =
-                        make_uint4(w[0], w[1], w[2], w[3]);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
-                dev::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) dev::mbar_arrive(pfull);
-            }
-            // epilogue: nch output chunks of 64 columns, this warp's 32 of them
-            const uint64_t orow = (uint64_t(f) * a.HW + p) * D + half * 32;
-            for (uint32_t oc = 0; oc < nch; ++oc, ++oc_count) {
-                const uint32_t b = oc_count & 1u;
-                uint32_t rv[16];  // the residual's 32 bf16 (two 32-byte loads)
-                if (live && a.fo.y) {
-                    const __nv_bfloat16* rs = static_cast<const __nv_bfloat16*>(a.fo.res) + orow + oc * kDC;
-#pragma unroll
-                    for (int k = 0; k < 2; ++k)
-                        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                                     : "=r"(rv[8 * k]), "=r"(rv[8 * k + 1]), "=r"(rv[8 * k + 2]), "=r"(rv[8 * k + 3]),
-                                       "=r"(rv[8 * k + 4]), "=r"(rv[8 * k + 5]), "=r"(rv[8 * k + 6]), "=r"(rv[8 * k + 7])
-                                     : "l"(rs + 16 * k));
-                }
-                dev::mbar_wait(&ofull[b], (oc_count >> 1) & 1u);
-                dev::tc_fence_after();
-                uint32_t o0[32];
-                dev::tmem_ld_32x32b_x32(tmem + lane_base + 128 + b * 64 + half * 32, o0);
-                dev::tmem_wait_ld();
-                dev::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&oempty[b]);
-                if (!live) continue;
-                uint32_t w[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {  // columns 2k, 2k + 1
-                    float v0 = __uint_as_float(o0[2 * k]), v1 = __uint_as_float(o0[2 * k + 1]);
-                    if (a.fo.y) {
-                        const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv[k]));
-                        if (tab) {
-                            const float* sc = stab + oc * kDC + half * 32 + 2 * k;
-                            v0 += x.x * sc[0] + sc[D];
-                            v1 += x.y * sc[1] + sc[D + 1];
-                        } else {
-                            v0 += x.x;
-                            v1 += x.y;
-                        }
-                    }
-                    w[k] = pack_bf16(v0, v1);
-                }
-                __nv_bfloat16* dst = (a.fo.y ? static_cast<__nv_bfloat16*>(a.fo.y) : a.ctx) + orow + oc * kDC;
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * k), "r"(w[8 * k]),
-                                 "r"(w[8 * k + 1]), "r"(w[8 * k + 2]), "r"(w[8 * k + 3]), "r"(w[8 * k + 4]),
-                                 "r"(w[8 * k + 5]), "r"(w[8 * k + 6]), "r"(w[8 * k + 7])
-                                 : "memory");
-            }
-        }
-    }
-    dev::tc_fence_before();
-    __syncthreads();
-    dev::tc_fence_after();
-    if (warp == 1) dev::tmem_dealloc(tmem, 256);
-}
-
 int g_sms = 0;
 
 // 4-D view of the [frames][HW][3 x heads][d] Q/K/V buffer (one bf16 plane): boxes of
@@ -1344,25 +1009,6 @@ int launch_mode(uint32_t RP, const AttnMaps& maps, const AttnArgs& args, cudaStr
 #undef CORE
 }
 
-template <int D>
-int launch_tc5_d(const AttnMaps& maps, const T5Args& args, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(attention_tc5_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(t5_total(D)));
-        if (e != cudaSuccess) return int(e);
-        attr = true;
-    }
-    if (g_sms == 0) {
-        int dv = 0;
-        cudaGetDevice(&dv);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dv);
-        if (g_sms <= 0) g_sms = 148;
-    }
-    const uint32_t grid = args.items < uint32_t(g_sms) ? args.items : uint32_t(g_sms);
-    return int(launch_pdl(attention_tc5_kernel<D>, dim3(grid), dim3(kT5Threads), t5_total(D), s, maps, args));
-}
-
 }  // namespace
 
 bool attention_core_supported(uint32_t C, uint32_t heads, const TokenTable& tt) {
@@ -1433,27 +1079,6 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
             cache_next = (cache_next + 1) % 8;
         }
         maps = cache[hit].maps;
-    }
-    // the tcgen05 core (one-block clips, <= 32 K/V rows, one head, VideoCrafter2 head dims)
-    if (impl == 3) {
-        if (qkv_lo || heads != 1 || nq > uint32_t(kQBlock) || tt.max_kv > 32 || g_attn_pos_major != 0 ||
-            !(C == 320 || C == 640 || C == 1280))
-            return int(cudaErrorInvalidValue);
-        T5Args t5;
-        t5.HW = HW;
-        t5.nq = nq;
-        t5.q_frame0 = q_frame0;
-        t5.items = (HW + kT5Pos - 1) / kT5Pos;
-        t5.scale = scale;
-        t5.bias = bias;
-        t5.tt = tt;
-        if (fo) t5.fo = *fo;
-        t5.ctx = static_cast<__nv_bfloat16*>(ctx);
-        switch (C) {
-            case 320: return launch_tc5_d<320>(maps, t5, s);
-            case 640: return launch_tc5_d<640>(maps, t5, s);
-            default: return launch_tc5_d<1280>(maps, t5, s);
-        }
     }
     AttnArgs args;
     args.HW = HW;

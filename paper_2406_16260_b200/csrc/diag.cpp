@@ -36,10 +36,10 @@ int vinf_bulk_bw_bench(uint64_t bytes, uint32_t chunk, uint32_t stages, uint32_t
 }
 
 // Selects the attention core implementation for later launches (0 = by configuration,
-// 1 = TMA ring, 2 = cp.async ring, 3 = tcgen05 core); returns the previous setting.
+// 1 = TMA ring, 2 = cp.async ring); returns the previous setting.
 int vinf_debug_attention_impl(int impl) {
     const int old = g_attn_impl;
-    if (impl >= 0 && impl <= 3) g_attn_impl = impl;
+    if (impl >= 0 && impl <= 2) g_attn_impl = impl;
     return old;
 }
 
