@@ -56,10 +56,11 @@ def main():
         st = e.kernel_stats()
         ms = a.elapsed_time(b) / args.steps
         attn_ms = st["attn_core"][0] / st["attn_core"][1]
-        attn_bytes = 4.0 * F * H * W * C * 2
-        flops = 14.0 * F * H * W * C * C
+        fused = "o_gemm" not in st  # one head: the O projection absorbed into V, output fused
+        attn_bytes = (5.0 if fused else 4.0) * F * H * W * C * 2
+        flops = (12.0 if fused else 14.0) * F * H * W * C * C
         row = {"frames": F, "n_global": ng, "n_local": nl, "ms_per_step": ms,
-               "frames_per_s": F / (ms / 1000.0), "attn_core_us": attn_ms * 1000.0,
+               "frames_per_s": F / (ms / 1000.0), "attn_core_us": attn_ms * 1000.0, "fused_output": fused,
                "attn_core_gbs": attn_bytes / (attn_ms / 1000.0) / 1e9,
                "attn_core_frac_hbm": attn_bytes / (attn_ms / 1000.0) / 1e9 / hbm,
                "block_frac_tensor": flops / (ms / 1000.0) / 1e12 / tf_sus}
