@@ -353,7 +353,8 @@ int vinf_engine_denoise_dist(vinf_engine* e, uint32_t steps, vinf_comm* comm, in
 int vinf_gemm_bench(uint32_t M, uint32_t N, uint32_t K, uint32_t nseg, int flags, int residual,
                     int iters, float* avg_ms);
 /* The attention core alone on a single-worker engine layout's token table (t > t_star),
- * over a synthetic Q/K/V buffer; pos_major = 1 views it as [HW][frames][3C]. */
+ * over a synthetic Q/K/V buffer; pos_major must be 0 (frame-major; the position-major and
+ * chunked layouts were measured and removed). */
 int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint32_t channels, uint32_t heads,
                          uint32_t n_local, uint32_t n_global, int f32, int pos_major, int iters, float* avg_ms);
 /* The attention core's feed for later launches: 0 = by configuration (TMA ring for bf16

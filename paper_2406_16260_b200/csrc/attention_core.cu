@@ -42,7 +42,6 @@
 namespace vinf {
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn();
-int g_attn_pos_major = 0;
 // widest K/V list (rows) the copy-warp TMA instances take for one-block clips
 // (VINF_ATTN_CW_ROWS, diagnostics)
 static const uint32_t g_cw_rows = [] {
@@ -74,12 +73,11 @@ struct AttnMaps {
 };
 
 struct AttnArgs {
-    uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items, ns, frames, pos_major;
-    uint32_t load_only;  // diagnostics: consumers only wait for and release the stages (2: bulk feed)
-    uint32_t qfeed;      // D > 0 instances: 1 = Q rows by the copy warp (cp.async), 2 = + V chunks 1..
+    uint32_t HW, C, heads, d, nch, nq, nqb, q_frame0, items, ns;
+    uint32_t load_only;  // diagnostics: 1 = the feed alone (consumers only release stages), 3 = no loads
+    uint32_t qfeed;      // D > 0 instances: 1 = Q rows (and residual chunks) by the copy warp (cp.async)
     const __nv_bfloat16* q;     // the Q/K/V buffer (and its lo plane) for the copy warp
     const __nv_bfloat16* q_lo;
-    const uint8_t* diag_src;
     float scale, bias;
     __nv_bfloat16* ctx;
     int64_t ctx_lo;  // elements from ctx to its lo plane (split mode)
@@ -268,50 +266,35 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     // fused output through the ring (copy-warp instances): each PV stage carries one V chunk
     // (K slot) and the matching residual chunk of the block's queries (Q slot), the residual
     // loaded by the copy warp; the consumers add it from shared memory
-    const bool fr = D > 0 && !SPLIT && a.qfeed == 1 && a.fo.y != nullptr && a.fo.res_bf16 && a.load_only != 2;
+    const bool fr = D > 0 && !SPLIT && a.qfeed && a.fo.y != nullptr && a.fo.res_bf16;
     const uint32_t VPS = fr ? 1u : kVPS;
     const uint32_t nvs = (nch + VPS - 1) / VPS;
     const uint32_t dd = kFixed ? uint32_t(D) : a.d, CC = kFixed ? uint32_t(D) : a.C;
     if (D > 0 && warp == kConsumerWarps + 1) {
-        // ------ copy warp: the Q rows of every S-phase stage, V chunks 1.. of every PV stage ------
+        // ------ copy warp: the Q rows of every S-phase stage (and the residual chunks) ------
         // lane: 16-byte piece lane & 7 of rows lane >> 3, +4, ...; destination in the TMA
-        // 128B-swizzle order the consumers read; one arrival per lane per stage. The TMA
-        // producer keeps the K chunks and the first V chunk of a stage (half the rows each).
+        // 128B-swizzle order the consumers read; one arrival per lane per stage.
         if (!a.qfeed) return;
         Ring r(NS);
         const uint32_t piece = uint32_t(lane) & 7u, r0 = uint32_t(lane) >> 3;
-        const uint64_t rowlen = a.pos_major == 2 ? uint64_t(kDC) : 3ull * CC;
         for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x) {
             const uint32_t p = item / a.nqb, qb = item - p * a.nqb;
-            const uint32_t nqh = min(uint32_t(kQBlock), a.nq - qb * kQBlock);
-            const uint32_t qf = a.q_frame0 + qb * kQBlock;
-            // this lane's K/V frames (rows r0, r0 + 4, ... < R <= RP), read once per item
-            const uint32_t R = a.tt.kv_count[qb];
-            constexpr int kVF = int(RP) / 4;
-            uint32_t vfr[kVF];
-#pragma unroll
-            for (int k = 0; k < kVF; ++k) {
-                const uint32_t row = r0 + 4u * uint32_t(k);
-                vfr[k] = a.qfeed >= 2 && row < R ? a.tt.kv_frames[size_t(qb) * kKvMax + row] : 0u;
-            }
+            const uint32_t a0 = qb * kQBlock;
+            const uint32_t nqh = min(uint32_t(kQBlock), a.nq - a0);
             for (uint32_t h = 0; h < heads; ++h) {
                 for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
                     dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
                     uint64_t* bar = &full[r.slot];
-                    if (a.load_only >= 2) {
+                    if (a.load_only == 3) {  // diagnostics: the consumers alone
                         dev::mbar_arrive(bar);
                         continue;
                     }
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
-                    const uint32_t col = ch * kDC + piece * 8;
-                    const bool valid = col < dd;
-                    const uint32_t chunk = (h * dd) / kDC + ch;
+                    const bool valid = ch * kDC + piece * 8 < dd;
                     for (uint32_t row = r0; row < nqh; row += 4) {
-                        const uint32_t f = qf + row;
-                        const uint64_t grow = a.pos_major == 2 ? (uint64_t(p) * (3 * CC / kDC) + chunk) * a.frames + f
-                                              : a.pos_major   ? uint64_t(p) * a.frames + f
-                                                              : uint64_t(f) * a.HW + p;
-                        const uint64_t off = grow * rowlen + (a.pos_major == 2 ? piece * 8 : h * dd + (valid ? col : 0));
+                        // frame-major [frames][HW][3C]: query frame q_frame0 + a0 + row, position p
+                        const uint64_t off = (uint64_t(a.q_frame0 + a0 + row) * a.HW + p) * (3ull * CC) + h * dd +
+                                             (valid ? ch * kDC + piece * 8 : 0);
                         const uint32_t dst = st + swz(row, piece);
                         cp_async16(dst, a.q + off, valid);
                         if (SPLIT) cp_async16(dst + kQT, a.q_lo + off, valid);
@@ -321,42 +304,18 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                 for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
                     dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
                     uint64_t* bar = &full[r.slot];
-                    if (a.load_only >= 2) {
-                        dev::mbar_arrive(bar);
-                        continue;
-                    }
-                    const uint32_t n = min(VPS, nch - vs * VPS);
-                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
-                    if (fr) {  // residual chunk vs (bf16) of the block's query rows -> the Q slot
-                        const uint32_t a0 = qb * kQBlock;
+                    if (fr && a.load_only != 3) {  // residual chunk vs (bf16) of the block's query rows -> the Q slot
+                        const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                         const bool valid = vs * kDC + piece * 8 < dd;
                         for (uint32_t row = r0; row < nqh; row += 4)
                             cp_async16(st + swz(row, piece),
                                        static_cast<const __nv_bfloat16*>(a.fo.res) +
                                            (uint64_t(a0 + row) * a.HW + p) * CC + (valid ? vs * kDC + piece * 8 : 0),
                                        valid);
+                        cp_async_arrive(bar);
+                    } else {
+                        dev::mbar_arrive(bar);
                     }
-                    for (uint32_t i = 1; i < (a.qfeed >= 2 ? n : 1u); ++i) {
-                        const uint32_t ch = vs * VPS + i;
-                        const uint32_t col = ch * kDC + piece * 8;
-                        const bool valid = col < dd;
-                        const uint32_t chunk = (2 * CC + h * dd) / kDC + ch;
-#pragma unroll
-                        for (int k = 0; k < kVF; ++k) {
-                            const uint32_t row = r0 + 4u * uint32_t(k);
-                            if (row >= R) break;
-                            const uint32_t f = vfr[k];
-                            const uint64_t grow = a.pos_major == 2 ? (uint64_t(p) * (3 * CC / kDC) + chunk) * a.frames + f
-                                                  : a.pos_major   ? uint64_t(p) * a.frames + f
-                                                                  : uint64_t(f) * a.HW + p;
-                            const uint64_t off =
-                                grow * rowlen + (a.pos_major == 2 ? piece * 8 : 2 * CC + h * dd + (valid ? col : 0));
-                            const uint32_t dst = st + i * LL::PL * LL::KT + swz(row, piece);
-                            cp_async16(dst, a.q + off, valid);
-                            if (SPLIT) cp_async16(dst + LL::KT, a.q_lo + off, valid);
-                        }
-                    }
-                    cp_async_arrive(bar);
                 }
             }
         }
@@ -374,21 +333,11 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
             const uint32_t* prog = a.tt.kv_box + size_t(qb) * kKvMax;
             const uint32_t nqh = min(uint32_t(kQBlock), a.nq - qb * kQBlock);
             const int32_t qf = int32_t(a.q_frame0 + qb * kQBlock);
-            // Layouts of the Q/K/V buffer (a.pos_major): 0 = frame-major rows [frames][HW][3C],
-            // 1 = position-major rows [HW][frames][3C], 2 = chunked [HW][3C/64][frames][64]
-            // (the 64-channel chunk of a position's frames contiguous). box: `rows` frames from
-            // f0 of 64-wide chunk ch of (which, head h); gathers: 2-D row of frame f.
-            const uint32_t nchk = 3 * CC / kDC;
+            // box: `rows` frames from f0 of 64-wide chunk ch of (which, head h) at position p, over
+            // the frame-major [frames][HW][3 x heads][d] buffer; gathers: 2-D row f * HW + p
             auto box4 = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, uint32_t which, uint32_t h,
                             uint32_t ch, uint32_t f0) {
-                if (a.pos_major == 2)
-                    tma_load_4d(dst, map, bar, 0, int32_t(f0), int32_t((which * CC + h * dd) / kDC + ch), int32_t(p));
-                else
-                    tma_load_4d(dst, map, bar, int32_t(ch * kDC), int32_t(which * heads + h), int32_t(p), int32_t(f0));
-            };
-            auto grow = [&](uint32_t chunk, uint32_t f) {
-                return int32_t(a.pos_major == 2 ? (p * nchk + chunk) * a.frames + f
-                                                : (a.pos_major ? p * a.frames + f : f * a.HW + p));
+                tma_load_4d(dst, map, bar, int32_t(ch * kDC), int32_t(which * heads + h), int32_t(p), int32_t(f0));
             };
             // K or V chunk ch (which = 1 / 2) of head h into the stage at dst
             auto load_kv = [&](uint32_t dst, uint64_t* bar, uint32_t which, uint32_t h, uint32_t ch) {
@@ -398,34 +347,28 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     if (kind == uint32_t(kBoxGather4)) {
                         const uint32_t e1 = prog[b + 1], e2 = prog[b + 2];
                         b += 2;
-                        const uint32_t chunk = (which * CC + h * dd) / kDC + ch;
-                        const int32_t col = a.pos_major == 2 ? 0 : int32_t(which * CC + h * dd + ch * kDC);
+                        const int32_t col = int32_t(which * CC + h * dd + ch * kDC);
+                        auto gr = [&](uint32_t f) { return int32_t(f * a.HW + p); };
                         for (uint32_t pl = 0; pl < LL::PL; ++pl)
-                            dev::tma_gather4(dst + pl * LL::KT + row * 128u, &maps.g4[pl], bar, col,
-                                             grow(chunk, e & 0xFFFFu), grow(chunk, e1 & 0xFFFFu),
-                                             grow(chunk, e1 >> 16), grow(chunk, e2 & 0xFFFFu));
+                            dev::tma_gather4(dst + pl * LL::KT + row * 128u, &maps.g4[pl], bar, col, gr(e & 0xFFFFu),
+                                             gr(e1 & 0xFFFFu), gr(e1 >> 16), gr(e2 & 0xFFFFu));
                         continue;
                     }
                     for (uint32_t pl = 0; pl < LL::PL; ++pl)
                         box4(dst + pl * LL::KT + row * 128u, &maps.box[pl][kind], bar, which, h, ch, e & 0xFFFFu);
                 }
             };
+            const bool qtma = !(D > 0 && a.qfeed);  // Q rows by TMA here (else the copy warp)
             for (uint32_t h = 0; h < heads; ++h) {
                 for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {  // S phase: Q + K chunk
                     dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
                     uint64_t* bar = &full[r.slot];
-                    const bool qtma = !(D > 0 && a.qfeed) || a.load_only == 2;  // Q rows by TMA here
-                    if (a.load_only != 3) dev::mbar_arrive_expect_tx(bar, kvb + (qtma ? nqh * 128u * LL::PL : 0u));
-                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (a.load_only == 3) {  // diagnostics: no loads at all (the consumers alone)
                         dev::mbar_arrive(bar);
                         continue;
                     }
-                    if (a.load_only == 2) {  // diagnostics: the same bytes as one contiguous bulk copy
-                        dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + ch) % 40000) * 8192u, kvb + nqh * 128u * LL::PL,
-                                      bar);
-                        continue;
-                    }
+                    dev::mbar_arrive_expect_tx(bar, kvb + (qtma ? nqh * 128u * LL::PL : 0u));
+                    const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (a.fo.y && !fr && h == 0 && ch == 0) {  // fused output: the item's residual rows into L2
                         const uint32_t rb = CC * (a.fo.res_bf16 ? 2u : 4u);
                         const uint8_t* res = static_cast<const uint8_t*>(a.fo.res);
@@ -449,18 +392,13 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                         dev::mbar_arrive(bar);
                         continue;
                     }
-                    const uint32_t nt = (D > 0 && a.qfeed >= 2 && a.load_only != 2) ? 1u : n;  // chunks by TMA
-                    dev::mbar_arrive_expect_tx(bar, kvb * nt);
+                    dev::mbar_arrive_expect_tx(bar, kvb * n);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (fr) {  // the V chunk into the K slot (the copy warp fills the Q slot)
                         load_kv(st + LL::PL * kQT, bar, 2, h, vs);
                         continue;
                     }
-                    if (a.load_only == 2) {
-                        dev::bulk_g2s(st, a.diag_src + ((uint64_t(item) * 32 + 16 + vs) % 40000) * 8192u, kvb * n, bar);
-                        continue;
-                    }
-                    for (uint32_t i = 0; i < nt; ++i) load_kv(st + i * LL::PL * LL::KT, bar, 2, h, vs * VPS + i);
+                    for (uint32_t i = 0; i < n; ++i) load_kv(st + i * LL::PL * LL::KT, bar, 2, h, vs * VPS + i);
                 }
             }
         }
@@ -490,7 +428,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     const uint64_t ldc = CC;
     uint8_t* ost = sm + LL::ost + warp * LL::OST;
     Ring r(NS);
-    if (a.load_only == 1 || a.load_only == 2) {  // diagnostics: the producer's feed rate alone
+    if (a.load_only == 1) {  // diagnostics: the producer's feed rate alone
         for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x)
             for (uint32_t k = 0; k < heads * (nch + nvs); ++k, r.next()) {
                 dev::mbar_wait(&full[r.slot], r.phase);
@@ -876,7 +814,7 @@ int g_sms = 0;
 // {64 head-dim elements, 1 head, 1 position, kind + 1 frames}, 128-byte swizzle; head-dim
 // elements past d read as zero.
 int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames, uint32_t HW, uint32_t C,
-              uint32_t heads, int layout) {
+              uint32_t heads) {
     auto fn = get_encode_fn();
     if (!fn) return int(cudaErrorNotSupported);
     const uint32_t d = C / heads;
@@ -887,24 +825,11 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
                 m.box[pl][k] = m.box[0][k];
                 continue;
             }
-            // frame-major [frames][HW][3C] rows (position stride 3C, frame stride HW 3C),
-            // position-major [HW][frames][3C], or chunked [HW][3C/64][frames][64]
+            // frame-major [frames][HW][3C] rows (position stride 3C, frame stride HW 3C)
             const uint64_t row = uint64_t(C) * 3 * 2;
-            const bool chunked = layout == 2;
             cuuint64_t gdim[4] = {d, 3ull * heads, HW, frames};
-            cuuint64_t gstride[3] = {uint64_t(d) * 2, layout ? row * frames : row, layout ? row : row * HW};
+            cuuint64_t gstride[3] = {uint64_t(d) * 2, row, row * HW};
             cuuint32_t box[4] = {uint32_t(kDC), 1, 1, uint32_t(k) + 1};
-            if (chunked) {
-                gdim[0] = kDC;
-                gdim[1] = frames;
-                gdim[2] = 3ull * C / kDC;
-                gdim[3] = HW;
-                gstride[0] = kDC * 2;
-                gstride[1] = uint64_t(frames) * kDC * 2;
-                gstride[2] = (3ull * C / kDC) * frames * kDC * 2;
-                box[1] = uint32_t(k) + 1;
-                box[3] = 1;
-            }
             cuuint32_t estride[4] = {1, 1, 1, 1};
             const CUresult r = fn(&m.box[pl][k], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), gdim,
                                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -915,9 +840,8 @@ int make_maps(AttnMaps& m, const void* qkv, const void* qkv_lo, uint32_t frames,
             m.g4[pl] = m.g4[0];
             continue;
         }
-        cuuint64_t gdim[2] = {layout == 2 ? uint64_t(kDC) : 3ull * C, layout == 2 ? 3ull * C / kDC * HW * frames
-                                                                                 : uint64_t(HW) * frames};
-        cuuint64_t gstride[1] = {layout == 2 ? uint64_t(kDC) * 2 : uint64_t(C) * 3 * 2};
+        cuuint64_t gdim[2] = {3ull * C, uint64_t(HW) * frames};
+        cuuint64_t gstride[1] = {uint64_t(C) * 3 * 2};
         cuuint32_t box[2] = {uint32_t(kDC), 1};
         cuuint32_t estride[2] = {1, 1};
         const CUresult r = fn(&m.g4[pl], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
@@ -958,42 +882,33 @@ int launch_core(const AttnMaps& maps, AttnArgs args, cudaStream_t s) {
     const uint32_t grid = args.items < slots ? args.items : slots;
     static const uint32_t qfeed = [] {
         const char* e = getenv("VINF_ATTN_QFEED");
-        return e ? uint32_t(atoi(e)) : 1u;  // 0 = all by TMA, 1 = Q rows, 2 = Q rows + V chunks 1..
+        return e ? uint32_t(atoi(e) != 0) : 1u;  // 0 = all by TMA, 1 = Q rows by the copy warp
     }();
     args.qfeed = D > 0 ? qfeed : 0u;
     return int(launch_pdl(attention_core_kernel<NTL, SPLIT, CW, D>, dim3(grid), dim3(LL::kThreads + (D > 0 ? 32 : 0)),
                           LL::total(int(args.ns)) + tab, s, maps, args));
 }
 
-// consumer warps per CTA: 4 (VINF_ATTN_WARPS=8 selects 8: measured no faster, at 2 CTAs per
-// SM, on the cfg2 and 288-frame shapes: profiles/r02_attn/warps_ctas.txt)
+// four consumer warps per CTA (eight, at 2 CTAs per SM, measured slower on the cfg2 and
+// 288-frame shapes and with the fused output: profiles/r02_attn/warps_ctas.txt; removed)
 template <int NTL, bool SPLIT>
 int launch_ntl(const AttnMaps& maps, const AttnArgs& args, cudaStream_t s) {
-    static const int env_w = [] {
-        const char* e = getenv("VINF_ATTN_WARPS");
-        return e ? atoi(e) : 0;
-    }();
-    const int cw = env_w == 8 ? 8 : 4;
-    // one head with the head dim of a VideoCrafter2 level: compile-time chunk loops
-    // (a fused output goes through the ring only with the Q copy warp: otherwise the generic
-    // instance, whose consumers load the residual themselves)
-    static const bool ring_fuse = [] {
+    // one head with the head dim of a VideoCrafter2 level: compile-time chunk loops and the
+    // copy warp (a fused output goes through the ring only with the copy warp: without it,
+    // VINF_ATTN_QFEED=0, the generic instance, whose consumers load the residual themselves)
+    static const bool qfeed = [] {
         const char* q = getenv("VINF_ATTN_QFEED");
-        const char* l = getenv("VINF_ATTN_LOAD_ONLY");
-        return (!q || atoi(q) == 1) && (!l || atoi(l) != 2);
+        return !q || atoi(q) != 0;
     }();
     if constexpr (NTL <= 8 && !SPLIT) {
-        if (args.heads == 1 && (!args.fo.y || (ring_fuse && args.fo.res_bf16))) switch (args.d) {
-                case 320: return cw == 8 ? launch_core<NTL, SPLIT, 8, 320>(maps, args, s)
-                                         : launch_core<NTL, SPLIT, 4, 320>(maps, args, s);
-                case 640: return cw == 8 ? launch_core<NTL, SPLIT, 8, 640>(maps, args, s)
-                                         : launch_core<NTL, SPLIT, 4, 640>(maps, args, s);
-                case 1280: return cw == 8 ? launch_core<NTL, SPLIT, 8, 1280>(maps, args, s)
-                                          : launch_core<NTL, SPLIT, 4, 1280>(maps, args, s);
+        if (args.heads == 1 && (!args.fo.y || (qfeed && args.fo.res_bf16))) switch (args.d) {
+                case 320: return launch_core<NTL, SPLIT, 4, 320>(maps, args, s);
+                case 640: return launch_core<NTL, SPLIT, 4, 640>(maps, args, s);
+                case 1280: return launch_core<NTL, SPLIT, 4, 1280>(maps, args, s);
                 default: break;
             }
     }
-    return cw == 8 ? launch_core<NTL, SPLIT, 8, 0>(maps, args, s) : launch_core<NTL, SPLIT, 4, 0>(maps, args, s);
+    return launch_core<NTL, SPLIT, 4, 0>(maps, args, s);
 }
 
 template <bool SPLIT>
@@ -1042,8 +957,7 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     if (impl == 2)
         return launch_attention_core_cpasync(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s,
                                              fo);
-    if (g_attn_pos_major == 2 && (C % kDC || (C / heads) % kDC)) return int(cudaErrorInvalidValue);
-    // 66 tensor maps per buffer: encoded once per (buffer, shape, layout), then reused
+    // 66 tensor maps per buffer: encoded once per (buffer, shape), then reused
     struct Cached {
         const void *q = nullptr, *ql = nullptr;
         uint32_t frames = 0, HW = 0, C = 0, heads = 0;
@@ -1060,13 +974,13 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
         for (int i = 0; i < 8; ++i) {
             const Cached& c = cache[i];
             if (c.q == qkv && c.ql == qkv_lo && c.frames == qkv_frames && c.HW == HW && c.C == C && c.heads == heads &&
-                c.layout == g_attn_pos_major)
+                true)
                 hit = i;
         }
         if (hit < 0) {
             Cached& c = cache[cache_next];
             c.layout = -1;
-            const int rc = make_maps(c.maps, qkv, qkv_lo, qkv_frames, HW, C, heads, g_attn_pos_major);
+            const int rc = make_maps(c.maps, qkv, qkv_lo, qkv_frames, HW, C, heads);
             if (rc) return rc;
             c.q = qkv;
             c.ql = qkv_lo;
@@ -1074,7 +988,7 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
             c.HW = HW;
             c.C = C;
             c.heads = heads;
-            c.layout = g_attn_pos_major;
+            c.layout = 0;
             hit = cache_next;
             cache_next = (cache_next + 1) % 8;
         }
@@ -1090,11 +1004,8 @@ int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_fram
     args.nqb = (nq + kQBlock - 1) / kQBlock;
     args.q_frame0 = q_frame0;
     args.items = HW * args.nqb;
-    args.frames = qkv_frames;
-    args.pos_major = uint32_t(g_attn_pos_major);
     static const uint32_t load_only = getenv("VINF_ATTN_LOAD_ONLY") ? uint32_t(atoi(getenv("VINF_ATTN_LOAD_ONLY"))) : 0u;
     args.load_only = load_only;
-    args.diag_src = static_cast<const uint8_t*>(qkv);  // load-only 2: reads within the first 320 MB
     args.q = static_cast<const __nv_bfloat16*>(qkv);
     args.q_lo = static_cast<const __nv_bfloat16*>(qkv_lo);
     args.scale = scale;

@@ -44,12 +44,13 @@ int vinf_debug_attention_impl(int impl) {
 }
 
 // The attention core alone over the Q/K/V buffer of a single-worker engine layout
-// (t > t_star token table), average ms over iters launches; pos_major = 1 views the
-// buffer as [HW][frames][3C] instead of [frames][HW][3C].
+// (t > t_star token table), average ms over iters launches; pos_major must be 0 (the
+// frame-major [frames][HW][3C] buffer; the other layouts were measured and removed).
 int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint32_t channels, uint32_t heads,
                          uint32_t n_local, uint32_t n_global, int f32, int pos_major, int iters, float* ms) {
     return guarded_call([&] {
         if (!ms || iters <= 0) shape_error("bad arguments");
+        if (pos_major) shape_error("pos_major: only the frame-major layout is built (DESIGN.md section 3)");
         vinf_engine_desc d{};
         d.frames = frames;
         d.workers = 1;
@@ -95,7 +96,6 @@ int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint3
         }
         auto* q = static_cast<__nv_bfloat16*>(qkv.p);
         auto* c = static_cast<__nv_bfloat16*>(ctx.p);
-        g_attn_pos_major = pos_major;
         auto launch = [&] {
             cuda_check(launch_attention_core(q, f32 ? q + plane : nullptr, L.af, L.hw, channels, heads, L.f_clip,
                                              L.ha, tok.tt, L.scale, d.bias, c, f32 ? c + ctxn : nullptr, s, &fo),
@@ -113,7 +113,6 @@ int vinf_attention_bench(uint32_t frames, uint32_t height, uint32_t width, uint3
         *ms /= float(iters);
         cudaEventDestroy(a);
         cudaEventDestroy(b);
-        g_attn_pos_major = 0;
         }
         cuda_check(cudaStreamSynchronize(s), "sync");
         tok.release();

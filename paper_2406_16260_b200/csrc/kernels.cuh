@@ -197,8 +197,6 @@ int launch_attention_core_cpasync(const void* qkv, const void* qkv_lo, uint32_t 
 // Which implementation launch_attention_core uses: 0 = by configuration, 1 = the TMA ring,
 // 2 = the cp.async ring (VINF_ATTN_IMPL=tma|cpasync, vinf_debug_attention_impl).
 extern int g_attn_impl;
-// Diagnostics knob: 1 = the qkv buffer is position-major [HW][frames][3C].
-extern int g_attn_pos_major;
 // qkv_frames: frames of the qkv buffer (the TMA tensor maps' outer extent). fo: fused output
 // (null or fo->y null: ctx is written).
 int launch_attention_core(const void* qkv, const void* qkv_lo, uint32_t qkv_frames, uint32_t HW, uint32_t C,
