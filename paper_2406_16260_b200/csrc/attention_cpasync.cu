@@ -308,84 +308,143 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
             }
         }
         __syncthreads();
-        // ---------------- softmax over the token lists, per column -> P (in place) ----------
-        // The reference's token list (window, then globals, duplicates kept; ops.cpp:209-241)
-        // in column form: column c carries the window token iff wlo <= c <= whi and gmult[c]
-        // global tokens; p_c = [window] e^(l_w - m) + gmult[c] e^(l_g - m), summed one token
-        // at a time. Lane l owns columns l + 32k: no token-list walk, no smem atomics.
-        for (uint32_t a = warp; a < uint32_t(kQBlock); a += kWarps) {
-            float* row = sp + a * SP;
-            float pv[KC];
-            float zi = 0.f;
-#pragma unroll
-            for (int k = 0; k < KC; ++k) pv[k] = 0.f;
-            if (a < nqh) {
-                const uint32_t qa = a0 + a;
+        if constexpr (RP == 64) {
+            // 64-column tiles (long clips): eight threads per row, eight columns each (three
+            // shuffle steps per reduction), P written straight to its bf16 planes
+            const uint32_t r = uint32_t(tid) >> 3, oct = uint32_t(tid) & 7u;
+            uint32_t w[4], wl[4];
+            if (r < nqh) {
+                const uint32_t qa = a0 + r;
                 const int lo = tt.wlo[qa], hi = tt.whi[qa];
                 const uint8_t* gm = tt.gmult + size_t(qb) * kKvMax;
                 const float bw = tt.wflag ? bias : 0.f, bg = tt.gflag ? bias : 0.f;
-                float sv[KC];
-                bool inw[KC];
-                int ng[KC];
-                float m = -INFINITY;
+                const float4 s0 = *reinterpret_cast<const float4*>(sp + r * SP + oct * 8);
+                const float4 s1 = *reinterpret_cast<const float4*>(sp + r * SP + oct * 8 + 4);
+                const float sr[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                float sv[8], m = -INFINITY;
+                bool inw[8];
+                int ng[8];
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    const int c = lane + 32 * k;
+                for (int k = 0; k < 8; ++k) {
+                    const int c = int(oct) * 8 + k;
                     const bool ok = c < int(R);
-                    sv[k] = ok ? scale * row[c] : 0.f;
+                    sv[k] = ok ? scale * sr[k] : 0.f;
                     inw[k] = ok && c >= lo && c <= hi;
                     ng[k] = ok ? gm[c] : 0;
                     if (inw[k]) m = fmaxf(m, sv[k] + bw);
                     if (ng[k]) m = fmaxf(m, sv[k] + bg);
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                float z = 0.f;
+                for (int o = 1; o < 8; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                float e[8], z = 0.f;
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    float e = inw[k] ? expf(sv[k] + bw - m) : 0.f;
-                    if (ng[k]) {
-                        const float eg = expf(sv[k] + bg - m);
-                        for (int t = 0; t < ng[k]; ++t) e += eg;
-                    }
-                    pv[k] = e;
-                    z += e;
+                for (int k = 0; k < 8; ++k) {
+                    e[k] = inw[k] ? (SPLIT ? expf(sv[k] + bw - m) : __expf(sv[k] + bw - m)) : 0.f;
+                    if (ng[k]) e[k] += float(ng[k]) * (SPLIT ? expf(sv[k] + bg - m) : __expf(sv[k] + bg - m));
+                    z += e[k];
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-                zi = 1.0f / z;
-            }
-            __syncwarp();
+                for (int o = 1; o < 8; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+                const float zi = 1.0f / z;
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const int c = lane + 32 * k;
-                if (c < SP) row[c] = pv[k];
-            }
-            if (lane < SP - 32 * KC) row[32 * KC + lane] = 0.f;
-            if (lane == 0) zinv[a] = zi;
-        }
-        __syncthreads();
-        // P = S_normalised -> bf16 planes (64-column blocks in the swizzled row layout)
-        for (int i = tid; i < int(kQBlock * RP / 8); i += kThreads) {
-            const uint32_t r = i / (RP / 8), c8 = i % (RP / 8);
-            const float zi = zinv[r];
-            const float4 s0 = *reinterpret_cast<const float4*>(sp + r * SP + c8 * 8);
-            const float4 s1 = *reinterpret_cast<const float4*>(sp + r * SP + c8 * 8 + 4);
-            const float v[8] = {s0.x * zi, s0.y * zi, s0.z * zi, s0.w * zi,
-                                s1.x * zi, s1.y * zi, s1.z * zi, s1.w * zi};
-            const uint32_t off = LL::pb + (c8 >> 3) * (kQBlock * 128) + swz(r, c8 & 7);
-            uint32_t w[4], wl[4];
+                for (int k = 0; k < 4; ++k) {
+                    if (SPLIT)
+                        split2(e[2 * k] * zi, e[2 * k + 1] * zi, w[k], wl[k]);
+                    else
+                        w[k] = pack_bf16(e[2 * k] * zi, e[2 * k + 1] * zi);
+                }
+            } else {
+                // rows past the block: P = 0, the octet's shuffles kept converged
+                float m = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (SPLIT)
-                    split2(v[2 * k], v[2 * k + 1], w[k], wl[k]);
-                else
-                    w[k] = pack_bf16(v[2 * k], v[2 * k + 1]);
+                for (int o = 1; o < 8; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) w[k] = wl[k] = 0u;
             }
+            const uint32_t off = LL::pb + swz(r, oct);
             *reinterpret_cast<uint4*>(sm + off) = make_uint4(w[0], w[1], w[2], w[3]);
             if (SPLIT) *reinterpret_cast<uint4*>(sm + off + LL::PB) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+            __syncthreads();
+        } else {
+        // ---------------- softmax over the token lists, per column -> P (in place) ----------
+            // The reference's token list (window, then globals, duplicates kept; ops.cpp:209-241)
+            // in column form: column c carries the window token iff wlo <= c <= whi and gmult[c]
+            // global tokens; p_c = [window] e^(l_w - m) + gmult[c] e^(l_g - m), summed one token
+            // at a time. Lane l owns columns l + 32k: no token-list walk, no smem atomics.
+            for (uint32_t a = warp; a < uint32_t(kQBlock); a += kWarps) {
+                float* row = sp + a * SP;
+                float pv[KC];
+                float zi = 0.f;
+    #pragma unroll
+                for (int k = 0; k < KC; ++k) pv[k] = 0.f;
+                if (a < nqh) {
+                    const uint32_t qa = a0 + a;
+                    const int lo = tt.wlo[qa], hi = tt.whi[qa];
+                    const uint8_t* gm = tt.gmult + size_t(qb) * kKvMax;
+                    const float bw = tt.wflag ? bias : 0.f, bg = tt.gflag ? bias : 0.f;
+                    float sv[KC];
+                    bool inw[KC];
+                    int ng[KC];
+                    float m = -INFINITY;
+    #pragma unroll
+                    for (int k = 0; k < KC; ++k) {
+                        const int c = lane + 32 * k;
+                        const bool ok = c < int(R);
+                        sv[k] = ok ? scale * row[c] : 0.f;
+                        inw[k] = ok && c >= lo && c <= hi;
+                        ng[k] = ok ? gm[c] : 0;
+                        if (inw[k]) m = fmaxf(m, sv[k] + bw);
+                        if (ng[k]) m = fmaxf(m, sv[k] + bg);
+                    }
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    float z = 0.f;
+    #pragma unroll
+                    for (int k = 0; k < KC; ++k) {
+                        // (the column's ng[k] global tokens as one product: bf16 mode in the fast exp)
+                        float e = inw[k] ? (SPLIT ? expf(sv[k] + bw - m) : __expf(sv[k] + bw - m)) : 0.f;
+                        if (ng[k]) e += float(ng[k]) * (SPLIT ? expf(sv[k] + bg - m) : __expf(sv[k] + bg - m));
+                        pv[k] = e;
+                        z += e;
+                    }
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+                    zi = 1.0f / z;
+                }
+                __syncwarp();
+    #pragma unroll
+                for (int k = 0; k < KC; ++k) {
+                    const int c = lane + 32 * k;
+                    if (c < SP) row[c] = pv[k];
+                }
+                if (lane < SP - 32 * KC) row[32 * KC + lane] = 0.f;
+                if (lane == 0) zinv[a] = zi;
+            }
+            __syncthreads();
+            // P = S_normalised -> bf16 planes (64-column blocks in the swizzled row layout)
+            for (int i = tid; i < int(kQBlock * RP / 8); i += kThreads) {
+                const uint32_t r = i / (RP / 8), c8 = i % (RP / 8);
+                const float zi = zinv[r];
+                const float4 s0 = *reinterpret_cast<const float4*>(sp + r * SP + c8 * 8);
+                const float4 s1 = *reinterpret_cast<const float4*>(sp + r * SP + c8 * 8 + 4);
+                const float v[8] = {s0.x * zi, s0.y * zi, s0.z * zi, s0.w * zi,
+                                    s1.x * zi, s1.y * zi, s1.z * zi, s1.w * zi};
+                const uint32_t off = LL::pb + (c8 >> 3) * (kQBlock * 128) + swz(r, c8 & 7);
+                uint32_t w[4], wl[4];
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (SPLIT)
+                        split2(v[2 * k], v[2 * k + 1], w[k], wl[k]);
+                    else
+                        w[k] = pack_bf16(v[2 * k], v[2 * k + 1]);
+                }
+                *reinterpret_cast<uint4*>(sm + off) = make_uint4(w[0], w[1], w[2], w[3]);
+                if (SPLIT) *reinterpret_cast<uint4*>(sm + off + LL::PB) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         // ---------------- ctx = P V ----------------
         // warp: m tile mt, n8 tiles 2wq, 2wq + 1 of each 64-wide output chunk
         uint32_t pa[LL::PREG ? NTL / 2 : 1][4], pal[LL::PREG && SPLIT ? NTL / 2 : 1][4];
