@@ -113,11 +113,13 @@ struct CoreLay {
     static constexpr int blocks = int(kSmemPerSm / (total + 1024)) > 4 ? 4 : int(kSmemPerSm / (total + 1024));
 };
 
-template <int NTL, int NS, bool SPLIT>
+// D > 0: one head with head dim D fixed at compile time (the VideoCrafter2 levels' long clips)
+template <int NTL, int NS, bool SPLIT, int D = 0>
 __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
-    attention_core_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_lo, uint32_t HW, uint32_t C,
-                          uint32_t heads, uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale,
+    attention_core_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_lo, uint32_t HW, uint32_t C_,
+                          uint32_t heads_, uint32_t nq, uint32_t q_frame0, TokenTable tt, float scale,
                           float bias, __nv_bfloat16* __restrict__ ctx, int64_t ctx_lo, const FuseO fo) {
+    const uint32_t C = D > 0 ? uint32_t(D) : C_, heads = D > 0 ? 1u : heads_;
     dev::pdl_wait();
     dev::pdl_trigger();
     using LL = CoreLay<NTL, NS, SPLIT>;
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
     const uint32_t a0 = qb * kQBlock;
     const uint32_t nqh = min(uint32_t(kQBlock), nq - a0);
     const uint32_t R = tt.kv_count[qb];
-    const uint32_t d = C / heads, nch = (d + kDC - 1) / kDC;
+    const uint32_t d = D > 0 ? uint32_t(D) : C / heads, nch = (d + kDC - 1) / kDC;
     const uint64_t ld = 3ull * C;
     const uint32_t sbase = dev::smem_u32(sm);
     float* sp = reinterpret_cast<float*>(sm + LL::sp);
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, CoreLay<NTL, NS, SPLIT>::blocks)
     cp_wait<0>();
 }
 
-template <int NTL, int NS, bool SPLIT>
+template <int NTL, int NS, bool SPLIT, int D = 0>
 int launch_core(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_t heads, uint32_t nq,
                 uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
                 cudaStream_t s, const FuseO& fo) {
@@ -529,13 +531,13 @@ int launch_core(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32
     static_assert(LL::total <= 227 * 1024, "attention core shared memory");
     static bool attr = false;
     if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, NS, SPLIT>,
+        const cudaError_t e = cudaFuncSetAttribute(attention_core_kernel<NTL, NS, SPLIT, D>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(LL::total));
         if (e != cudaSuccess) return int(e);
         attr = true;
     }
     dim3 grid(HW * ((nq + kQBlock - 1) / kQBlock));
-    return int(launch_pdl(attention_core_kernel<NTL, NS, SPLIT>, grid, dim3(kThreads), LL::total, s,
+    return int(launch_pdl(attention_core_kernel<NTL, NS, SPLIT, D>, grid, dim3(kThreads), LL::total, s,
                           static_cast<const __nv_bfloat16*>(qkv), qkv_lo, HW, C, heads, nq, q_frame0, tt,
                           scale, bias, static_cast<__nv_bfloat16*>(ctx), ctx_lo, fo));
 }
@@ -547,6 +549,14 @@ int launch_ntl(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_
                uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
                cudaStream_t s, const FuseO& fo) {
     constexpr int NS = NTL <= 4 ? 5 : (NTL <= 8 ? 4 : (SPLIT ? 2 : 3));
+    if constexpr (!SPLIT && (NTL == 6 || NTL == 8)) {  // the long clips' 48/64-row tiles
+        if (heads == 1) switch (C) {
+                case 320: return launch_core<NTL, NS, SPLIT, 320>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
+                case 640: return launch_core<NTL, NS, SPLIT, 640>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
+                case 1280: return launch_core<NTL, NS, SPLIT, 1280>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
+                default: break;
+            }
+    }
     return launch_core<NTL, NS, SPLIT>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
 }
 
