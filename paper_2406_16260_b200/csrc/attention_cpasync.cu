@@ -549,7 +549,8 @@ int launch_ntl(const void* qkv, int64_t qkv_lo, uint32_t HW, uint32_t C, uint32_
                uint32_t q_frame0, const TokenTable& tt, float scale, float bias, void* ctx, int64_t ctx_lo,
                cudaStream_t s, const FuseO& fo) {
     constexpr int NS = NTL <= 4 ? 5 : (NTL <= 8 ? 4 : (SPLIT ? 2 : 3));
-    if constexpr (!SPLIT && (NTL == 6 || NTL == 8)) {  // the long clips' 48/64-row tiles
+    // the long clips' 48/64-row tiles (bf16), and the fp32 mode's tiles up to 64 rows
+    if constexpr ((!SPLIT && (NTL == 6 || NTL == 8)) || (SPLIT && NTL <= 8)) {
         if (heads == 1) switch (C) {
                 case 320: return launch_core<NTL, NS, SPLIT, 320>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
                 case 640: return launch_core<NTL, NS, SPLIT, 640>(qkv, qkv_lo, HW, C, heads, nq, q_frame0, tt, scale, bias, ctx, ctx_lo, s, fo);
