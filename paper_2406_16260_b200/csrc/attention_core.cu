@@ -58,7 +58,7 @@ int g_attn_impl = []() {  // 0 = by configuration, 1 = TMA ring, 2 = cp.async ri
 namespace {
 
 constexpr int kDC = 64;  // head-dim chunk (one 128-byte swizzle row of bf16)
-// CW consumer warps per CTA (4 or 8) + one producer warp; derived tile constants:
+// CW consumer warps per CTA (4 in every instance) + one producer warp; derived tile constants:
 #define VINF_ATTN_WARP_CONSTANTS(CW)                                                         \
     static constexpr int kConsumerWarps = CW;                                                  \
     static constexpr int kThreads = (kConsumerWarps + 1) * 32; /* + the producer warp */      \
@@ -169,7 +169,7 @@ struct CoreLay {
     static constexpr uint32_t scratch = (kQBlock * SP * 4 + PL * PB + kConsumerWarps * OST + 127) / 128 * 128;
     // as many CTAs per SM (up to 4) as leave a ring of >= 4 stages each
     static constexpr int pick_ctas() {
-        for (int c = CW == 8 ? 2 : 4; c > 1; --c)  // 8 consumer warps: registers allow 2
+        for (int c = 4; c > 1; --c)
             if (c * (scratch + 4 * ST + 2048) <= 226u * 1024u) return c;
         return 1;
     }
