@@ -63,6 +63,27 @@ def test_native_executor_equals_stage_loop(en, oracle, dtype, n):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n,Ch", [(2, 640), (4, 320)])
+def test_native_executor_worker_tiles(en, oracle, dtype, n, Ch):
+    # 24 frames per worker at VideoCrafter2 channel counts: the copy-warp TMA instances with
+    # the O projection absorbed (bf16) under the C++ executor and graph replay, bitwise equal
+    # to the stage loop and within the bar of the oracle
+    F, H, W = 24 * n, 2, 4
+    x = oracle.tensor_from_seed((F, H, W, Ch), 4)
+    a = build(en, x, n, dtype, n_local=16, n_global=16, groups=32)
+    en.forward(900.0, a, en.LocalGroup())
+    b = build(en, x, n, dtype, n_local=16, n_global=16, groups=32)
+    g = native(en, b)
+    en.forward(900.0, b, g)
+    en.forward(900.0, b, g)  # second call replays the captured graph
+    assert torch.equal(out(a), out(b))
+    bp = oracle.build_block(Ch, 3, weight_seed=1)
+    want = oracle.block_forward(x, bp, 900.0, 32)
+    tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
+    assert normwise(out(b).numpy(), want) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_native_executor_uneven_two_blocks(en, dtype):
     from oracle.oracle import Oracle
     x = Oracle().tensor_from_seed((50, 2, 8, 64), 4)
