@@ -118,6 +118,11 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
 __device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
+__device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0), "r"(r1),
+                 "r"(r2), "r"(r3)
+                 : "memory");
+}
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -490,6 +495,17 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     uint32_t qa[4], ql[4];
                     ldsm_x4(st + a_off[kk], qa);
                     if (SPLIT) ldsm_x4(st + kQT + a_off[kk], ql);
+                    if constexpr (!SPLIT && NJ % 2 == 0 && NTL == NJ * kWQ) {
+                        // two n8 key tiles per ldmatrix.x4 (lanes 16-31 address the second)
+#pragma unroll
+                        for (int j = 0; j < NJ; j += 2) {
+                            uint32_t kf[4];
+                            ldsm_x4(st + b_off[kk] + (wq + kWQ * (j + int(hb))) * 1024, kf);
+                            mma_bf16(acc[j][NA == 2 ? (kk & 1) : 0], qa, kf[0], kf[1]);
+                            mma_bf16(acc[j + 1][NA == 2 ? (kk & 1) : 0], qa, kf[2], kf[3]);
+                        }
+                        continue;
+                    }
 #pragma unroll
                     for (int j = 0; j < NJ; ++j) {
                         if (wq + kWQ * j < NTL) {
@@ -720,7 +736,18 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                                 }
                             }
                         }
-                        // accumulators -> staging [16 rows][kON*8 cols] (bf16; lo plane after it)
+                        // accumulators -> staging [16 rows][kON*8 cols] (bf16; lo plane after it);
+                        // bf16 mode: two n8 tiles per stmatrix.x4
+                        if constexpr (!SPLIT && kON % 2 == 0) {
+                            const uint32_t mrow = ((uint32_t(lane) >> 3) & 1u) * 8u + (uint32_t(lane) & 7u);
+#pragma unroll
+                            for (int nn = 0; nn < kON; nn += 2) {
+                                const uint32_t addr = dev::smem_u32(ost) + mrow * kOPitch +
+                                                      uint32_t(nn + int(uint32_t(lane) >> 4)) * 16u;
+                                stsm_x4(addr, pack_bf16(o[nn][0], o[nn][1]), pack_bf16(o[nn][2], o[nn][3]),
+                                        pack_bf16(o[nn + 1][0], o[nn + 1][1]), pack_bf16(o[nn + 1][2], o[nn + 1][3]));
+                            }
+                        } else
 #pragma unroll
                         for (int nn = 0; nn < kON; ++nn) {
                             const uint32_t o0 = uint32_t(g) * kOPitch + (nn * 8 + t4 * 2) * 2, o1 = o0 + 8 * kOPitch;
