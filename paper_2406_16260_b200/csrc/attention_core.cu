@@ -118,6 +118,15 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
 __device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
+// v0, v1 += x0 * s0 + t0, x1 * s1 + t1 on the packed fp32 pipe (FFMA2 / FADD2)
+__device__ __forceinline__ void fma2_acc(float& v0, float& v1, float x0, float x1, float s0, float s1, float t0,
+                                         float t1) {
+    asm("{\n.reg .b64 X, S, T, V;\n"
+        "mov.b64 X, {%2, %3};\nmov.b64 S, {%4, %5};\nmov.b64 T, {%6, %7};\nmov.b64 V, {%0, %1};\n"
+        "fma.rn.f32x2 T, X, S, T;\nadd.rn.f32x2 V, V, T;\nmov.b64 {%0, %1}, V;\n}"
+        : "+f"(v0), "+f"(v1)
+        : "f"(x0), "f"(x1), "f"(s0), "f"(s1), "f"(t0), "f"(t1));
+}
 __device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
     asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0), "r"(r1),
                  "r"(r2), "r"(r3)
@@ -804,8 +813,8 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
 #pragma unroll
                                             for (int k = 0; k < 4; ++k) {
                                                 const float2 x = __bfloat1622float2(u2[k]);
-                                                v[2 * k] += x.x * ssc[2 * k] + tsc[2 * k];
-                                                v[2 * k + 1] += x.y * ssc[2 * k + 1] + tsc[2 * k + 1];
+                                                fma2_acc(v[2 * k], v[2 * k + 1], x.x, x.y, ssc[2 * k], ssc[2 * k + 1],
+                                                         tsc[2 * k], tsc[2 * k + 1]);
                                             }
                                         } else {
                                             fuse_o_add_bf16(a.fo, u, ch * kDC + col, v);
