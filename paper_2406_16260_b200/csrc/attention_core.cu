@@ -91,12 +91,12 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
     return row * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
                                             int32_t c1, int32_t c2, int32_t c3) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(dev::smem_u32(bar))
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
         : "memory");
 }
 
@@ -106,8 +106,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
                  : "memory");
 }
 // arrives on the mbarrier once this thread's earlier cp.async copies have landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(dev::smem_u32(bar)) : "memory");
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -248,6 +248,8 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     const uint32_t sbase = dev::smem_u32(sm);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + LL::bars(int(NS)));
     uint64_t* empty = full + NS;
+    // the ring's barriers as shared-space addresses (slot s at + 8 s)
+    const uint32_t fa = dev::smem_u32(full), ea = fa + 8u * NS;
     float* sp = reinterpret_cast<float*>(sm + LL::sp);
 
     // zero the ring and scratch once: rows no load of an item writes (K/V padding rows, Q rows
@@ -297,10 +299,10 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
             const uint32_t nqh = min(uint32_t(kQBlock), a.nq - a0);
             for (uint32_t h = 0; h < heads; ++h) {
                 for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
-                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
-                    uint64_t* bar = &full[r.slot];
+                    dev::mbar_wait_a(ea + 8u * r.slot, r.phase ^ 1u);
+                    const uint32_t bar = fa + 8u * r.slot;
                     if (a.load_only == 3) {  // diagnostics: the consumers alone
-                        dev::mbar_arrive(bar);
+                        dev::mbar_arrive_a(bar);
                         continue;
                     }
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
@@ -316,8 +318,8 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     cp_async_arrive(bar);
                 }
                 for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
-                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
-                    uint64_t* bar = &full[r.slot];
+                    dev::mbar_wait_a(ea + 8u * r.slot, r.phase ^ 1u);
+                    const uint32_t bar = fa + 8u * r.slot;
                     if (fr && a.load_only != 3) {  // residual chunk vs (bf16) of the block's query rows -> the Q slot
                         const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                         const bool valid = vs * kDC + piece * 8 < dd;
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                                        valid);
                         cp_async_arrive(bar);
                     } else {
-                        dev::mbar_arrive(bar);
+                        dev::mbar_arrive_a(bar);
                     }
                 }
             }
@@ -349,12 +351,12 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
             const int32_t qf = int32_t(a.q_frame0 + qb * kQBlock);
             // box: `rows` frames from f0 of 64-wide chunk ch of (which, head h) at position p, over
             // the frame-major [frames][HW][3 x heads][d] buffer; gathers: 2-D row f * HW + p
-            auto box4 = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, uint32_t which, uint32_t h,
+            auto box4 = [&](uint32_t dst, const CUtensorMap* map, uint32_t bar, uint32_t which, uint32_t h,
                             uint32_t ch, uint32_t f0) {
                 tma_load_4d(dst, map, bar, int32_t(ch * kDC), int32_t(which * heads + h), int32_t(p), int32_t(f0));
             };
             // K or V chunk ch (which = 1 / 2) of head h into the stage at dst
-            auto load_kv = [&](uint32_t dst, uint64_t* bar, uint32_t which, uint32_t h, uint32_t ch) {
+            auto load_kv = [&](uint32_t dst, uint32_t bar, uint32_t which, uint32_t h, uint32_t ch) {
                 for (uint32_t b = 0; b < nb; ++b) {
                     const uint32_t e = prog[b];
                     const uint32_t row = (e >> 16) & 0xFFu, kind = e >> 24;
@@ -375,13 +377,13 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
             const bool qtma = !(D > 0 && a.qfeed);  // Q rows by TMA here (else the copy warp)
             for (uint32_t h = 0; h < heads; ++h) {
                 for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {  // S phase: Q + K chunk
-                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
-                    uint64_t* bar = &full[r.slot];
+                    dev::mbar_wait_a(ea + 8u * r.slot, r.phase ^ 1u);
+                    const uint32_t bar = fa + 8u * r.slot;
                     if (a.load_only == 3) {  // diagnostics: no loads at all (the consumers alone)
-                        dev::mbar_arrive(bar);
+                        dev::mbar_arrive_a(bar);
                         continue;
                     }
-                    dev::mbar_arrive_expect_tx(bar, kvb + (qtma ? nqh * 128u * LL::PL : 0u));
+                    dev::mbar_arrive_expect_tx_a(bar, kvb + (qtma ? nqh * 128u * LL::PL : 0u));
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (a.fo.y && !fr && h == 0 && ch == 0) {  // fused output: the item's residual rows into L2
                         const uint32_t rb = CC * (a.fo.res_bf16 ? 2u : 4u);
@@ -400,13 +402,13 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                 }
                 for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {  // PV phase: VPS V chunks
                     const uint32_t n = min(VPS, nch - vs * VPS);
-                    dev::mbar_wait(&empty[r.slot], r.phase ^ 1u);
-                    uint64_t* bar = &full[r.slot];
+                    dev::mbar_wait_a(ea + 8u * r.slot, r.phase ^ 1u);
+                    const uint32_t bar = fa + 8u * r.slot;
                     if (a.load_only == 3) {
-                        dev::mbar_arrive(bar);
+                        dev::mbar_arrive_a(bar);
                         continue;
                     }
-                    dev::mbar_arrive_expect_tx(bar, kvb * n);
+                    dev::mbar_arrive_expect_tx_a(bar, kvb * n);
                     const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                     if (fr) {  // the V chunk into the K slot (the copy warp fills the Q slot)
                         load_kv(st + LL::PL * kQT, bar, 2, h, vs);
@@ -445,9 +447,9 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
     if (a.load_only == 1) {  // diagnostics: the producer's feed rate alone
         for (uint32_t item = blockIdx.x; item < a.items; item += gridDim.x)
             for (uint32_t k = 0; k < heads * (nch + nvs); ++k, r.next()) {
-                dev::mbar_wait(&full[r.slot], r.phase);
+                dev::mbar_wait_a(fa + 8u * r.slot, r.phase);
                 __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
+                if (lane == 0) dev::mbar_arrive_a(ea + 8u * r.slot);
             }
         return;
     }
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
 #pragma unroll
                 for (int x = 0; x < NA; ++x) acc[j][x][0] = acc[j][x][1] = acc[j][x][2] = acc[j][x][3] = 0.f;
             for (uint32_t ch = 0; ch < nch; ++ch, r.next()) {
-                dev::mbar_wait(&full[r.slot], r.phase);
+                dev::mbar_wait_a(fa + 8u * r.slot, r.phase);
                 const uint32_t st = sbase + LL::ring + r.slot * LL::ST;
                 const uint32_t vw = min(uint32_t(kDC), dd - ch * kDC);
 #pragma unroll
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     }
                 }
                 __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
+                if (lane == 0) dev::mbar_arrive_a(ea + 8u * r.slot);
             }
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
             }
             constexpr int kPc = (16 * kON + 31) / 32;  // output pieces per lane per chunk
             for (uint32_t vs = 0; vs < nvs; ++vs, r.next()) {
-                dev::mbar_wait(&full[r.slot], r.phase);
+                dev::mbar_wait_a(fa + 8u * r.slot, r.phase);
                 const uint32_t n = min(VPS, nch - vs * VPS);
                 // fused output, bf16 residual: this stage's residual pieces requested up front, so
                 // their latency (L2: the producer prefetched the item's rows) hides under the PV math
@@ -838,7 +840,7 @@ __global__ void __launch_bounds__((CW + 1 + (D > 0)) * 32, CoreLay<NTL, SPLIT, C
                     }
                 }
                 __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&empty[r.slot]);
+                if (lane == 0) dev::mbar_arrive_a(ea + 8u * r.slot);
             }
         }
     }
